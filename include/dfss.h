@@ -1,0 +1,159 @@
+/*
+ * dfss.h -- C ABI of libdfss_sm100a.so, the B200 (sm_100a) DFSS attention path.
+ *
+ * This is the drop-in boundary for the kernel-backend interface of the
+ * reference package nmattn 0.1.0 (backend.kernels(), backend.py:63-67): the
+ * numba kernels _kernels_numba.sddmm_compress / softmax_nonzeros /
+ * spmm_gather are replaced by dfss_sddmm_prune / dfss_softmax_rows /
+ * dfss_spmm, and pipeline.nm_attention (pipeline.py:15-32) by
+ * dfss_nm_attention.  Citations are file:line into /root/reference/pkg/src/nmattn.
+ *
+ * Conventions (all entry points):
+ *   - every pointer argument is DEVICE memory unless stated otherwise; the
+ *     caller allocates every output (the reference kernels return fresh
+ *     arrays, _kernels_numba.py:20,69,95,115; here the host layer allocates);
+ *   - tensors are dense, row-major, batched over a leading "bh" dimension
+ *     (flattened batch x heads); the reference ops have no batch dimension
+ *     (SPEC.md:310), slice h of every argument is one reference call;
+ *   - calls are asynchronous and stream-ordered on `stream` (a cudaStream_t
+ *     passed as void*; NULL = legacy default stream);
+ *   - the return value is a dfss_status; validation failures are reported
+ *     before any launch (the reference validates before dispatch, fused.py:58-82);
+ *   - no global state other than a per-device attribute cache.
+ *
+ * Sparse layouts on the device:
+ *   nonzeros : [bh, rows, cols/2] in the nonzero dtype, row-major -- the
+ *              reference's compressed nonzeros (codec.py:203-216), kept values
+ *              of each group in ascending column order;
+ *   meta_hw  : uint32 words, [bh, ceil(rows/128), ceil(groups/8), 128] where
+ *              groups = cols/group_size.  Word (rb, c, L) with
+ *              L = 16*m2 + 8*k1 + m0 (m0<8, k1<2, m2<8) packs the 4-bit nibbles
+ *              (codec.py:72-76, value lo|hi<<2) of groups 8c+4k1 .. 8c+4k1+3:
+ *              bits [0,16)  from row 128*rb + 16*m2 + m0   (nibble i at bits 4i),
+ *              bits [16,32) from row 128*rb + 16*m2 + 8 + m0.
+ *              This is the tcgen05.mma.sp metadata layout of one 128-lane TMEM
+ *              column, so the SpMM moves words straight into TMEM.  Padding rows /
+ *              groups hold nibble 0x4 with zero nonzeros.
+ *   meta_logical : uint8 per group, [bh, rows, groups] -- the reference's
+ *              LOGICAL metadata stream (codec.py:331-335), one nibble per byte.
+ */
+#ifndef DFSS_H_
+#define DFSS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DFSS_OK = 0,
+  DFSS_ERR_INVALID = -1,      /* argument validation failed (reference: ValueError) */
+  DFSS_ERR_UNSUPPORTED = -2,  /* valid request this build has no kernel for */
+  DFSS_ERR_CUDA = -3,         /* CUDA runtime / driver error (reference: none; host raises RuntimeError) */
+  DFSS_ERR_NO_DEVICE = -4     /* no sm_100 device or driver entry point */
+} dfss_status;
+
+/* group size doubles as the mode id: codec.py:34-50 */
+enum { DFSS_MODE_1_2 = 2, DFSS_MODE_2_4 = 4 };
+
+enum { DFSS_F32 = 0, DFSS_BF16 = 1, DFSS_F16 = 2 };
+
+/* arithmetic for the QK^T contraction */
+enum {
+  DFSS_MATH_AUTO = 0, /* tcgen05 for 16-bit inputs, exact FP32 FFMA for fp32 inputs */
+  DFSS_MATH_FFMA = 1, /* force SIMT FP32 FFMA (any dtype) */
+  DFSS_MATH_TF32 = 2  /* fp32 inputs on tcgen05 kind::tf32 */
+};
+
+/* Words in a meta_hw buffer for [bh, rows, cols] under `mode`. */
+int64_t dfss_meta_hw_words(int mode, int64_t bh, int64_t rows, int64_t cols);
+
+/*
+ * Fused score + prune: replaces _kernels_numba.sddmm_compress
+ * (_kernels_numba.py:110-188) behind fused.sddmm_prune (fused.py:41-96).
+ *   q [bh, n_q, d], k [bh, n_k, d] in `in_dtype`; scores = scale * q k^T
+ *   accumulated in fp32; each group of `mode` consecutive scores of a row is
+ *   pruned by signed value, ties to the lower index (codec.py:104-123),
+ *   AFTER scaling (_kernels_numba.py:140-145).  Writes nonzeros [bh, n_q, n_k/2]
+ *   in `nz_dtype` and meta_hw; never a dense score matrix unless `scores_dbg`
+ *   (nullable, fp32 [bh, n_q, n_k]) is given -- the parity hook that dumps the
+ *   exact post-scale scores the epilogue selected on.
+ *   tile_keep (nullable): uint8 [ceil(n_q/tile_rows), ceil(n_k/tile_cols)] shared by
+ *   all bh -- the BlockMask grid (codec.py:150-200); masked tiles are skipped
+ *   and left as zero nonzeros / nibble 0x4 padding.
+ *   FusedStats (fused.py:22-38) are structural and computed by the host layer
+ *   from the tile grid; dense_elems_written is 0 unless scores_dbg is given.
+ */
+int dfss_sddmm_prune(const void* q, const void* k, void* nonzeros, uint32_t* meta_hw, float scale,
+                     int mode, int in_dtype, int nz_dtype, int math, int64_t bh, int n_q, int n_k, int d,
+                     const uint8_t* tile_keep, int tile_rows, int tile_cols, float* scores_dbg,
+                     void* stream);
+
+/*
+ * Softmax over each row's present nonzeros: replaces
+ * _kernels_numba.softmax_nonzeros (_kernels_numba.py:66-87) behind
+ * sparse_ops.softmax_rows (sparse_ops.py:18-37).  nz_in [bh, rows, nz_cols]
+ * in `in_dtype` -> p_out in `out_dtype` (may alias nz_in when dtypes match).
+ * tile_keep/tile_rows/tile_cols: optional BlockMask grid in DENSE columns
+ * (present nonzero j of row i <=> keep[i/tile_rows][2j/tile_cols]).
+ * err_row (nullable, device int32[2], caller-initialised to INT32_MAX):
+ * err_row[0] = 1 + first empty flattened row (bh*rows + row), err_row[1] =
+ * 1 + first flattened row holding a NaN (sparse_ops.py:27-32); the host layer
+ * turns them into the reference's ValueErrors.
+ */
+int dfss_softmax_rows(const void* nz_in, void* p_out, int in_dtype, int out_dtype, int64_t bh, int rows,
+                      int nz_cols, const uint8_t* tile_keep, int tile_rows, int tile_cols, int32_t* err_row,
+                      void* stream);
+
+/*
+ * Compressed SpMM out = decompress(P) . V: replaces _kernels_numba.spmm_gather
+ * (_kernels_numba.py:91-103) behind sparse_ops.spmm (sparse_ops.py:40-68).
+ *   p [bh, rows, n_k/2] in `p_dtype`, meta_hw for [bh, rows, n_k],
+ *   v [bh, n_k, d] in `v_dtype`, out [bh, rows, d] in `out_dtype`, fp32 accumulation.
+ *   16-bit P and V on aligned shapes run tcgen05.mma.sp with the metadata
+ *   consumed straight from meta_hw; otherwise an FP32 FFMA gather kernel.
+ *   tile_keep: optional BlockMask grid (masked tiles contribute zero).
+ */
+int dfss_spmm(const void* p, const uint32_t* meta_hw, const void* v, void* out, int mode, int p_dtype,
+              int v_dtype, int out_dtype, int64_t bh, int rows, int n_k, int d, const uint8_t* tile_keep,
+              int tile_rows, int tile_cols, void* stream);
+
+/*
+ * End-to-end DFSS attention: replaces pipeline.nm_attention (pipeline.py:15-32)
+ * for [bh, n, d] q/k/v in `dtype`, scale = 1/sqrt(d) (fused.py:110).
+ *   out [bh, n, d] in `dtype`.  `workspace` (device) must hold
+ *   dfss_nm_attention_workspace_bytes(...) bytes for the compressed P and meta.
+ */
+int64_t dfss_nm_attention_workspace_bytes(int mode, int dtype, int64_t bh, int n, int d);
+int dfss_nm_attention(const void* q, const void* k, const void* v, void* out, int mode, int dtype, int math,
+                      int64_t bh, int n, int d, void* workspace, int64_t workspace_bytes, void* stream);
+
+/*
+ * Parity hook: prune a given fp32 score tensor with the SAME device selection
+ * routine the SDDMM epilogue uses (codec._select_rows, codec.py:289-313).
+ *   scores [rows, cols] fp32 -> nonzeros [rows, cols/2] (nz_dtype),
+ *   meta_logical uint8 [rows, cols/gs], kept uint8 [rows, cols] (prune_dense mask,
+ *   codec.py:324-328).  Any output pointer may be NULL.
+ */
+int dfss_prune_scores(const float* scores, void* nonzeros, uint8_t* meta_logical, uint8_t* kept, int mode,
+                      int nz_dtype, int64_t rows, int cols, void* stream);
+
+/* meta_hw <-> LOGICAL nibble stream (one nibble per byte), [bh, rows, cols/gs]. */
+int dfss_meta_hw_to_logical(const uint32_t* meta_hw, uint8_t* meta_logical, int mode, int64_t bh, int rows,
+                            int cols, void* stream);
+int dfss_meta_logical_to_hw(const uint8_t* meta_logical, uint32_t* meta_hw, int mode, int64_t bh, int rows,
+                            int cols, void* stream);
+
+/* Human-readable status; last CUDA error text for DFSS_ERR_CUDA. Never NULL. */
+const char* dfss_status_string(int status);
+const char* dfss_last_error(void);
+/* 1 if the tcgen05 path can run on the current device (sm_100), else 0. */
+int dfss_has_tcgen05(void);
+int dfss_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DFSS_H_ */

@@ -1,0 +1,181 @@
+// capi.cu -- extern "C" entry points of libdfss_sm100a.so (include/dfss.h).
+//
+// Validation happens here, before any launch, mirroring the reference's
+// wrappers (fused.py:58-82, sparse_ops.py:25-32,50-64); dispatch picks the
+// tcgen05 kernels for 16-bit inputs on shapes they tile and the FP32 FFMA
+// kernels otherwise.  There is no CPU path.
+#include <stdio.h>
+
+#include <string>
+
+#include "dfss_common.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int status, const char* what) {
+  g_last_error = what;
+  return status;
+}
+
+int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return DFSS_OK;
+  g_last_error = std::string(cudaGetErrorName(e)) + ": " + cudaGetErrorString(e);
+  return DFSS_ERR_CUDA;
+}
+
+bool valid_mode(int mode) { return mode == DFSS_MODE_1_2 || mode == DFSS_MODE_2_4; }
+bool valid_dtype(int dt) { return dt == DFSS_F32 || dt == DFSS_BF16 || dt == DFSS_F16; }
+
+int check_keep(const uint8_t* keep, int tile_rows, int tile_cols, int gs) {
+  if (!keep) return DFSS_OK;
+  if (tile_rows < 1 || tile_cols < 1) return fail(DFSS_ERR_INVALID, "tile dimensions must be >= 1");
+  if (tile_cols % gs != 0) return fail(DFSS_ERR_INVALID, "tile columns not divisible by the group size");
+  return DFSS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dfss_version(void) { return 100; }
+
+const char* dfss_status_string(int status) {
+  switch (status) {
+    case DFSS_OK: return "ok";
+    case DFSS_ERR_INVALID: return "invalid argument";
+    case DFSS_ERR_UNSUPPORTED: return "unsupported configuration";
+    case DFSS_ERR_CUDA: return "CUDA error";
+    case DFSS_ERR_NO_DEVICE: return "no sm_100 device";
+    default: return "unknown status";
+  }
+}
+
+const char* dfss_last_error(void) { return g_last_error.c_str(); }
+
+int dfss_has_tcgen05(void) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) return 0;
+  return (major == 10 && minor == 0) ? 1 : 0;
+}
+
+int64_t dfss_meta_hw_words(int mode, int64_t bh, int64_t rows, int64_t cols) {
+  if (!valid_mode(mode) || rows < 0 || cols < 0 || bh < 0) return -1;
+  dfss::MetaGeom geo((int)rows, (int)(cols / mode));
+  return bh * geo.words_per_bh();
+}
+
+int dfss_sddmm_prune(const void* q, const void* k, void* nonzeros, uint32_t* meta_hw, float scale, int mode,
+                     int in_dtype, int nz_dtype, int math, int64_t bh, int n_q, int n_k, int d,
+                     const uint8_t* tile_keep, int tile_rows, int tile_cols, float* scores_dbg, void* stream) {
+  if (!valid_mode(mode)) return fail(DFSS_ERR_INVALID, "unknown sparsity mode (expected 2 or 4)");
+  if (!valid_dtype(in_dtype) || !valid_dtype(nz_dtype)) return fail(DFSS_ERR_INVALID, "unknown dtype");
+  if (bh < 0 || n_q < 1 || n_k < 1 || d < 1) return fail(DFSS_ERR_INVALID, "shape dimensions must be positive");
+  if (n_k % mode != 0) return fail(DFSS_ERR_INVALID, "score columns not group-aligned for the mode");
+  if (int st = check_keep(tile_keep, tile_rows, tile_cols, mode)) return st;
+  if (!q || !k || !nonzeros || !meta_hw) return fail(DFSS_ERR_INVALID, "null tensor pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool tc_ok = !tile_keep && dfss::tc_sddmm_supported(mode, in_dtype, nz_dtype, n_q, n_k, d) &&
+                     dfss_has_tcgen05();
+  if (math == DFSS_MATH_TF32) {
+    if (in_dtype != DFSS_F32 || !tc_ok) return fail(DFSS_ERR_UNSUPPORTED, "tf32 path needs fp32 inputs on a tiled shape");
+    return cuda_status(dfss::launch_sddmm_tc(q, k, nonzeros, meta_hw, scale, mode, in_dtype, bh, n_q, n_k, d,
+                                             scores_dbg, s));
+  }
+  if (math == DFSS_MATH_AUTO && in_dtype != DFSS_F32 && tc_ok)
+    return cuda_status(dfss::launch_sddmm_tc(q, k, nonzeros, meta_hw, scale, mode, in_dtype, bh, n_q, n_k, d,
+                                             scores_dbg, s));
+  return cuda_status(dfss::launch_sddmm_simt(q, k, nonzeros, meta_hw, scale, mode, in_dtype, nz_dtype, bh, n_q, n_k,
+                                             d, tile_keep, tile_rows, tile_cols, scores_dbg, s));
+}
+
+int dfss_softmax_rows(const void* nz_in, void* p_out, int in_dtype, int out_dtype, int64_t bh, int rows, int nz_cols,
+                      const uint8_t* tile_keep, int tile_rows, int tile_cols, int32_t* err_row, void* stream) {
+  if (!valid_dtype(in_dtype) || !valid_dtype(out_dtype)) return fail(DFSS_ERR_INVALID, "unknown dtype");
+  if (bh < 0 || rows < 1 || nz_cols < 1) return fail(DFSS_ERR_INVALID, "shape dimensions must be positive");
+  if (tile_keep && (tile_rows < 1 || tile_cols < 2 || tile_cols % 2))
+    return fail(DFSS_ERR_INVALID, "tile_cols must be even to map tiles onto nonzeros");
+  if (nz_in == p_out && in_dtype != out_dtype) return fail(DFSS_ERR_INVALID, "in-place softmax needs equal dtypes");
+  if (!nz_in || !p_out) return fail(DFSS_ERR_INVALID, "null tensor pointer");
+  return cuda_status(dfss::launch_softmax(nz_in, p_out, in_dtype, out_dtype, bh, rows, nz_cols, tile_keep, tile_rows,
+                                          tile_cols, err_row, (cudaStream_t)stream));
+}
+
+int dfss_spmm(const void* p, const uint32_t* meta_hw, const void* v, void* out, int mode, int p_dtype, int v_dtype,
+              int out_dtype, int64_t bh, int rows, int n_k, int d, const uint8_t* tile_keep, int tile_rows,
+              int tile_cols, void* stream) {
+  if (!valid_mode(mode)) return fail(DFSS_ERR_INVALID, "unknown sparsity mode (expected 2 or 4)");
+  if (!valid_dtype(p_dtype) || !valid_dtype(v_dtype) || !valid_dtype(out_dtype))
+    return fail(DFSS_ERR_INVALID, "unknown dtype");
+  if (bh < 0 || rows < 1 || n_k < 1 || d < 1) return fail(DFSS_ERR_INVALID, "shape dimensions must be positive");
+  if (n_k % mode != 0) return fail(DFSS_ERR_INVALID, "dense columns not divisible by the group size");
+  if (int st = check_keep(tile_keep, tile_rows, tile_cols, mode)) return st;
+  if (!p || !meta_hw || !v || !out) return fail(DFSS_ERR_INVALID, "null tensor pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!tile_keep && dfss::tc_spmm_supported(mode, p_dtype, v_dtype, out_dtype, rows, n_k, d) && dfss_has_tcgen05())
+    return cuda_status(dfss::launch_spmm_tc(p, meta_hw, v, out, mode, p_dtype, out_dtype, bh, rows, n_k, d, s));
+  if (d > 256) return fail(DFSS_ERR_UNSUPPORTED, "head dim > 256 not supported by the FFMA SpMM");
+  return cuda_status(dfss::launch_spmm_simt(p, meta_hw, v, out, mode, p_dtype, v_dtype, out_dtype, bh, rows, n_k, d,
+                                            tile_keep, tile_rows, tile_cols, s));
+}
+
+int64_t dfss_nm_attention_workspace_bytes(int mode, int dtype, int64_t bh, int n, int d) {
+  (void)d;
+  if (!valid_mode(mode) || !valid_dtype(dtype) || bh < 0 || n < 1) return -1;
+  const int64_t nz = bh * (int64_t)n * (n / 2) * dfss::dtype_bytes(dtype);
+  const int64_t nz_aligned = (nz + 255) / 256 * 256;
+  return nz_aligned + dfss_meta_hw_words(mode, bh, n, n) * 4 + 256;
+}
+
+int dfss_nm_attention(const void* q, const void* k, const void* v, void* out, int mode, int dtype, int math,
+                      int64_t bh, int n, int d, void* workspace, int64_t workspace_bytes, void* stream) {
+  if (!valid_mode(mode)) return fail(DFSS_ERR_INVALID, "unknown sparsity mode (expected 2 or 4)");
+  if (!valid_dtype(dtype)) return fail(DFSS_ERR_INVALID, "unknown dtype");
+  if (bh < 0 || n < 1 || d < 1) return fail(DFSS_ERR_INVALID, "shape dimensions must be positive");
+  if (n % mode != 0) return fail(DFSS_ERR_INVALID, "sequence length not group-aligned for the mode");
+  const int64_t need = dfss_nm_attention_workspace_bytes(mode, dtype, bh, n, d);
+  if (!workspace || workspace_bytes < need) return fail(DFSS_ERR_INVALID, "workspace too small");
+  if (bh == 0) return DFSS_OK;
+  const int64_t nz_bytes = bh * (int64_t)n * (n / 2) * dfss::dtype_bytes(dtype);
+  char* ws = (char*)workspace;
+  void* nz = ws;
+  uint32_t* meta = (uint32_t*)(ws + (nz_bytes + 255) / 256 * 256);
+  const float scale = 1.0f / sqrtf((float)d);
+  int st = dfss_sddmm_prune(q, k, nz, meta, scale, mode, dtype, dtype, math, bh, n, n, d, nullptr, 0, 0, nullptr,
+                            stream);
+  if (st) return st;
+  st = dfss_softmax_rows(nz, nz, dtype, dtype, bh, n, n / 2, nullptr, 0, 0, nullptr, stream);
+  if (st) return st;
+  return dfss_spmm(nz, meta, v, out, mode, dtype, dtype, dtype, bh, n, n, d, nullptr, 0, 0, stream);
+}
+
+int dfss_prune_scores(const float* scores, void* nonzeros, uint8_t* meta_logical, uint8_t* kept, int mode,
+                      int nz_dtype, int64_t rows, int cols, void* stream) {
+  if (!valid_mode(mode)) return fail(DFSS_ERR_INVALID, "unknown sparsity mode (expected 2 or 4)");
+  if (!valid_dtype(nz_dtype)) return fail(DFSS_ERR_INVALID, "unknown dtype");
+  if (rows < 0 || cols < 0 || cols % mode) return fail(DFSS_ERR_INVALID, "column count not divisible by group size");
+  if (!scores) return fail(DFSS_ERR_INVALID, "null tensor pointer");
+  return cuda_status(
+      dfss::launch_prune_scores(scores, nonzeros, meta_logical, kept, mode, nz_dtype, rows, cols, (cudaStream_t)stream));
+}
+
+int dfss_meta_hw_to_logical(const uint32_t* meta_hw, uint8_t* meta_logical, int mode, int64_t bh, int rows, int cols,
+                            void* stream) {
+  if (!valid_mode(mode) || rows < 0 || cols < 0 || cols % mode || bh < 0)
+    return fail(DFSS_ERR_INVALID, "invalid metadata geometry");
+  if (!meta_hw || !meta_logical) return fail(DFSS_ERR_INVALID, "null tensor pointer");
+  return cuda_status(dfss::launch_meta_hw_to_logical(meta_hw, meta_logical, mode, bh, rows, cols, (cudaStream_t)stream));
+}
+
+int dfss_meta_logical_to_hw(const uint8_t* meta_logical, uint32_t* meta_hw, int mode, int64_t bh, int rows, int cols,
+                            void* stream) {
+  if (!valid_mode(mode) || rows < 0 || cols < 0 || cols % mode || bh < 0)
+    return fail(DFSS_ERR_INVALID, "invalid metadata geometry");
+  if (!meta_hw || !meta_logical) return fail(DFSS_ERR_INVALID, "null tensor pointer");
+  return cuda_status(dfss::launch_meta_logical_to_hw(meta_logical, meta_hw, mode, bh, rows, cols, (cudaStream_t)stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,157 @@
+// dfss_common.cuh -- shared device helpers for the DFSS sm_100a kernels:
+// dtype conversion, the N:M selection rule, and the meta_hw word layout.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/dfss.h"
+
+namespace dfss {
+
+// ----------------------------------------------------------------------------
+// dtype helpers
+
+template <typename T>
+struct DT;
+template <>
+struct DT<float> {
+  static constexpr int id = DFSS_F32;
+  __device__ __forceinline__ static float to_f(float x) { return x; }
+  __device__ __forceinline__ static float from_f(float x) { return x; }
+};
+template <>
+struct DT<__nv_bfloat16> {
+  static constexpr int id = DFSS_BF16;
+  __device__ __forceinline__ static float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+  __device__ __forceinline__ static __nv_bfloat16 from_f(float x) { return __float2bfloat16_rn(x); }
+};
+template <>
+struct DT<__half> {
+  static constexpr int id = DFSS_F16;
+  __device__ __forceinline__ static float to_f(__half x) { return __half2float(x); }
+  __device__ __forceinline__ static __half from_f(float x) { return __float2half_rn(x); }
+};
+
+inline int dtype_bytes(int dtype) { return dtype == DFSS_F32 ? 4 : 2; }
+
+// ----------------------------------------------------------------------------
+// N:M selection (codec.py:104-123, codec.py:289-313, _kernels_numba.py:145-184).
+//
+// Signed-value order with ties to the lower index.  2:4 uses the rank rule
+//   rank_i = #{j : v_j > v_i} + #{j < i : v_j == v_i},  keep iff rank_i < 2,
+// which is exactly "first two entries of a stable descending argsort"
+// (codec.py:121) and the numba first-strict-max loops (:165-176).  Never the
+// paper's pair-sum rule, which differs under fp32 ties.
+
+// Nibble (lo | hi << 2) for each 4-bit kept mask with two bits set.
+// mask 0b0011 -> 0x4, 0b0101 -> 0x8, 0b1001 -> 0xC, 0b0110 -> 0x9, 0b1010 -> 0xD, 0b1100 -> 0xE.
+__device__ __forceinline__ uint32_t nibble_of_mask(uint32_t mask) {
+  constexpr unsigned long long kTable = (0x4ull << (4 * 3)) | (0x8ull << (4 * 5)) | (0xCull << (4 * 9)) |
+                                        (0x9ull << (4 * 6)) | (0xDull << (4 * 10)) | (0xEull << (4 * 12));
+  return (uint32_t)(kTable >> (4 * mask)) & 0xFu;
+}
+
+// 2:4 select: returns the nibble, writes the kept values in ascending column order.
+//
+// Tournament form of the rank rule under the total order "i beats j iff
+// v_i > v_j, or v_i == v_j and i < j": the pair winners w01 / w23 and losers
+// l01 / l23 decide everything.  {0,1} survive iff l01 beats w23, {2,3} iff l23
+// beats w01, otherwise {w01, w23}.  Every comparison puts the lower index on
+// the left of >= (or the higher on the left of >), so ties resolve exactly as
+// the reference's stable argsort.  4 compares + 8 selects, no pair sums.
+__device__ __forceinline__ uint32_t select24(float v0, float v1, float v2, float v3, float& lo, float& hi) {
+  const bool a = v0 >= v1;  // element 0 beats element 1
+  const bool b = v2 >= v3;  // element 2 beats element 3
+  const float w01 = a ? v0 : v1, l01 = a ? v1 : v0;
+  const float w23 = b ? v2 : v3, l23 = b ? v3 : v2;
+  const bool keep01 = l01 >= w23;  // lower-index loser vs higher-index winner
+  const bool keep23 = l23 > w01;   // higher-index loser must strictly beat the winner
+  lo = keep01 ? v0 : (keep23 ? v2 : w01);
+  hi = keep01 ? v1 : (keep23 ? v3 : w23);
+  const uint32_t mixed = (a ? 0u : 1u) | (b ? 8u : 12u);  // (w01 idx) | (w23 idx) << 2
+  return keep01 ? 0x4u : (keep23 ? 0xEu : mixed);
+}
+
+// Reference rank rule (codec.py:121, kept for the self-check kernel in tests).
+__device__ __forceinline__ uint32_t select24_rank(float v0, float v1, float v2, float v3) {
+  const int r0 = (v1 > v0) + (v2 > v0) + (v3 > v0);
+  const int r1 = (v0 >= v1) + (v2 > v1) + (v3 > v1);
+  const int r2 = (v0 >= v2) + (v1 >= v2) + (v3 > v2);
+  const int r3 = (v0 >= v3) + (v1 >= v3) + (v2 >= v3);
+  return nibble_of_mask((uint32_t)(r0 < 2) | ((uint32_t)(r1 < 2) << 1) | ((uint32_t)(r2 < 2) << 2) |
+                        ((uint32_t)(r3 < 2) << 3));
+}
+
+// 1:2 select: element 1 survives iff v1 > v0 (codec.py:114-117); 0x4 / 0xE.
+__device__ __forceinline__ uint32_t select12(float v0, float v1, float& kept) {
+  const bool second = v1 > v0;
+  kept = second ? v1 : v0;
+  return second ? 0xEu : 0x4u;
+}
+
+// Kept mask bits (bit i = element i of the group kept) from a nibble.
+__device__ __forceinline__ uint32_t kept_bits(uint32_t nib, int gs) {
+  if (gs == 2) return nib == 0xEu ? 2u : 1u;
+  return (1u << (nib & 3u)) | (1u << ((nib >> 2) & 3u));
+}
+
+// ----------------------------------------------------------------------------
+// meta_hw layout (dfss.h): words [bh][ceil(rows/128)][ceil(groups/8)][128].
+
+constexpr uint32_t kPadNibble = 0x4u;
+
+struct MetaGeom {
+  int rows, groups;   // logical
+  int rblocks, chunks;  // ceil(rows/128), ceil(groups/8)
+  __host__ __device__ MetaGeom(int rows_, int groups_)
+      : rows(rows_), groups(groups_), rblocks((rows_ + 127) / 128), chunks((groups_ + 7) / 8) {}
+  __host__ __device__ int64_t words_per_bh() const { return (int64_t)rblocks * chunks * 128; }
+  // word index (within one bh) and bit shift of the nibble of (row, group)
+  __device__ __forceinline__ int64_t word_of(int row, int group, int& shift) const {
+    const int rb = row >> 7, rr = row & 127;
+    const int m2 = rr >> 4, m1 = (rr >> 3) & 1, m0 = rr & 7;
+    const int c = group >> 3, gi = group & 7, k1 = gi >> 2, slot = gi & 3;
+    shift = 16 * m1 + 4 * slot;
+    return ((int64_t)rb * chunks + c) * 128 + (16 * m2 + 8 * k1 + m0);
+  }
+  // inverse: (rb, c, lane, nibble index 0..7 in the word) -> row, group
+  __device__ __forceinline__ static void coords_of(int rb, int c, int lane, int idx, int& row, int& group) {
+    const int m2 = lane >> 4, k1 = (lane >> 3) & 1, m0 = lane & 7;
+    const int m1 = idx >> 2, slot = idx & 3;
+    row = rb * 128 + 16 * m2 + 8 * m1 + m0;
+    group = c * 8 + 4 * k1 + slot;
+  }
+};
+
+}  // namespace dfss
+
+// ----------------------------------------------------------------------------
+// internal launchers (implemented in the .cu files, dispatched from capi.cu)
+
+namespace dfss {
+cudaError_t launch_sddmm_simt(const void* q, const void* k, void* nz, uint32_t* meta, float scale, int gs,
+                              int in_dtype, int nz_dtype, int64_t bh, int n, int m, int d, const uint8_t* keep,
+                              int tile_rows, int tile_cols, float* dbg, cudaStream_t s);
+cudaError_t launch_softmax(const void* in, void* out, int in_dtype, int out_dtype, int64_t bh, int rows,
+                           int cols, const uint8_t* keep, int tile_rows, int tile_cols, int32_t* err,
+                           cudaStream_t s);
+cudaError_t launch_spmm_simt(const void* p, const uint32_t* meta, const void* v, void* out, int gs, int p_dtype,
+                             int v_dtype, int out_dtype, int64_t bh, int rows, int n_k, int d, const uint8_t* keep,
+                             int tile_rows, int tile_cols, cudaStream_t s);
+cudaError_t launch_prune_scores(const float* scores, void* nz, uint8_t* meta, uint8_t* kept, int gs, int nz_dtype,
+                                int64_t rows, int cols, cudaStream_t s);
+cudaError_t launch_meta_hw_to_logical(const uint32_t* hw, uint8_t* logical, int gs, int64_t bh, int rows, int cols,
+                                      cudaStream_t s);
+cudaError_t launch_meta_logical_to_hw(const uint8_t* logical, uint32_t* hw, int gs, int64_t bh, int rows, int cols,
+                                      cudaStream_t s);
+// tcgen05 paths: return cudaErrorNotSupported when the shape is not covered.
+cudaError_t launch_sddmm_tc(const void* q, const void* k, void* nz, uint32_t* meta, float scale, int gs,
+                            int in_dtype, int64_t bh, int n, int m, int d, float* dbg, cudaStream_t s);
+cudaError_t launch_spmm_tc(const void* p, const uint32_t* meta, const void* v, void* out, int gs, int dtype,
+                           int out_dtype, int64_t bh, int rows, int n_k, int d, cudaStream_t s);
+bool tc_sddmm_supported(int gs, int in_dtype, int nz_dtype, int n, int m, int d);
+bool tc_spmm_supported(int gs, int p_dtype, int v_dtype, int out_dtype, int rows, int n_k, int d);
+}  // namespace dfss

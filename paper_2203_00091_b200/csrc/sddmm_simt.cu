@@ -1,0 +1,176 @@
+// sddmm_simt.cu -- generic fused score + N:M prune on FP32 FFMA.
+//
+// The exact-FP32 path (fp32 inputs at the 1e-5 tolerance, where TF32 tensor
+// cores would round the inputs to a 10-bit mantissa) and the fallback for
+// shapes the tcgen05 kernel does not tile (ragged n, odd d, block masks).
+// Same epilogue semantics as the tcgen05 kernel and as the reference
+// _sddmm_compress (_kernels_numba.py:110-185): scale, then select by signed
+// value with ties to the lower index, then write nonzeros + nibbles only.
+#include "dfss_common.cuh"
+
+namespace dfss {
+
+namespace {
+constexpr int BM = 64, BN = 64, BK = 32;
+}
+
+// grid: (ceil(m/64), 2*ceil(n/128), bh); 256 threads, each a 4x4 score block:
+// rows ty + 16*i, columns 4*tx .. 4*tx+3 (one 2:4 group, two 1:2 groups).
+template <typename TIn, typename TNz, int GS>
+__global__ void __launch_bounds__(256) sddmm_simt_kernel(const TIn* __restrict__ q, const TIn* __restrict__ k,
+                                                         TNz* __restrict__ nz, uint32_t* __restrict__ meta,
+                                                         float scale, int n, int m, int d,
+                                                         const uint8_t* __restrict__ keep, int tile_rows,
+                                                         int tile_cols, float* __restrict__ dbg, MetaGeom geo) {
+  __shared__ float Qs[BK][BM + 1];
+  __shared__ __align__(16) float Ks[BK][BN + 4];
+  __shared__ uint8_t nibs[BM][BN / GS];
+
+  const int b = blockIdx.z;
+  const int row0 = blockIdx.y * BM, col0 = blockIdx.x * BN;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  q += (int64_t)b * n * d;
+  k += (int64_t)b * m * d;
+  nz += (int64_t)b * n * (m / 2);
+  meta += (int64_t)b * geo.words_per_bh();
+  if (dbg) dbg += (int64_t)b * n * m;
+  const int grid_cols = keep ? (m + tile_cols - 1) / tile_cols : 0;
+
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+  if (row0 < n) {
+    for (int k0 = 0; k0 < d; k0 += BK) {
+      for (int i = threadIdx.x; i < BM * BK; i += 256) {
+        const int r = i / BK, kk = i % BK;
+        const int gr = row0 + r, gk = k0 + kk;
+        Qs[kk][r] = (gr < n && gk < d) ? DT<TIn>::to_f(q[(int64_t)gr * d + gk]) : 0.f;
+        const int gc = col0 + r;
+        Ks[kk][r] = (gc < m && gk < d) ? DT<TIn>::to_f(k[(int64_t)gc * d + gk]) : 0.f;
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int kk = 0; kk < BK; ++kk) {
+        const float4 bv = *reinterpret_cast<const float4*>(&Ks[kk][4 * tx]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float a = Qs[kk][ty + 16 * i];
+          acc[i][0] = fmaf(a, bv.x, acc[i][0]);
+          acc[i][1] = fmaf(a, bv.y, acc[i][1]);
+          acc[i][2] = fmaf(a, bv.z, acc[i][2]);
+          acc[i][3] = fmaf(a, bv.w, acc[i][3]);
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- prune/encode epilogue: nonzeros and nibbles leave, dense scores never do
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int lr = ty + 16 * i;
+    const int row = row0 + lr;
+    const int c0 = col0 + 4 * tx;
+    float v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = acc[i][j] * scale;
+    const bool row_ok = row < n;
+    if (dbg && row_ok) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (c0 + j < m) dbg[(int64_t)row * m + c0 + j] = v[j];
+    }
+#pragma unroll
+    for (int h = 0; h < 4 / GS; ++h) {
+      const int c = c0 + GS * h;  // first dense column of this group
+      uint32_t nib = kPadNibble;
+      if (row_ok && c < m) {
+        const bool kept_tile = !keep || keep[(row / tile_rows) * grid_cols + c / tile_cols];
+        const int g = c / GS;
+        if (GS == 4) {
+          float lo = 0.f, hi = 0.f;
+          if (kept_tile) nib = select24(v[0], v[1], v[2], v[3], lo, hi);
+          nz[(int64_t)row * (m / 2) + 2 * g] = DT<TNz>::from_f(lo);
+          nz[(int64_t)row * (m / 2) + 2 * g + 1] = DT<TNz>::from_f(hi);
+        } else {
+          float kv = 0.f;
+          if (kept_tile) nib = select12(v[2 * h], v[2 * h + 1], kv);
+          nz[(int64_t)row * (m / 2) + g] = DT<TNz>::from_f(kv);
+        }
+      }
+      nibs[lr][(4 / GS) * tx + h] = (uint8_t)nib;
+    }
+  }
+  __syncthreads();
+
+  // ---- assemble meta_hw words for the 64 lanes this row half covers
+  constexpr int kChunks = BN / (8 * GS);  // chunks of 8 groups inside the tile
+  const int rb = row0 >> 7, half = (row0 >> 6) & 1;
+  const int c_base = col0 / (8 * GS);
+  if (threadIdx.x < kChunks * 64) {
+    const int cl = threadIdx.x >> 6;
+    const int lane = 64 * half + (threadIdx.x & 63);
+    const int c = c_base + cl;
+    if (c < geo.chunks) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int idx = 0; idx < 8; ++idx) {
+        int row, group;
+        MetaGeom::coords_of(rb, c, lane, idx, row, group);
+        const uint32_t nib = nibs[row - row0][group - col0 / GS];
+        word |= nib << (16 * (idx >> 2) + 4 * (idx & 3));
+      }
+      meta[((int64_t)rb * geo.chunks + c) * 128 + lane] = word;
+    }
+  }
+}
+
+template <typename TIn, typename TNz>
+static cudaError_t sddmm_simt_typed(const void* q, const void* k, void* nz, uint32_t* meta, float scale, int gs,
+                                    int64_t bh, int n, int m, int d, const uint8_t* keep, int tile_rows,
+                                    int tile_cols, float* dbg, cudaStream_t s) {
+  MetaGeom geo(n, m / gs);
+  dim3 grid((m + BN - 1) / BN, 2 * geo.rblocks, (unsigned)bh);
+  if (gs == 4)
+    sddmm_simt_kernel<TIn, TNz, 4><<<grid, 256, 0, s>>>((const TIn*)q, (const TIn*)k, (TNz*)nz, meta, scale, n, m, d,
+                                                        keep, tile_rows, tile_cols, dbg, geo);
+  else
+    sddmm_simt_kernel<TIn, TNz, 2><<<grid, 256, 0, s>>>((const TIn*)q, (const TIn*)k, (TNz*)nz, meta, scale, n, m, d,
+                                                        keep, tile_rows, tile_cols, dbg, geo);
+  return cudaGetLastError();
+}
+
+template <typename TIn>
+static cudaError_t sddmm_simt_in(const void* q, const void* k, void* nz, uint32_t* meta, float scale, int gs,
+                                 int nz_dtype, int64_t bh, int n, int m, int d, const uint8_t* keep, int tile_rows,
+                                 int tile_cols, float* dbg, cudaStream_t s) {
+  switch (nz_dtype) {
+    case DFSS_F32:
+      return sddmm_simt_typed<TIn, float>(q, k, nz, meta, scale, gs, bh, n, m, d, keep, tile_rows, tile_cols, dbg, s);
+    case DFSS_BF16:
+      return sddmm_simt_typed<TIn, __nv_bfloat16>(q, k, nz, meta, scale, gs, bh, n, m, d, keep, tile_rows, tile_cols,
+                                                  dbg, s);
+    default:
+      return sddmm_simt_typed<TIn, __half>(q, k, nz, meta, scale, gs, bh, n, m, d, keep, tile_rows, tile_cols, dbg, s);
+  }
+}
+
+cudaError_t launch_sddmm_simt(const void* q, const void* k, void* nz, uint32_t* meta, float scale, int gs,
+                              int in_dtype, int nz_dtype, int64_t bh, int n, int m, int d, const uint8_t* keep,
+                              int tile_rows, int tile_cols, float* dbg, cudaStream_t s) {
+  if (bh == 0 || n == 0 || m == 0) return cudaSuccess;
+  switch (in_dtype) {
+    case DFSS_F32:
+      return sddmm_simt_in<float>(q, k, nz, meta, scale, gs, nz_dtype, bh, n, m, d, keep, tile_rows, tile_cols, dbg, s);
+    case DFSS_BF16:
+      return sddmm_simt_in<__nv_bfloat16>(q, k, nz, meta, scale, gs, nz_dtype, bh, n, m, d, keep, tile_rows, tile_cols,
+                                          dbg, s);
+    default:
+      return sddmm_simt_in<__half>(q, k, nz, meta, scale, gs, nz_dtype, bh, n, m, d, keep, tile_rows, tile_cols, dbg, s);
+  }
+}
+
+}  // namespace dfss

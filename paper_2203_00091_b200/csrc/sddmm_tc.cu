@@ -1,0 +1,293 @@
+// sddmm_tc.cu -- fused Q.K^T + 2:4 prune on tcgen05 (bf16 / fp16, head dim 64).
+//
+// Replaces _sddmm_compress (_kernels_numba.py:110-185) for the 16-bit
+// configurations.  Persistent, warp-specialised, one CTA per SM:
+//   warp 0      TMA producer: Q tile (128 x 64) once per work item, K tiles
+//               (256 x 64) through a KSTAGES-deep mbarrier ring;
+//   warp 1      MMA issuer: 4 x tcgen05.mma.kind::f16 (M=128, N=256, K=16) per
+//               K tile into one of two TMEM accumulators (2 x 256 columns);
+//   warp 2      TMEM allocator;
+//   warps 4-11  epilogue: warp w reads TMEM lanes 32*(w%4).. (its 32 query rows)
+//               and one 128-column half of the accumulator, scales, selects
+//               2-of-4 in registers (select24, the same routine as the parity
+//               hook), packs the kept pair to 16-bit, stages the nonzeros in
+//               128B-swizzled smem for a TMA store, and writes the metadata
+//               words of its lanes straight to meta_hw (coalesced 128 B).
+// No dense score ever leaves the SM unless the debug dump is requested.
+// Work item = (bh, 128-row block); items are strided over the persistent CTAs.
+#include <stdio.h>
+
+#include <type_traits>
+
+#include "dfss_common.cuh"
+#include "tc_common.cuh"
+
+namespace dfss {
+
+namespace {
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int HD = 64;
+constexpr int KSTAGES = 3;
+constexpr int NACC = 2;
+constexpr int EPI_WARPS = 8;
+constexpr int NUM_THREADS = (4 + EPI_WARPS) * 32;
+constexpr int Q_BYTES = BM * HD * 2;
+constexpr int K_BYTES = BN * HD * 2;
+constexpr int STG_BYTES = 32 * 128;  // 32 rows x 64 nonzeros x 2 B
+constexpr int SMEM_Q = 0;
+constexpr int SMEM_K = SMEM_Q + 2 * Q_BYTES;
+constexpr int SMEM_STG = SMEM_K + KSTAGES * K_BYTES;
+constexpr int SMEM_BAR = SMEM_STG + EPI_WARPS * 2 * STG_BYTES;
+constexpr int SMEM_TOTAL = SMEM_BAR + 256 + 1024;  // + barriers + alignment slack
+}  // namespace
+
+template <typename T>
+__device__ __forceinline__ uint32_t pack2(float lo, float hi);
+template <>
+__device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float lo, float hi) {
+  __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&p);
+}
+template <>
+__device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) {
+  __half2 p = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&p);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    sddmm24_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                      const __grid_constant__ CUtensorMap tm_nz, uint32_t* __restrict__ meta, float scale, int bh,
+                      int n, int m, float* __restrict__ dbg) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = (uint64_t*)(smem + SMEM_BAR);
+  uint64_t* q_full = bars;                 // [2]
+  uint64_t* q_empty = bars + 2;            // [2]
+  uint64_t* k_full = bars + 4;             // [KSTAGES]
+  uint64_t* k_empty = k_full + KSTAGES;    // [KSTAGES]
+  uint64_t* t_full = k_empty + KSTAGES;    // [NACC]
+  uint64_t* t_empty = t_full + NACC;       // [NACC]
+  uint32_t* tmem_slot = (uint32_t*)(t_empty + NACC);
+
+  const uint32_t warp = tc::warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+  const int mblocks = n / BM;
+  const int items = bh * mblocks;
+  const int ntiles = (m + BN - 1) / BN;
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tm_q);
+    tc::prefetch_tmap(&tm_k);
+    tc::prefetch_tmap(&tm_nz);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&q_full[i], 1);
+      tc::mbar_init(&q_empty[i], 1);
+    }
+    for (int i = 0; i < KSTAGES; ++i) {
+      tc::mbar_init(&k_full[i], 1);
+      tc::mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < NACC; ++i) {
+      tc::mbar_init(&t_full[i], 1);
+      tc::mbar_init(&t_empty[i], EPI_WARPS);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 2) tc::tmem_alloc<512>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int ks = 0;
+      uint32_t kph = 0;
+      int it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        const int b = item / mblocks, mb = item % mblocks;
+        const int qs = it & 1;
+        const uint32_t qph = (it >> 1) & 1;
+        tc::mbar_wait(&q_empty[qs], qph ^ 1);
+        tc::mbar_arrive_expect_tx(&q_full[qs], Q_BYTES);
+        tc::tma_load_3d(smem + SMEM_Q + qs * Q_BYTES, &tm_q, &q_full[qs], 0, mb * BM, b);
+        for (int t = 0; t < ntiles; ++t) {
+          tc::mbar_wait(&k_empty[ks], kph ^ 1);
+          tc::mbar_arrive_expect_tx(&k_full[ks], K_BYTES);
+          tc::tma_load_3d(smem + SMEM_K + ks * K_BYTES, &tm_k, &k_full[ks], 0, t * BN, b);
+          if (++ks == KSTAGES) { ks = 0; kph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+      constexpr uint32_t idesc256 = tc::instr_desc(fmt, BM, 256, false, false, false);
+      constexpr uint32_t idesc128 = tc::instr_desc(fmt, BM, 128, false, false, false);
+      int ks = 0, acc = 0;
+      uint32_t kph = 0, aph = 0;
+      int it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        const int qs = it & 1;
+        const uint32_t qph = (it >> 1) & 1;
+        tc::mbar_wait(&q_full[qs], qph);
+        const uint32_t q_addr = tc::smem_u32(smem + SMEM_Q + qs * Q_BYTES);
+        for (int t = 0; t < ntiles; ++t) {
+          const uint32_t idesc = (m - t * BN >= BN) ? idesc256 : idesc128;
+          tc::mbar_wait(&t_empty[acc], aph ^ 1);
+          tc::mbar_wait(&k_full[ks], kph);
+          tc::tc_fence_after();
+          const uint32_t k_addr = tc::smem_u32(smem + SMEM_K + ks * K_BYTES);
+          const uint32_t d_tmem = tmem_base + acc * BN;
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint64_t ad = tc::smem_desc(q_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
+            const uint64_t bd = tc::smem_desc(k_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
+            tc::mma_f16_ss(d_tmem, ad, bd, idesc, kk > 0 ? 1u : 0u);
+          }
+          tc::mma_commit(&k_empty[ks]);
+          tc::mma_commit(&t_full[acc]);
+          if (++ks == KSTAGES) { ks = 0; kph ^= 1; }
+          if (++acc == NACC) { acc = 0; aph ^= 1; }
+        }
+        tc::mma_commit(&q_empty[qs]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 4;
+    const int quad = warp & 3;
+    const int half = ew >> 2;
+    const int chunks = m / 32;  // meta chunks of 8 groups per row block
+    uint8_t* stg_base = smem + SMEM_STG + ew * 2 * STG_BYTES;
+    int acc = 0, sb = 0;
+    uint32_t aph = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+      const int b = item / mblocks, mb = item % mblocks;
+      const int row_blk = quad * 32 + lane;  // row within the 128-row block
+      const int grow = mb * BM + row_blk;    // row within the head
+      uint32_t* meta_b = meta + ((int64_t)b * mblocks + mb) * chunks * 128;
+      for (int t = 0; t < ntiles; ++t) {
+        const int width = min(BN, m - t * BN);
+        const bool active = half * 128 < width;
+        tc::mbar_wait(&t_full[acc], aph);
+        tc::tc_fence_after();
+        uint8_t* stg = stg_base + sb * STG_BYTES;
+        if (active) {
+          if (lane == 0) tc::bulk_wait_read<1>();  // staging buffer from two tiles ago drained
+          __syncwarp();
+#pragma unroll 1
+          for (int cc = 0; cc < 4; ++cc) {
+            uint32_t r[32];
+            tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + half * 128 + cc * 32, r);
+            tc::tmem_ld_wait();
+            const int col0 = t * BN + half * 128 + cc * 32;
+            uint32_t packed[8];
+            uint32_t W = 0;
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+              const float v0 = __uint_as_float(r[4 * g + 0]) * scale;
+              const float v1 = __uint_as_float(r[4 * g + 1]) * scale;
+              const float v2 = __uint_as_float(r[4 * g + 2]) * scale;
+              const float v3 = __uint_as_float(r[4 * g + 3]) * scale;
+              if (dbg) {
+                float4 sv = make_float4(v0, v1, v2, v3);
+                *reinterpret_cast<float4*>(dbg + ((int64_t)b * n + grow) * m + col0 + 4 * g) = sv;
+              }
+              float lo, hi;
+              const uint32_t nib = select24(v0, v1, v2, v3, lo, hi);
+              packed[g] = pack2<T>(lo, hi);
+              W |= nib << (4 * g);
+            }
+            // nonzeros -> 128B-swizzled staging row (16B unit u lands at u ^ (row % 8))
+            const int u0 = 2 * cc, sw = lane & 7;
+            *reinterpret_cast<uint4*>(stg + lane * 128 + ((u0 ^ sw) << 4)) =
+                make_uint4(packed[0], packed[1], packed[2], packed[3]);
+            *reinterpret_cast<uint4*>(stg + lane * 128 + (((u0 + 1) ^ sw) << 4)) =
+                make_uint4(packed[4], packed[5], packed[6], packed[7]);
+            // metadata: rows r and r^8 trade 16-bit halves -> the word of TMEM lane r (include/dfss.h)
+            const uint32_t partner = __shfl_xor_sync(0xffffffffu, W, 8);
+            const uint32_t word = (lane & 8) ? ((partner >> 16) | (W & 0xFFFF0000u)) : ((W & 0xFFFFu) | (partner << 16));
+            meta_b[(int64_t)(col0 >> 5) * 128 + row_blk] = word;
+          }
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&t_empty[acc]);
+        if (active) {
+          tc::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            tc::tma_store_3d(&tm_nz, stg, t * (BN / 2) + half * 64, mb * BM + quad * 32, b);
+            tc::bulk_commit();
+          }
+          sb ^= 1;
+        }
+        if (++acc == NACC) { acc = 0; aph ^= 1; }
+      }
+    }
+    if (lane == 0) tc::bulk_wait<0>();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<512>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+
+bool tc_sddmm_supported(int gs, int in_dtype, int nz_dtype, int n, int m, int d) {
+  return gs == 4 && (in_dtype == DFSS_BF16 || in_dtype == DFSS_F16) && nz_dtype == in_dtype && d == HD &&
+         n % BM == 0 && m % 128 == 0 && n > 0 && m > 0;
+}
+
+static int num_sms() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    if (cached <= 0) cached = 148;
+  }
+  return cached;
+}
+
+template <typename T>
+static cudaError_t launch_typed(const void* q, const void* k, void* nz, uint32_t* meta, float scale, int64_t bh, int n,
+                                int m, float* dbg, cudaStream_t s) {
+  const CUtensorMapDataType dt =
+      std::is_same<T, __nv_bfloat16>::value ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap tq, tk, tn;
+  if (!encode_tmap_3d(&tq, dt, 2, (void*)q, HD, n, bh, HD, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !encode_tmap_3d(&tk, dt, 2, (void*)k, HD, m, bh, HD, BN, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !encode_tmap_3d(&tn, dt, 2, nz, m / 2, n, bh, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  auto kern = sddmm24_tc_kernel<T>;
+  static bool attr_set[2] = {false, false};
+  const int ti = std::is_same<T, __nv_bfloat16>::value ? 0 : 1;
+  if (!attr_set[ti]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
+    if (e != cudaSuccess) return e;
+    attr_set[ti] = true;
+  }
+  const int items = (int)bh * (n / BM);
+  const int grid = items < num_sms() ? items : num_sms();
+  kern<<<grid, NUM_THREADS, SMEM_TOTAL, s>>>(tq, tk, tn, meta, scale, (int)bh, n, m, dbg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sddmm_tc(const void* q, const void* k, void* nz, uint32_t* meta, float scale, int gs, int in_dtype,
+                            int64_t bh, int n, int m, int d, float* dbg, cudaStream_t s) {
+  if (!tc_sddmm_supported(gs, in_dtype, in_dtype, n, m, d)) return cudaErrorNotSupported;
+  if (bh == 0) return cudaSuccess;
+  if (in_dtype == DFSS_BF16) return launch_typed<__nv_bfloat16>(q, k, nz, meta, scale, bh, n, m, dbg, s);
+  return launch_typed<__half>(q, k, nz, meta, scale, bh, n, m, dbg, s);
+}
+
+}  // namespace dfss

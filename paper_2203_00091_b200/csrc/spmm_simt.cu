@@ -1,0 +1,141 @@
+// spmm_simt.cu -- generic compressed SpMM on FP32 FFMA: out = decompress(P) . V.
+//
+// Replaces _spmm_gather (_kernels_numba.py:91-103): for every row, the
+// stored nonzeros are visited in ascending order and out[i,:] += p * V[col,:],
+// where the dense column comes from the nibble in meta_hw (the decode of
+// codec.nonzero_columns, codec.py:346-360, done in registers).  One warp per
+// output row; each lane decodes one nonzero of a 32-wide batch, the batch is
+// broadcast by shuffles, lanes own output columns lane + 32*t.
+// This is the exact-FP32 path (c1 at 1e-5) and the fallback for shapes the
+// tcgen05.mma.sp kernel does not tile.
+#include "dfss_common.cuh"
+
+namespace dfss {
+
+template <typename TP, typename TV, typename TO, int GS, int DPER>
+__global__ void __launch_bounds__(256) spmm_simt_kernel(const TP* __restrict__ p, const uint32_t* __restrict__ meta,
+                                                        const TV* __restrict__ v, TO* __restrict__ out,
+                                                        int64_t total_rows, int rows, int n_k, int d,
+                                                        const uint8_t* __restrict__ keep, int tile_rows,
+                                                        int tile_cols, MetaGeom geo) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int nzc = n_k / 2;
+  const int grid_cols = keep ? (n_k + tile_cols - 1) / tile_cols : 0;
+
+  for (int64_t rg = warp; rg < total_rows; rg += nwarps) {
+    const int64_t b = rg / rows;
+    const int r = (int)(rg % rows);
+    const TP* prow = p + rg * nzc;
+    const uint32_t* mb = meta + b * geo.words_per_bh();
+    const TV* vb = v + b * (int64_t)n_k * d;
+    float acc[DPER];
+#pragma unroll
+    for (int t = 0; t < DPER; ++t) acc[t] = 0.f;
+
+    for (int j0 = 0; j0 < nzc; j0 += 32) {
+      const int j = j0 + lane;
+      float pv = 0.f;
+      int col = 0;
+      if (j < nzc) {
+        const int g = (GS == 4) ? (j >> 1) : j;
+        int shift;
+        const uint32_t nib = (mb[geo.word_of(r, g, shift)] >> shift) & 0xFu;
+        col = (GS == 4) ? 4 * g + (int)((j & 1) ? ((nib >> 2) & 3u) : (nib & 3u)) : 2 * g + (nib == 0xEu ? 1 : 0);
+        pv = DT<TP>::to_f(prow[j]);
+        if (keep && !keep[(int64_t)(r / tile_rows) * grid_cols + col / tile_cols]) pv = 0.f;
+      }
+      const int cnt = min(32, nzc - j0);
+      for (int l = 0; l < cnt; ++l) {
+        const float pl = __shfl_sync(0xffffffffu, pv, l);
+        const int cl = __shfl_sync(0xffffffffu, col, l);
+        const TV* vr = vb + (int64_t)cl * d;
+#pragma unroll
+        for (int t = 0; t < DPER; ++t) {
+          const int c = lane + 32 * t;
+          if (c < d) acc[t] = fmaf(pl, DT<TV>::to_f(vr[c]), acc[t]);
+        }
+      }
+    }
+    TO* orow = out + rg * d;
+#pragma unroll
+    for (int t = 0; t < DPER; ++t) {
+      const int c = lane + 32 * t;
+      if (c < d) orow[c] = DT<TO>::from_f(acc[t]);
+    }
+  }
+}
+
+template <typename TP, typename TV, typename TO, int GS>
+static cudaError_t spmm_simt_gs(const void* p, const uint32_t* meta, const void* v, void* out, int64_t bh, int rows,
+                                int n_k, int d, const uint8_t* keep, int tr, int tc, cudaStream_t s) {
+  MetaGeom geo(rows, n_k / GS);
+  const int64_t total = bh * rows;
+  int64_t blocks = (total + 7) / 8;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  const int dper = (d + 31) / 32;
+#define DFSS_SPMM_LAUNCH(DP)                                                                                    \
+  spmm_simt_kernel<TP, TV, TO, GS, DP><<<(int)blocks, 256, 0, s>>>((const TP*)p, meta, (const TV*)v, (TO*)out, \
+                                                                   total, rows, n_k, d, keep, tr, tc, geo)
+  if (dper <= 1)
+    DFSS_SPMM_LAUNCH(1);
+  else if (dper <= 2)
+    DFSS_SPMM_LAUNCH(2);
+  else if (dper <= 4)
+    DFSS_SPMM_LAUNCH(4);
+  else
+    DFSS_SPMM_LAUNCH(8);
+#undef DFSS_SPMM_LAUNCH
+  return cudaGetLastError();
+}
+
+template <typename TP, typename TV, typename TO>
+static cudaError_t spmm_simt_typed(const void* p, const uint32_t* meta, const void* v, void* out, int gs, int64_t bh,
+                                   int rows, int n_k, int d, const uint8_t* keep, int tr, int tc, cudaStream_t s) {
+  return gs == 4 ? spmm_simt_gs<TP, TV, TO, 4>(p, meta, v, out, bh, rows, n_k, d, keep, tr, tc, s)
+                 : spmm_simt_gs<TP, TV, TO, 2>(p, meta, v, out, bh, rows, n_k, d, keep, tr, tc, s);
+}
+
+template <typename TP, typename TV>
+static cudaError_t spmm_simt_pv(const void* p, const uint32_t* meta, const void* v, void* out, int gs, int out_dtype,
+                                int64_t bh, int rows, int n_k, int d, const uint8_t* keep, int tr, int tc,
+                                cudaStream_t s) {
+  switch (out_dtype) {
+    case DFSS_F32: return spmm_simt_typed<TP, TV, float>(p, meta, v, out, gs, bh, rows, n_k, d, keep, tr, tc, s);
+    case DFSS_BF16:
+      return spmm_simt_typed<TP, TV, __nv_bfloat16>(p, meta, v, out, gs, bh, rows, n_k, d, keep, tr, tc, s);
+    default: return spmm_simt_typed<TP, TV, __half>(p, meta, v, out, gs, bh, rows, n_k, d, keep, tr, tc, s);
+  }
+}
+
+template <typename TP>
+static cudaError_t spmm_simt_p(const void* p, const uint32_t* meta, const void* v, void* out, int gs, int v_dtype,
+                               int out_dtype, int64_t bh, int rows, int n_k, int d, const uint8_t* keep, int tr, int tc,
+                               cudaStream_t s) {
+  switch (v_dtype) {
+    case DFSS_F32: return spmm_simt_pv<TP, float>(p, meta, v, out, gs, out_dtype, bh, rows, n_k, d, keep, tr, tc, s);
+    case DFSS_BF16:
+      return spmm_simt_pv<TP, __nv_bfloat16>(p, meta, v, out, gs, out_dtype, bh, rows, n_k, d, keep, tr, tc, s);
+    default: return spmm_simt_pv<TP, __half>(p, meta, v, out, gs, out_dtype, bh, rows, n_k, d, keep, tr, tc, s);
+  }
+}
+
+cudaError_t launch_spmm_simt(const void* p, const uint32_t* meta, const void* v, void* out, int gs, int p_dtype,
+                             int v_dtype, int out_dtype, int64_t bh, int rows, int n_k, int d, const uint8_t* keep,
+                             int tile_rows, int tile_cols, cudaStream_t s) {
+  if (bh == 0 || rows == 0 || d == 0) return cudaSuccess;
+  switch (p_dtype) {
+    case DFSS_F32:
+      return spmm_simt_p<float>(p, meta, v, out, gs, v_dtype, out_dtype, bh, rows, n_k, d, keep, tile_rows, tile_cols,
+                                s);
+    case DFSS_BF16:
+      return spmm_simt_p<__nv_bfloat16>(p, meta, v, out, gs, v_dtype, out_dtype, bh, rows, n_k, d, keep, tile_rows,
+                                        tile_cols, s);
+    default:
+      return spmm_simt_p<__half>(p, meta, v, out, gs, v_dtype, out_dtype, bh, rows, n_k, d, keep, tile_rows, tile_cols,
+                                 s);
+  }
+}
+
+}  // namespace dfss

@@ -1,0 +1,246 @@
+// spmm_tc.cu -- compressed SpMM O = P_sparse . V on tcgen05.mma.sp (2:4, bf16/fp16, d = 64).
+//
+// Replaces _spmm_gather (_kernels_numba.py:91-103) for the 16-bit path.  The
+// compressed P rows ARE the sparse A operand (kept values in ascending column
+// order, K-major) and meta_hw words ARE the TMEM metadata columns, so nothing
+// is decoded: the SDDMM output is consumed as written.  Persistent,
+// warp-specialised, one CTA per SM:
+//   warp 0      TMA producer: P tile (128 rows x 64 stored = 128 logical K) and
+//               V tile (128 K-rows x 64, MN-major) per stage, STAGES-deep ring;
+//   warp 1      MMA issuer: 4 x tcgen05.mma.sp.kind::f16 (M=128, N=64, K=32) per
+//               stage, metadata column s*4+kk, accumulator double-buffered;
+//   warp 2      TMEM allocator;
+//   warps 4-7   metadata loaders: warp w copies the words of TMEM lanes
+//               32*(w%4).. for the stage's 4 K-chunks global -> tcgen05.st;
+//   warps 8-11  epilogue: TMEM -> registers -> 16-bit -> O rows.
+#include <type_traits>
+
+#include "dfss_common.cuh"
+#include "tc_common.cuh"
+
+namespace dfss {
+
+namespace {
+constexpr int BM = 128;
+constexpr int HD = 64;
+constexpr int BKL = 128;  // logical K per stage
+constexpr int STAGES = 6;
+constexpr int NACC = 2;
+constexpr int NUM_THREADS = 12 * 32;
+constexpr int P_BYTES = BM * (BKL / 2) * 2;  // 16 KB
+constexpr int V_BYTES = BKL * HD * 2;        // 16 KB
+constexpr int SMEM_P = 0;
+constexpr int SMEM_V = SMEM_P + STAGES * P_BYTES;
+constexpr int SMEM_BAR = SMEM_V + STAGES * V_BYTES;
+constexpr int SMEM_TOTAL = SMEM_BAR + 512 + 1024;
+constexpr int TMEM_COLS = 256;
+constexpr int E_COL0 = NACC * HD;  // metadata columns start after the accumulators
+}  // namespace
+
+template <typename T, typename TO>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    spmm24_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_v,
+                     const uint32_t* __restrict__ meta, TO* __restrict__ out, int bh, int rows, int n_k) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = (uint64_t*)(smem + SMEM_BAR);
+  uint64_t* full = bars;                 // [STAGES] TMA bytes landed
+  uint64_t* e_full = full + STAGES;      // [STAGES] metadata columns written (4 warps)
+  uint64_t* empty = e_full + STAGES;     // [STAGES] MMAs of the stage retired
+  uint64_t* d_full = empty + STAGES;     // [NACC]
+  uint64_t* d_empty = d_full + NACC;     // [NACC] (4 epilogue warps)
+  uint32_t* tmem_slot = (uint32_t*)(d_empty + NACC);
+
+  const uint32_t warp = tc::warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+  const int rblocks = rows / BM;
+  const int items = bh * rblocks;
+  const int kblocks = n_k / BKL;
+  const int chunks = n_k / 32;
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tm_p);
+    tc::prefetch_tmap(&tm_v);
+    for (int i = 0; i < STAGES; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&e_full[i], 4);
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < NACC; ++i) {
+      tc::mbar_init(&d_full[i], 1);
+      tc::mbar_init(&d_empty[i], 4);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 2) tc::tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const int b = item / rblocks, rb = item % rblocks;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          tc::mbar_wait(&empty[s], ph ^ 1);
+          tc::mbar_arrive_expect_tx(&full[s], P_BYTES + V_BYTES);
+          tc::tma_load_3d(smem + SMEM_P + s * P_BYTES, &tm_p, &full[s], kb * (BKL / 2), rb * BM, b);
+          tc::tma_load_3d(smem + SMEM_V + s * V_BYTES, &tm_v, &full[s], 0, kb * BKL, b);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+      constexpr uint32_t idesc = tc::instr_desc(fmt, BM, HD, /*a_mn=*/false, /*b_mn=*/true, /*sparse=*/true);
+      int s = 0, acc = 0;
+      uint32_t ph = 0, aph = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        tc::mbar_wait(&d_empty[acc], aph ^ 1);
+        const uint32_t d_tmem = tmem_base + acc * HD;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          tc::mbar_wait(&full[s], ph);
+          tc::mbar_wait(&e_full[s], ph);
+          tc::tc_fence_after();
+          const uint32_t p_addr = tc::smem_u32(smem + SMEM_P + s * P_BYTES);
+          const uint32_t v_addr = tc::smem_u32(smem + SMEM_V + s * V_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BKL / 32; ++kk) {
+            // A: K-major, 16 stored elements (32 B) per MMA inside the 128B swizzle row
+            const uint64_t ad = tc::smem_desc(p_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
+            // B: MN-major, 32 K-rows of 128 B per MMA = 4 whole swizzle atoms
+            const uint64_t bd = tc::smem_desc(v_addr + kk * 32 * 128, V_BYTES, 1024, tc::kSwizzle128B);
+            tc::mma_sp_f16_ss(d_tmem, ad, bd, tmem_base + E_COL0 + s * 4 + kk, idesc, (kb | kk) ? 1u : 0u);
+          }
+          tc::mma_commit(&empty[s]);
+          if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+        tc::mma_commit(&d_full[acc]);
+        if (++acc == NACC) { acc = 0; aph ^= 1; }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------------------ metadata -> TMEM
+    const int quad = warp & 3;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+      const int b = item / rblocks, rb = item % rblocks;
+      const uint32_t* mrow = meta + ((int64_t)b * rblocks + rb) * chunks * 128 + quad * 32 + lane;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const uint32_t w0 = __ldg(mrow + (int64_t)(kb * 4 + 0) * 128);
+        const uint32_t w1 = __ldg(mrow + (int64_t)(kb * 4 + 1) * 128);
+        const uint32_t w2 = __ldg(mrow + (int64_t)(kb * 4 + 2) * 128);
+        const uint32_t w3 = __ldg(mrow + (int64_t)(kb * 4 + 3) * 128);
+        tc::mbar_wait(&empty[s], ph ^ 1);
+        tc::tc_fence_after();
+        tc::tmem_st_32x32b_x4(tmem_base + ((uint32_t)(quad * 32) << 16) + E_COL0 + s * 4, w0, w1, w2, w3);
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&e_full[s]);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------------------------ epilogue
+    const int quad = warp & 3;
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+      const int b = item / rblocks, rb = item % rblocks;
+      tc::mbar_wait(&d_full[acc], aph);
+      tc::tc_fence_after();
+      uint32_t r0[32], r1[32];
+      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * HD;
+      tc::tmem_ld_32x32b_x32(taddr, r0);
+      tc::tmem_ld_32x32b_x32(taddr + 32, r1);
+      tc::tmem_ld_wait();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&d_empty[acc]);
+      TO* orow = out + ((int64_t)b * rows + rb * BM + quad * 32 + lane) * HD;
+      if constexpr (std::is_same<TO, float>::value) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          reinterpret_cast<float4*>(orow)[j] = make_float4(__uint_as_float(r0[4 * j]), __uint_as_float(r0[4 * j + 1]),
+                                                           __uint_as_float(r0[4 * j + 2]), __uint_as_float(r0[4 * j + 3]));
+          reinterpret_cast<float4*>(orow)[8 + j] =
+              make_float4(__uint_as_float(r1[4 * j]), __uint_as_float(r1[4 * j + 1]), __uint_as_float(r1[4 * j + 2]),
+                          __uint_as_float(r1[4 * j + 3]));
+        }
+      } else {
+        uint32_t pk[32];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          TO lo = DT<TO>::from_f(__uint_as_float(r0[2 * j])), hi = DT<TO>::from_f(__uint_as_float(r0[2 * j + 1]));
+          pk[j] = (uint32_t)(*reinterpret_cast<uint16_t*>(&lo)) | ((uint32_t)(*reinterpret_cast<uint16_t*>(&hi)) << 16);
+          TO lo2 = DT<TO>::from_f(__uint_as_float(r1[2 * j])), hi2 = DT<TO>::from_f(__uint_as_float(r1[2 * j + 1]));
+          pk[16 + j] =
+              (uint32_t)(*reinterpret_cast<uint16_t*>(&lo2)) | ((uint32_t)(*reinterpret_cast<uint16_t*>(&hi2)) << 16);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          reinterpret_cast<uint4*>(orow)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+      }
+      if (++acc == NACC) { acc = 0; aph ^= 1; }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+bool tc_spmm_supported(int gs, int p_dtype, int v_dtype, int out_dtype, int rows, int n_k, int d) {
+  return gs == 4 && (p_dtype == DFSS_BF16 || p_dtype == DFSS_F16) && v_dtype == p_dtype &&
+         (out_dtype == p_dtype || out_dtype == DFSS_F32) && d == HD && rows % BM == 0 && n_k % BKL == 0 && rows > 0;
+}
+
+static int num_sms_spmm() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev);
+    if (cached <= 0) cached = 148;
+  }
+  return cached;
+}
+
+template <typename T, typename TO>
+static cudaError_t spmm_launch_typed(const void* p, const uint32_t* meta, const void* v, void* out, int64_t bh, int rows,
+                                     int n_k, cudaStream_t s) {
+  const CUtensorMapDataType dt =
+      std::is_same<T, __nv_bfloat16>::value ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  CUtensorMap tp, tv;
+  if (!encode_tmap_3d(&tp, dt, 2, (void*)p, n_k / 2, rows, bh, BKL / 2, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !encode_tmap_3d(&tv, dt, 2, (void*)v, HD, n_k, bh, HD, BKL, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  auto kern = spmm24_tc_kernel<T, TO>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
+  if (e != cudaSuccess) return e;
+  const int items = (int)bh * (rows / BM);
+  const int grid = items < num_sms_spmm() ? items : num_sms_spmm();
+  kern<<<grid, NUM_THREADS, SMEM_TOTAL, s>>>(tp, tv, meta, (TO*)out, (int)bh, rows, n_k);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spmm_tc(const void* p, const uint32_t* meta, const void* v, void* out, int gs, int dtype,
+                           int out_dtype, int64_t bh, int rows, int n_k, int d, cudaStream_t s) {
+  if (!tc_spmm_supported(gs, dtype, dtype, out_dtype, rows, n_k, d)) return cudaErrorNotSupported;
+  if (bh == 0) return cudaSuccess;
+  if (dtype == DFSS_BF16)
+    return out_dtype == DFSS_F32 ? spmm_launch_typed<__nv_bfloat16, float>(p, meta, v, out, bh, rows, n_k, s)
+                                 : spmm_launch_typed<__nv_bfloat16, __nv_bfloat16>(p, meta, v, out, bh, rows, n_k, s);
+  return out_dtype == DFSS_F32 ? spmm_launch_typed<__half, float>(p, meta, v, out, bh, rows, n_k, s)
+                               : spmm_launch_typed<__half, __half>(p, meta, v, out, bh, rows, n_k, s);
+}
+
+}  // namespace dfss

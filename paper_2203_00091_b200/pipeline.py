@@ -1,0 +1,113 @@
+"""End-to-end DFSS attention on the B200 (reference: pipeline.py).
+
+``nm_attention`` keeps the reference signature (pipeline.py:15-32);
+``dfss_attention`` is the tensor-level drop-in for a model's attention over
+[..., n, d] CUDA tensors and is what ``DFSSAttention`` and bench.py call.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .codec import BlockMask, SparsityMode, as_mode, decompress
+from .dense import AttentionInputs, DenseMatrix, as_tensor, dense_attention_weights
+from .fused import _MATH, attention_sddmm
+from .sparse_ops import softmax_rows, spmm
+
+
+def workspace_bytes(mode, dtype: torch.dtype, bh: int, n: int, d: int) -> int:
+    """Device scratch for the compressed P and metadata of one dfss_attention call."""
+    mode = as_mode(mode)
+    return int(_lib.load().dfss_nm_attention_workspace_bytes(mode.group_size, _lib.dtype_id(dtype), bh, n, d))
+
+
+def dfss_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode="2:4", *, math_mode: str = "auto",
+                   out: torch.Tensor | None = None, workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """softmax_N:M(Q K^T / sqrt d) V for [..., n, d] q/k/v on one CUDA device.
+
+    One C-ABI call (dfss_nm_attention); no dense n x n tensor is allocated.
+    """
+    mode = as_mode(mode)
+    if q.shape != k.shape or q.shape != v.shape:
+        raise ValueError(f"Q, K, V must share shape (n, d); got {tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
+    if q.dim() < 2:
+        raise ValueError("expected [..., n, d] tensors")
+    n, d = q.shape[-2], q.shape[-1]
+    if n % mode.group_size:
+        raise ValueError(f"score columns {n} not group-aligned for mode {mode.value} (need a multiple of {mode.group_size})")
+    if math_mode not in _MATH:
+        raise ValueError(f"unknown math mode {math_mode!r}")
+    _lib.require_cuda(q, k, v)
+    if not (q.dtype == k.dtype == v.dtype):
+        raise ValueError("Q, K, V must share a dtype")
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    bh = int(np.prod(q.shape[:-2], dtype=np.int64)) if q.dim() > 2 else 1
+    if out is None:
+        out = torch.empty_like(q)
+    need = workspace_bytes(mode, q.dtype, bh, n, d)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
+    lib = _lib.load()
+    _lib.check(lib.dfss_nm_attention(_lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(out), mode.group_size,
+                                     _lib.dtype_id(q.dtype), _MATH[math_mode], bh, n, d, _lib.ptr(workspace), need,
+                                     _lib.stream_of(q)), "nm_attention")
+    return out
+
+
+def nm_attention(inputs: AttentionInputs, mode: SparsityMode, block_mask: BlockMask | None = None, *,
+                 tile_rows: int = 32, tile_cols: int = 64) -> DenseMatrix:
+    """Drop-in sparse attention: fused prune -> sparse softmax -> SpMM (pipeline.py:15-32)."""
+    mode = as_mode(mode)
+    if block_mask is None:
+        return DenseMatrix(dfss_attention(inputs.q.data, inputs.k.data, inputs.v.data, mode), check_finite=False)
+    compressed, _ = attention_sddmm(inputs.q, inputs.k, mode, block_mask, tile_rows=tile_rows, tile_cols=tile_cols)
+    return spmm(softmax_rows(compressed, check=False), inputs.v)
+
+
+@dataclass(frozen=True)
+class ApproxError:
+    """Error of a sparse output against the full-attention baseline (pipeline.py:35-46)."""
+
+    rel_l2: float
+    max_abs: float
+    row_rel: torch.Tensor
+
+    def __str__(self) -> str:
+        return f"rel_l2={self.rel_l2:.6e} max_abs={self.max_abs:.6e}"
+
+
+def approx_error(full, sparse) -> ApproxError:
+    """Relative Frobenius error, max absolute error, per-row errors (pipeline.py:49-57), in float64."""
+    f = as_tensor(full).double()
+    s = as_tensor(sparse).double()
+    if f.shape != s.shape:
+        raise ValueError(f"shape mismatch: {tuple(f.shape)} vs {tuple(s.shape)}")
+    diff = f - s
+    denom = torch.linalg.norm(f)
+    rel = float(torch.linalg.norm(diff) / denom) if float(denom) > 0 else 0.0
+    row_norms = torch.linalg.norm(f, dim=-1)
+    safe = torch.where(row_norms > 0, row_norms, torch.ones_like(row_norms))
+    row_rel = torch.where(row_norms > 0, torch.linalg.norm(diff, dim=-1) / safe, torch.zeros_like(row_norms))
+    return ApproxError(rel, float(diff.abs().max()), row_rel)
+
+
+@dataclass(frozen=True)
+class AttentionWeights:
+    dense: DenseMatrix
+    sparse: DenseMatrix
+
+
+def attention_heatmap(inputs: AttentionInputs, mode: SparsityMode) -> AttentionWeights:
+    """Dense and sparse weight matrices (pipeline.py:60-78)."""
+    dense = dense_attention_weights(inputs)
+    compressed, _ = attention_sddmm(inputs.q, inputs.k, as_mode(mode))
+    return AttentionWeights(dense, decompress(softmax_rows(compressed)))
+
+
+def reference_scale(d: int) -> float:
+    return 1.0 / math.sqrt(d)

@@ -1,0 +1,81 @@
+"""Operations on compressed matrices: per-row softmax and SpMM (reference: sparse_ops.py)."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .codec import BlockMask, CompressedSparse, Layout
+from .dense import DenseMatrix, as_tensor
+
+_INT32_MAX = 2**31 - 1
+
+
+def softmax_rows(c: CompressedSparse, out_dtype: torch.dtype | None = None, *, check: bool = True) -> CompressedSparse:
+    """Stable softmax over each row's kept entries (sparse_ops.py:18-37).
+
+    Rows whose tiles are all masked are rejected ("empty row N"), as is NaN
+    input ("NaN") -- the NaN check reads a device flag, i.e. synchronises;
+    pass ``check=False`` on hot paths.
+    """
+    if c.layout is not Layout.LOGICAL:
+        raise ValueError("softmax requires the logical layout")
+    if c.block_mask is not None:
+        bm = c.block_mask
+        rows_present = bm.nonzero_keep(c.rows, c.dense_cols).any(axis=1)
+        if not rows_present.all():
+            row = int(np.flatnonzero(~rows_present)[0])
+            raise ValueError(f"empty row {row}: all tiles masked, softmax undefined")
+    out_dtype = out_dtype or c.nonzeros.dtype
+    out = torch.empty(c.nonzeros.shape, dtype=out_dtype, device=c.device)
+    err = torch.full((2,), _INT32_MAX, dtype=torch.int32, device=c.device) if check else None
+    keep = c.block_mask.device_keep(c.device) if c.block_mask is not None else None
+    tr = c.block_mask.tile_rows if c.block_mask is not None else 0
+    tc = c.block_mask.tile_cols if c.block_mask is not None else 0
+    lib = _lib.load()
+    _lib.check(lib.dfss_softmax_rows(_lib.ptr(c.nonzeros), _lib.ptr(out), _lib.dtype_id(c.nonzeros.dtype),
+                                     _lib.dtype_id(out_dtype), c.bh, c.rows, c.nonzero_cols, _lib.ptr(keep), tr, tc,
+                                     _lib.ptr(err), _lib.stream_of(out)), "softmax_rows")
+    if check:
+        e = err.tolist()
+        if e[1] != _INT32_MAX:
+            raise ValueError("NaN in nonzeros, softmax rejected")
+        if e[0] != _INT32_MAX:
+            raise ValueError(f"empty row {(e[0] - 1) % c.rows}: all tiles masked, softmax undefined")
+    return CompressedSparse(c.rows, c.dense_cols, c.mode, out, c.meta_hw, layout=Layout.LOGICAL,
+                            block_mask=c.block_mask)
+
+
+def spmm(a: CompressedSparse, v, block_mask: BlockMask | None = None, out_dtype: torch.dtype | None = None) -> DenseMatrix:
+    """decompress(a) @ v with the metadata consumed in place (sparse_ops.py:40-68)."""
+    if a.layout is not Layout.LOGICAL:
+        raise ValueError("spmm requires the logical layout")
+    vt = as_tensor(v)
+    if a.dense_cols != vt.shape[-2]:
+        raise ValueError(
+            f"shape mismatch: sparse operand is {a.rows}x{a.dense_cols}, dense operand has {vt.shape[-2]} rows"
+        )
+    if block_mask is not None and a.block_mask is not None:
+        raise ValueError("block mask given both on the matrix and as an argument")
+    bm = block_mask if block_mask is not None else a.block_mask
+    if bm is not None:
+        bm.check_covers(a.rows, a.dense_cols)
+    _lib.require_cuda(vt)
+    if tuple(vt.shape[:-2]) != a.batch_shape:
+        if vt.dim() == 2 and a.bh == 1:
+            pass
+        else:
+            raise ValueError(f"shape mismatch: batch dims {a.batch_shape} vs {tuple(vt.shape[:-2])}")
+    vt = vt.contiguous()
+    d = vt.shape[-1]
+    out_dtype = out_dtype or torch.promote_types(a.nonzeros.dtype, vt.dtype)
+    out = torch.empty(a.batch_shape + (a.rows, d), dtype=out_dtype, device=a.device)
+    keep = bm.device_keep(a.device) if bm is not None else None
+    tr = bm.tile_rows if bm is not None else 0
+    tc = bm.tile_cols if bm is not None else 0
+    lib = _lib.load()
+    _lib.check(lib.dfss_spmm(_lib.ptr(a.nonzeros), _lib.ptr(a.meta_hw), _lib.ptr(vt), _lib.ptr(out), a.mode.group_size,
+                             _lib.dtype_id(a.nonzeros.dtype), _lib.dtype_id(vt.dtype), _lib.dtype_id(out_dtype), a.bh,
+                             a.rows, a.dense_cols, d, _lib.ptr(keep), tr, tc, _lib.stream_of(out)), "spmm")
+    return DenseMatrix(out, check_finite=False)

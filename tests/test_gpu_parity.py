@@ -1,0 +1,378 @@
+"""GPU parity tests: the sm_100a kernels against the CPU oracle (pinned to the reference).
+
+Bars (BASELINE.json north_star):
+  * metadata and kept masks BIT-EXACT when the oracle is fed the same score
+    tensor the epilogue selected on (the fp32 post-scale dump);
+  * nonzeros bit-exact in fp32, equal to the RNE-rounded oracle nonzeros in 16-bit;
+  * attention outputs |o - o_ref| <= atol + rtol*|o_ref| with rtol = atol = 1e-5
+    (fp32) and 2e-2 (bf16 / fp16), o_ref = reference nm_attention in float64 on
+    the same dtype-rounded inputs.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+from gpu_helpers import assert_close, logical_meta, oracle_attention, oracle_on_scores, seeded_qkv
+
+import paper_2203_00091_b200 as dfss
+from oracle import nmattn_oracle as ref
+from oracle import oracle_c
+
+pytestmark = pytest.mark.gpu
+
+M12 = dfss.SparsityMode.ONE_OF_TWO
+M24 = dfss.SparsityMode.TWO_OF_FOUR
+MODES = {"1:2": M12, "2:4": M24}
+TOL = {torch.float32: 1e-5, torch.bfloat16: 2e-2, torch.float16: 2e-2}
+
+
+def _np(t):
+    return t.detach().float().cpu().numpy().astype(np.float64)
+
+
+# ---------------------------------------------------------------- selection hook
+
+
+def test_select_group_anchors_on_device():
+    g = golden("codec.npz")
+    for i in range(int(g["n_groups"])):
+        mode = str(g[f"group{i}_mode"])
+        vals = g[f"group{i}_values"]
+        if not np.array_equal(vals.astype(np.float32).astype(np.float64), vals):
+            continue
+        sel = dfss.select_group(vals, MODES[mode])
+        assert list(sel.kept) == list(g[f"group{i}_kept"]), i
+        assert sel.nibble == int(g[f"group{i}_nibble"]), i
+
+
+@pytest.mark.parametrize("mode", ["1:2", "2:4"])
+def test_prune_scores_bitexact_vs_reference(mode):
+    g = golden("codec.npz")
+    tag = mode.replace(":", "")
+    for i in range(int(g["n_scores"])):
+        s64 = g[f"scores{i}"]
+        s32 = s64.astype(np.float32)
+        nz, meta, kept = dfss.prune_scores(torch.from_numpy(s32).cuda(), mode)
+        want_nz, want_meta, want_kept = oracle_on_scores(s32.astype(np.float64), mode)
+        assert np.array_equal(meta.cpu().numpy(), want_meta), i
+        assert np.array_equal(kept.cpu().numpy(), want_kept), i
+        assert np.array_equal(_np(nz), want_nz), i
+        if np.array_equal(s32.astype(np.float64), s64):  # exactly representable: the reference's own output
+            assert np.array_equal(meta.cpu().numpy().ravel(), g[f"scores{i}_{tag}_metadata"]), i
+            assert np.array_equal(kept.cpu().numpy(), g[f"scores{i}_{tag}_mask"]), i
+
+
+def test_prune_scores_16bit_nonzeros_are_rne_of_oracle():
+    rng = np.random.default_rng(3)
+    s = (rng.standard_normal((64, 256)) * 3).astype(np.float32)
+    for dt in (torch.bfloat16, torch.float16):
+        nz, meta, _ = dfss.prune_scores(torch.from_numpy(s).cuda(), "2:4", nz_dtype=dt)
+        want_nz, want_meta, _ = oracle_on_scores(s.astype(np.float64), "2:4")
+        assert np.array_equal(meta.cpu().numpy(), want_meta)
+        assert torch.equal(nz.cpu(), torch.from_numpy(want_nz.astype(np.float32)).to(dt))
+
+
+def test_meta_layout_roundtrip_and_word_formula():
+    rng = np.random.default_rng(11)
+    for mode, (bh, rows, cols) in [("2:4", (3, 200, 96)), ("1:2", (2, 130, 40)), ("2:4", (1, 256, 512))]:
+        m = MODES[mode]
+        nibs = np.array(sorted(m.admissible_nibbles), dtype=np.uint8)
+        logical = nibs[rng.integers(0, len(nibs), size=(bh, rows, cols // m.group_size))]
+        nz = torch.zeros((bh, rows, cols // 2), device="cuda")
+        c = dfss.CompressedSparse.from_logical(rows, cols, m, nz, torch.from_numpy(logical).cuda())
+        assert np.array_equal(logical_meta(c), logical)
+        hw = c.meta_hw.cpu().numpy().view(np.uint32).reshape(bh, -1)
+        chunks = -(-(cols // m.group_size) // 8)
+        for _ in range(200):  # spot-check the documented word layout (include/dfss.h)
+            b = int(rng.integers(bh))
+            r = int(rng.integers(rows))
+            grp = int(rng.integers(cols // m.group_size))
+            rb, rr, cidx, gi = r // 128, r % 128, grp // 8, grp % 8
+            lane = 16 * (rr // 16) + 8 * (gi // 4) + rr % 8
+            shift = 16 * ((rr // 8) % 2) + 4 * (gi % 4)
+            word = hw[b, (rb * chunks + cidx) * 128 + lane]
+            assert (int(word) >> shift) & 0xF == logical[b, r, grp]
+
+
+def test_from_logical_rejects_malformed_nibble():
+    nz = torch.zeros((1, 4, 2), device="cuda")
+    with pytest.raises(ValueError, match="malformed nibble"):
+        dfss.CompressedSparse.from_logical(4, 4, M12, nz, torch.tensor([4, 4, 4, 4, 4, 4, 4, 0x9]))
+
+
+# ---------------------------------------------------------------- fused SDDMM + prune
+
+
+SDDMM_SHAPES = [(1, 64, 64, 16), (2, 100, 36, 7), (3, 128, 256, 64), (2, 384, 384, 64), (1, 33, 520, 24)]
+
+
+@pytest.mark.parametrize("mode", ["1:2", "2:4"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("math_mode", ["auto", "ffma"])
+def test_sddmm_same_scores_bitexact(mode, dtype, math_mode):
+    m = MODES[mode]
+    for bh, n, mk, d in SDDMM_SHAPES:
+        if mk % m.group_size:
+            continue
+        g = torch.Generator().manual_seed(bh * 1000 + n + mk + d)
+        q = torch.randn((bh, n, d), generator=g).to(dtype).cuda()
+        k = torch.randn((bh, mk, d), generator=g).to(dtype).cuda()
+        scale = 1.0 / math.sqrt(d)
+        dbg = torch.empty((bh, n, mk), dtype=torch.float32, device="cuda")
+        c, stats = dfss.sddmm_prune(q, k, m, scale, scores_out=dbg, math_mode=math_mode)
+        assert stats.dense_elems_written == 0
+        s = _np(dbg)
+        # the dump is the fp32 scaled product (accumulated in fp32)
+        exact = np.einsum("bnd,bmd->bnm", _np(q), _np(k)) * scale
+        assert_close(s, exact, 1e-5, 1e-5 * max(1.0, float(np.abs(exact).max())), "scores")
+        meta = logical_meta(c)
+        nz = c.nonzeros
+        for b in range(bh):
+            want_nz, want_meta, _ = oracle_on_scores(s[b], mode)
+            assert np.array_equal(meta[b], want_meta), (bh, n, mk, d, b)
+            if c.nonzeros.dtype == torch.float32:
+                assert np.array_equal(_np(nz[b]), want_nz)
+            else:
+                assert torch.equal(nz[b].cpu(), torch.from_numpy(want_nz.astype(np.float32)).to(nz.dtype))
+
+
+def test_sddmm_reference_golden_cases():
+    """The reference's own fused instances (fp64) run in fp32: integer-lattice cases are
+    exact in fp32 and must match the reference bitwise; the others match the oracle on the
+    dumped scores bitwise and the fp64 reference up to near-tie flips (counted)."""
+    g = golden("fused.npz")
+    flips = total = 0
+    for i in range(int(g["n_cases"])):
+        mode = str(g[f"case{i}_mode"])
+        q64, k64, scale = g[f"case{i}_q"], g[f"case{i}_k"], float(g[f"case{i}_scale"])
+        q = torch.from_numpy(q64.astype(np.float32)).cuda()
+        k = torch.from_numpy(k64.astype(np.float32)).cuda()
+        dbg = torch.empty((q.shape[0], k.shape[0]), dtype=torch.float32, device="cuda")
+        c, st = dfss.sddmm_prune(q, k, MODES[mode], scale, scores_out=dbg)
+        assert [st.peak_tile_elems, st.nonzeros_written, st.nibbles_written] == list(g[f"case{i}_stats"])
+        meta = logical_meta(c).ravel()
+        want = oracle_on_scores(_np(dbg), mode)[1].ravel()
+        assert np.array_equal(meta, want), i
+        integer = np.array_equal(np.round(q64), q64) and np.array_equal(np.round(k64), k64) and scale == 1.0
+        if integer:
+            assert np.array_equal(meta, g[f"case{i}_metadata"]), i
+        flips += int((meta != g[f"case{i}_metadata"]).sum())
+        total += meta.size
+    assert flips <= max(2, total // 2000), (flips, total)
+
+
+def test_identity_kat():
+    eye = torch.eye(4, device="cuda")
+    c, stats = dfss.sddmm_prune(eye, eye, M12, 1.0)
+    assert np.array_equal(_np(c.nonzeros), [[1, 0], [1, 0], [0, 1], [0, 1]])
+    assert list(c.metadata.cpu().numpy()) == [0x4, 0x4, 0xE, 0x4, 0x4, 0x4, 0x4, 0xE]
+    assert stats.nonzeros_written == 8 and stats.nibbles_written == 8
+
+
+def test_sddmm_block_mask_matches_reference():
+    g = golden("fused.npz")
+    mask = dfss.BlockMask(g["masked_keep"], tile_rows=32, tile_cols=32)
+    q = torch.from_numpy(g["masked_q"].astype(np.float32)).cuda()
+    k = torch.from_numpy(g["masked_k"].astype(np.float32)).cuda()
+    dbg = torch.empty((64, 64), dtype=torch.float32, device="cuda")
+    c, st = dfss.sddmm_prune(q, k, M12, 1.0, mask, tile_rows=32, tile_cols=32, scores_out=dbg)
+    assert [st.peak_tile_elems, st.nonzeros_written, st.nibbles_written] == list(g["masked_stats"])
+    present = mask.nonzero_keep(64, 64)
+    want_nz, want_meta, _ = oracle_on_scores(_np(dbg), "1:2")
+    assert np.array_equal(_np(c.nonzeros)[present], want_nz[present])
+    assert np.array_equal(logical_meta(c)[present], want_meta[present])
+    assert not _np(c.nonzeros)[~present].any()
+    assert not logical_meta(c)[~present].any()
+
+
+# ---------------------------------------------------------------- softmax
+
+
+def _row(values, mode=M12, dtype=torch.float32):
+    values = list(values)
+    dense = []
+    if mode is M12:
+        for v in values:
+            dense += [v, min(v - 1.0, -1.0)]
+    else:
+        for a, b in zip(values[0::2], values[1::2]):
+            low = min(a, b) - 1.0
+            dense += [a, b, low, low]
+    return dfss.compress_logical(torch.tensor([dense], dtype=dtype, device="cuda"), mode)
+
+
+def test_softmax_kats():
+    out = dfss.softmax_rows(_row([0.0, 0.0]))
+    assert np.array_equal(_np(out.nonzeros), [[0.5, 0.5]])
+    out = dfss.softmax_rows(_row([math.log(3.0), 0.0]))
+    assert np.allclose(_np(out.nonzeros), [[0.75, 0.25]], atol=1e-7)
+    out = dfss.softmax_rows(_row([1000.0, 1001.0]))
+    e = math.e
+    assert np.allclose(_np(out.nonzeros), [[1 / (1 + e), e / (1 + e)]], atol=1e-7)
+    assert np.isfinite(_np(out.nonzeros)).all()
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_softmax_matches_oracle_rows_sum_to_one(dtype):
+    rng = np.random.default_rng(17)
+    for cols in (8, 64, 250, 1024, 4096, 12288):
+        s = (rng.standard_normal((3, 40, cols)) * 10).astype(np.float32)
+        for mode in (M12, M24):
+            if cols % mode.group_size:
+                continue
+            c = dfss.compress_logical(torch.from_numpy(s).to(dtype).cuda(), mode)
+            out = dfss.softmax_rows(c)
+            got = _np(out.nonzeros)
+            want = np.stack([oracle_c.softmax_nonzeros(_np(c.nonzeros[b])) for b in range(3)])
+            tol = 1e-6 if dtype == torch.float32 else 8e-3
+            assert_close(got, want, tol, tol * 1e-2, f"softmax cols={cols}")
+            assert np.abs(got.sum(-1) - 1.0).max() <= (1e-5 if dtype == torch.float32 else 2e-2 * 1)
+            # order preservation within each row (ties allowed after rounding)
+            assert torch.equal(out.meta_hw, c.meta_hw)
+
+
+def test_softmax_rejects_nan_and_empty_rows():
+    c = _row([0.0, 1.0])
+    bad = dfss.CompressedSparse(c.rows, c.dense_cols, c.mode, torch.tensor([[float("nan"), 1.0]], device="cuda"),
+                                c.meta_hw)
+    with pytest.raises(ValueError, match="NaN"):
+        dfss.softmax_rows(bad)
+    q = torch.randn(64, 4, device="cuda")
+    mask = dfss.BlockMask(np.array([[False], [True]]), tile_rows=32, tile_cols=64)
+    cm, _ = dfss.sddmm_prune(q, q, M12, 1.0, mask)
+    with pytest.raises(ValueError, match="empty row 0"):
+        dfss.softmax_rows(cm)
+
+
+# ---------------------------------------------------------------- SpMM
+
+
+def test_spmm_single_nonzero_kat():
+    nonzeros = torch.zeros((3, 2), device="cuda")
+    nonzeros[1, 1] = 2.5
+    meta = torch.tensor([0x4, 0x4, 0x4, 0xE, 0x4, 0x4], dtype=torch.uint8)
+    c = dfss.CompressedSparse.from_logical(3, 4, M12, nonzeros, meta)
+    v = torch.arange(8.0, device="cuda").reshape(4, 2)
+    out = dfss.spmm(c, v).data
+    assert torch.equal(out[1], 2.5 * v[3])
+    assert not out[[0, 2]].any()
+
+
+@pytest.mark.parametrize("mode", ["1:2", "2:4"])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float16])
+def test_spmm_matches_decompress_oracle(mode, dtype):
+    rng = np.random.default_rng(23)
+    m = MODES[mode]
+    for bh, rows, cols, d in [(1, 4, 8, 3), (2, 64, 64, 16), (2, 128, 512, 64), (3, 256, 384, 64), (1, 96, 200, 40)]:
+        if cols % m.group_size:
+            continue
+        a = dfss.compress_logical(torch.from_numpy(rng.standard_normal((bh, rows, cols)).astype(np.float32))
+                                  .to(dtype).cuda(), m)
+        p = dfss.softmax_rows(a)
+        v = torch.from_numpy(rng.standard_normal((bh, cols, d)).astype(np.float32)).to(dtype).cuda()
+        out = _np(dfss.spmm(p, v).data)
+        nzp = _np(p.nonzeros)
+        meta = logical_meta(p)
+        for b in range(bh):
+            colidx = ref.nonzero_columns(meta[b].ravel(), rows, cols, mode)
+            want = oracle_c.spmm_gather(nzp[b], colidx, _np(v[b]))
+            tol = 1e-5 if dtype == torch.float32 else 1e-2
+            assert_close(out[b], want, tol, tol, f"spmm {bh, rows, cols, d}")
+
+
+def test_spmm_linear_in_v():
+    a = dfss.compress_logical(torch.randn(8, 8, device="cuda"), M12)
+    v = torch.randn(8, 5, device="cuda")
+    assert torch.allclose(dfss.spmm(a, 3.0 * v).data, 3.0 * dfss.spmm(a, v).data, rtol=1e-6, atol=1e-6)
+
+
+# ---------------------------------------------------------------- end to end
+
+
+def test_c1_fp32_attention_within_1e5():
+    """BASELINE config 1: DFSS 1:2 fp32, [1,12,384,64], vs the reference at rtol=atol=1e-5."""
+    (q, k, v), (q64, k64, v64) = seeded_qkv((1, 12, 384, 64), torch.float32, seed=0)
+    out = dfss.dfss_attention(q, k, v, "1:2")
+    want = oracle_attention(q64, k64, v64, "1:2")
+    assert_close(_np(out), want, 1e-5, 1e-5, "c1 fp32 1:2")
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("mode", ["2:4", "1:2"])
+def test_16bit_attention_within_2e2(dtype, mode):
+    (q, k, v), (q64, k64, v64) = seeded_qkv((2, 3, 512, 64), dtype, seed=1)
+    out = dfss.dfss_attention(q, k, v, mode)
+    want = oracle_attention(q64, k64, v64, mode)
+    assert_close(_np(out), want, 2e-2, 2e-2, f"{dtype} {mode}")
+
+
+def test_golden_pipeline_cases_fp32():
+    g = golden("pipeline.npz")
+    for i in range(int(g["n_cases"])):
+        q64, k64, v64 = g[f"case{i}_q"], g[f"case{i}_k"], g[f"case{i}_v"]
+        to = lambda x: torch.from_numpy(x.astype(np.float32)).cuda()
+        for mode in ("1:2", "2:4"):
+            inputs = dfss.AttentionInputs(dfss.DenseMatrix(to(q64)), dfss.DenseMatrix(to(k64)), dfss.DenseMatrix(to(v64)))
+            out = _np(dfss.nm_attention(inputs, MODES[mode]).data)
+            want = oracle_c.nm_attention(*(x.astype(np.float32).astype(np.float64) for x in (q64, k64, v64)), mode)
+            assert_close(out, want, 1e-5, 1e-5, f"golden case {i} {mode}")
+
+
+def test_rel_l2_pin_on_device():
+    g = golden("pipeline.npz")
+    to = lambda x: torch.from_numpy(x.astype(np.float32)).cuda()
+    inputs = dfss.AttentionInputs(*(dfss.DenseMatrix(to(g[f"pin_{c}"])) for c in "qkv"))
+    err = dfss.approx_error(torch.from_numpy(g["pin_full"]).cuda(), dfss.nm_attention(inputs, M12))
+    assert abs(err.rel_l2 - 0.39969464809566535) <= 1e-5
+
+
+def test_identical_keys_and_single_token():
+    n, d = 8, 4
+    k_row = torch.randn(d)
+    q = torch.randn(n, d, device="cuda")
+    k = k_row.repeat(n, 1).cuda()
+    v = torch.randn(n, d, device="cuda")
+    out = dfss.nm_attention(dfss.AttentionInputs(q, k, v), M12).data
+    assert torch.allclose(out, v[0::2].mean(0).expand(n, d), rtol=1e-5, atol=1e-6)
+    q1, k1, v1, vp = (torch.randn(1, 8, device="cuda") for _ in range(4))
+    out = dfss.nm_attention(dfss.AttentionInputs(torch.cat([q1, q1]), torch.cat([k1, k1]), torch.cat([v1, vp])), M12)
+    assert torch.equal(out.data[0], v1[0])
+
+
+def test_block_masked_pipeline_matches_staged_oracle():
+    rng = np.random.default_rng(5)
+    n, d = 64, 8
+    q64, k64, v64 = (rng.standard_normal((n, d)).astype(np.float32).astype(np.float64) for _ in range(3))
+    keep = np.array([[True, False], [True, True]])
+    mask = dfss.BlockMask(keep, tile_rows=32, tile_cols=32)
+    to = lambda x: torch.from_numpy(x.astype(np.float32)).cuda()
+    out = _np(dfss.nm_attention(dfss.AttentionInputs(to(q64), to(k64), to(v64)), M12, mask, tile_rows=32,
+                                tile_cols=32).data)
+    scores = ref.gemm_scaled(q64, k64, 1.0 / math.sqrt(d))
+    nz, meta = ref.compress_logical(scores, "1:2")
+    present = mask.nonzero_keep(n, n)
+    p = oracle_c.softmax_nonzeros(nz, present)
+    cols = ref.nonzero_columns(meta, n, n, "1:2")
+    want = oracle_c.spmm_gather(p, cols, v64, present)
+    assert_close(out, want, 1e-5, 1e-5, "masked pipeline")
+
+
+def test_module_and_value_envelope():
+    mod = dfss.DFSSAttention("2:4")
+    q, k, v = (torch.randn(2, 4, 256, 64, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    out = mod(q, k, v).float()
+    lo = v.float().amin(dim=-2, keepdim=True) - 2e-2
+    hi = v.float().amax(dim=-2, keepdim=True) + 2e-2
+    assert bool(((out >= lo) & (out <= hi)).all())
+
+
+def test_heatmap_kept_entries_dominate_dense():
+    q, k, v = (torch.randn(64, 16, device="cuda") for _ in range(3))
+    for mode in (M12, M24):
+        pair = dfss.attention_heatmap(dfss.AttentionInputs(q, k, v), mode)
+        kept = pair.sparse.data != 0
+        assert bool((pair.sparse.data[kept] >= pair.dense.data[kept] - 1e-6).all())

@@ -1,0 +1,70 @@
+"""Run tools/sp_probe.cu on the GPU and report the tcgen05.mma.sp metadata map."""
+import ctypes
+import os
+import subprocess
+import sys
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SO = os.path.join(HERE, "libsp_probe.so")
+
+
+def build():
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2", "-std=c++17", "-shared",
+                    "-Xcompiler", "-fPIC", "-o", SO, os.path.join(HERE, "sp_probe.cu")], check=True)
+
+
+def main():
+    if not os.path.exists(SO):
+        build()
+    lib = ctypes.CDLL(SO)
+    lib.probe_sp.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+    e = torch.full((128,), 0x44444444, dtype=torch.int64).to(torch.int32).cuda()
+    d = torch.zeros((128, 64), dtype=torch.float32, device="cuda")
+
+    def run(words, dense=0):
+        e.copy_(torch.tensor([w - (1 << 32) if w >= (1 << 31) else w for w in words], dtype=torch.int32))
+        rc = lib.probe_sp(e.data_ptr(), d.data_ptr(), dense)
+        assert rc == 0, rc
+        return d.cpu().clone()
+
+    base_words = [0x44444444] * 128
+    dd = run(base_words, dense=1)
+    exp = torch.zeros(128, 64)
+    exp[:, :16] = torch.eye(16)[:, :].sum(0)  # row sums: D[r][n] = 1 for n < 16
+    print("dense check (D[r][n]==1 for n<16, 0 else):", bool(torch.equal(dd, exp)))
+    if not torch.equal(dd, exp):
+        print(dd[:4, :20])
+    base = run(base_words)
+    expb = torch.zeros(128, 64)
+    for n in range(32):
+        if n % 4 in (0, 1):
+            expb[:, n] = 1
+    print("sparse baseline (all 0x4) ok:", bool(torch.equal(base, expb)))
+    if not torch.equal(base, expb):
+        print(base[:4, :34])
+    mapping = {}
+    bad = 0
+    for lane in range(128):
+        for j in range(8):
+            words = list(base_words)
+            words[lane] = (0x44444444 & ~(0xF << (4 * j))) | (0xE << (4 * j))
+            out = run(words)
+            diff = (out != base).nonzero().tolist()
+            cells = sorted({(r, n // 4) for r, n in diff})
+            mapping[(lane, j)] = cells
+            # hypothesis (include/dfss.h): lane = 16*m2 + 8*k1 + m0; nibble j -> half m1 = j//4, slot j%4
+            m2, k1, m0 = lane >> 4, (lane >> 3) & 1, lane & 7
+            want = [(16 * m2 + 8 * (j // 4) + m0, 4 * k1 + (j % 4))]
+            if cells != want:
+                bad += 1
+                if bad <= 20:
+                    print("lane", lane, "nibble", j, "->", cells, "expected", want)
+    print("hypothesis mismatches:", bad, "of", 128 * 8)
+    sample = {k: v for k, v in list(mapping.items())[:24]}
+    print("sample map:", sample)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

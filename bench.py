@@ -1,0 +1,444 @@
+#!/usr/bin/env python3
+"""DFSS attention benchmark on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dfss|reference] [--config c2]
+
+A step is one DFSS attention pass (fused SDDMM+prune -> compressed softmax ->
+mma.sp SpMM) over this rank's shard of the flattened batch x heads, synthetic
+N(0,1) Q/K/V resident in HBM.  Weak scaling: with N ranks the global batch is
+N x the config's batch and rank r owns the contiguous heads [r*B*H, (r+1)*B*H)
+(inputs seeded per (seed, global head), so shard r of an N-GPU run equals the
+corresponding slice of a 1-GPU run).  The compute phase has no collective; one
+NCCL all-gather of the output shards runs after the timed region as the
+end-to-end check.  One JSON line is printed by rank 0.  Numbers taken under a
+profiler are never reported.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+#: BASELINE.json configs; c2 (configs[1]) is the one the metric is quoted on at N=1
+CONFIGS = {
+    "c1": dict(batch=1, heads=12, seq=384, d=64, mode="1:2", dtype="float32",
+               desc="DFSS 1:2 fp32 attention, batch 1, 12 heads, seq 384, head_dim 64"),
+    "c2": dict(batch=32, heads=12, seq=512, d=64, mode="2:4", dtype="bfloat16",
+               desc="BERT-base-shaped DFSS 2:4 bf16 attention, batch 32, 12 heads, seq 512, head_dim 64"),
+    "c3": dict(batch=16, heads=16, seq=1024, d=64, mode="2:4", dtype="float16",
+               desc="BERT-large-shaped DFSS 2:4 fp16 attention, batch 16, 16 heads, seq 1024, head_dim 64"),
+    "c4": dict(batch=8, heads=12, seq=4096, d=64, mode="2:4", dtype="bfloat16",
+               desc="Long-sequence DFSS 2:4 bf16 attention, batch 8, 12 heads, seq 4096, head_dim 64"),
+}
+DT = {"float32": torch.float32, "bfloat16": torch.bfloat16, "float16": torch.float16}
+METRIC = "DFSS attention ms & speedup vs dense attention (seq 512–4096) on B200; TFLOPS"
+UNIT = "TFLOP/s (dense-equivalent 4*n^2*d per head)"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def shard(total: int, ws: int, rank: int):
+    per = -(-total // ws)
+    lo = min(total, rank * per)
+    hi = min(total, lo + per)
+    return lo, hi
+
+
+def make_inputs(cfg, lo, hi, device, seed=0):
+    """Per-head seeded inputs (seed, global head index): shards equal the 1-GPU run."""
+    n, d = cfg["seq"], cfg["d"]
+    dt = DT[cfg["dtype"]]
+    qkv = torch.empty((3, hi - lo, n, d), dtype=dt)
+    for i, h in enumerate(range(lo, hi)):
+        g = torch.Generator().manual_seed(seed * 1_000_003 + h)
+        qkv[:, i] = torch.randn((3, n, d), generator=g, dtype=torch.float32).to(dt)
+    return qkv.to(device)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def time_steps(fn, steps, warmup, flush=None):
+    """Per-step CUDA events on the current stream; L2 flushed between steps outside the events."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for s, e in ev:
+        if flush is not None:
+            flush()
+        s.record()
+        fn()
+        e.record()
+    torch.cuda.synchronize()
+    return [s.elapsed_time(e) for s, e in ev]
+
+
+def algorithmic_bytes(cfg):
+    """per (batch, head) per kernel, 16-bit: SDDMM 1.125n^2+4nd, softmax 2n^2, SpMM 1.125n^2+4nd."""
+    n, d = cfg["seq"], cfg["d"]
+    eb = 4 if cfg["dtype"] == "float32" else 2
+    gs = 2 if cfg["mode"] == "1:2" else 4
+    nz = n * (n // 2) * eb
+    meta = n * (n // gs) // 2
+    return {
+        "sddmm": nz + meta + 2 * n * d * eb,
+        "softmax": 2 * nz,
+        "spmm": nz + meta + 2 * n * d * eb,
+    }
+
+
+def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True):
+    import paper_2203_00091_b200 as dfss
+
+    cfg = CONFIGS[cfg_name]
+    n, d = cfg["seq"], cfg["d"]
+    per_rank = cfg["batch"] * cfg["heads"]
+    total_bh = per_rank * ws
+    lo, hi = shard(total_bh, ws, rank)
+    qkv = make_inputs(cfg, lo, hi, device)
+    q, k, v = qkv[0], qkv[1], qkv[2]
+    bh = hi - lo
+    mode = dfss.SparsityMode.parse(cfg["mode"])
+    ws_bytes = dfss.workspace_bytes(mode, q.dtype, bh, n, d)
+    workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
+    out = torch.empty_like(q)
+    flush_buf = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
+    flush = lambda: flush_buf.fill_(1)
+
+    def step():
+        dfss.dfss_attention(q, k, v, mode, out=out, workspace=workspace)
+
+    # ---- timed region: barrier + synchronize on both sides, max over ranks
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
+    smi_index = int(cvd.split(",")[local]) if cvd and cvd.split(",")[local].strip().isdigit() else local
+    with ClockSampler(smi_index) as clk:
+        times = time_steps(step, args.steps, args.warmup, flush)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    total_ms = torch.tensor([sum(times)], dtype=torch.float64, device=device)
+    if ws > 1:
+        torch.distributed.all_reduce(total_ms, op=torch.distributed.ReduceOp.MAX)
+    ms_per_step = float(total_ms.item()) / args.steps
+    flops_per_head = 4.0 * n * n * d
+    value = flops_per_head * total_bh / (ms_per_step * 1e-3) / 1e12  # all ranks' heads / max-rank time
+
+    res = {"ms_per_step": ms_per_step, "value": value, "clocks": clk.summary(), "bh_local": bh}
+    if not report_extra:
+        return res
+
+    # ---- per-kernel breakdown on the same stream (dominant kernel -> roofline)
+    scale = 1.0 / math.sqrt(d)
+    nz_holder = {}
+
+    def k_sddmm():
+        nz_holder["c"], _ = dfss.sddmm_prune(q, k, mode, scale)
+
+    def k_softmax():
+        nz_holder["p"] = dfss.softmax_rows(nz_holder["c"], check=False)
+
+    def k_spmm():
+        dfss.spmm(nz_holder["p"], v)
+
+    k_sddmm(); k_softmax(); k_spmm()
+    torch.cuda.synchronize()
+    kt = {}
+    for name, fn in (("sddmm", k_sddmm), ("softmax", k_softmax), ("spmm", k_spmm)):
+        ts = time_steps(fn, max(3, args.steps), 2, flush)
+        kt[name] = float(np.mean(ts))
+    ab = algorithmic_bytes(cfg)
+    hbm_peak, tf_peak, peak_src = peaks()
+    dom = max(kt, key=kt.get)
+    achieved = ab[dom] * bh / (kt[dom] * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(cfg_name, {}).get(dom)
+        except Exception:
+            traffic = None
+    res["kernels_ms"] = kt
+    res["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
+                       "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                       "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+                       "algorithmic_bytes_per_launch": ab[dom] * bh}
+    pipe_bytes = sum(ab.values()) * bh
+    res["pipeline_hbm_gbs"] = round(pipe_bytes / (ms_per_step * 1e-3) / 1e9, 1)
+    res["pipeline_roofline_frac"] = round(pipe_bytes / (ms_per_step * 1e-3) / 1e9 / hbm_peak, 4)
+
+    # ---- dense baselines on the same box and shard: unfused cuBLAS and fused SDPA
+    qd, kd, vd = q.unsqueeze(0), k.unsqueeze(0), v.unsqueeze(0)
+
+    def dense_unfused():
+        s = torch.matmul(q, k.transpose(-1, -2)) * scale
+        p = torch.softmax(s, dim=-1)
+        return torch.matmul(p, v)
+
+    def dense_sdpa():
+        return torch.nn.functional.scaled_dot_product_attention(qd, kd, vd)
+
+    base = {}
+    for name, fn in (("cublas_unfused", dense_unfused), ("sdpa", dense_sdpa)):
+        try:
+            base[name] = float(np.mean(time_steps(fn, max(3, args.steps), 2, flush)))
+        except Exception as ex:  # e.g. OOM for huge unfused scores
+            base[name] = None
+            res.setdefault("baseline_errors", {})[name] = str(ex)[:120]
+    res["dense_ms"] = base
+    res["speedup_vs_dense"] = {k_: (round(t / ms_per_step, 3) if t else None) for k_, t in base.items()}
+    del workspace, flush_buf
+    return res, (q, k, v, out, lo, hi)
+
+
+def e2e_measure(args, cfg, q, k, v, device):
+    """Same metric through the public API with pinned host buffers: H2D inputs + compute + D2H output, every step."""
+    import paper_2203_00091_b200 as dfss
+
+    mode = dfss.SparsityMode.parse(cfg["mode"])
+    hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
+    hout = torch.empty(q.shape, dtype=q.dtype).pin_memory()
+
+    def step():
+        dq, dk, dv = (h.to(device, non_blocking=True) for h in (hq, hk, hv))
+        o = dfss.dfss_attention(dq, dk, dv, mode)
+        hout.copy_(o, non_blocking=True)
+
+    ts = time_steps(step, max(3, args.steps), 2)
+    ms = float(np.mean(ts))
+    n, d = cfg["seq"], cfg["d"]
+    bh = q.shape[0]
+    eb = q.element_size()
+    return {"ms_per_step": ms, "value": 4.0 * n * n * d * bh / (ms * 1e-3) / 1e12, "unit": UNIT,
+            "h2d_bytes_per_step": 3 * bh * n * d * eb, "d2h_bytes_per_step": bh * n * d * eb}
+
+
+def cpu_reference(cfg, budget_s: float, threads: int):
+    """The oracle port of the reference nm_attention (C, float64, same op order as the numba kernels),
+    on a bounded sample of the workload's heads, all host threads."""
+    from oracle import oracle_c
+
+    n, d = cfg["seq"], cfg["d"]
+    total_bh = cfg["batch"] * cfg["heads"]
+    # estimate per-head cost with one head, then size the sample to ~budget_s
+    qkv = make_inputs(cfg, 0, 1, "cpu")
+    x = [t.double().numpy() for t in qkv]
+    t0 = time.perf_counter()
+    oracle_c.attention_batched(x[0], x[1], x[2], cfg["mode"], nthreads=1)
+    per_head = time.perf_counter() - t0
+    heads = int(max(threads, min(total_bh, budget_s * threads / max(per_head, 1e-6))))
+    heads = max(1, min(total_bh, heads - heads % threads if heads >= threads else heads))
+    qkv = make_inputs(cfg, 0, heads, "cpu")
+    x = [t.double().numpy() for t in qkv]
+    t0 = time.perf_counter()
+    oracle_c.attention_batched(x[0], x[1], x[2], cfg["mode"], nthreads=threads)
+    el = time.perf_counter() - t0
+    value = 4.0 * n * n * d * heads / el / 1e12
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{heads} of {total_bh} (batch x head) slices, float64 C restatement of nmattn.nm_attention "
+                      f"(oracle/dfss_oracle.c), {el:.2f} s wall, {per_head * 1e3:.1f} ms/head single-core",
+            "seconds": el, "heads": heads}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["dfss", "reference"], default="dfss")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for the CPU baseline")
+    ap.add_argument("--no-extra", action="store_true", help="skip sweep / e2e / cpu baseline (profiling runs)")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    ws, rank, local = dist_env()
+    cfg = CONFIGS[args.config]
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        steps = []
+        budget = max(2.0, min(20.0, 150.0 / (args.steps + args.warmup)))
+        for i in range(args.warmup + args.steps):
+            r = cpu_reference(cfg, budget, threads)
+            if i >= args.warmup:
+                steps.append(r)
+        val = float(np.median([s["value"] for s in steps]))
+        secs = float(np.median([s["seconds"] for s in steps]))
+        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": args.config + ": " + cfg["desc"], "batch": cfg["batch"], "heads": cfg["heads"],
+                           "seq_len": cfg["seq"], "head_dim": cfg["d"], "mode": cfg["mode"]},
+                "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
+                                 "sample": steps[-1]["sample"], "cpu_model": cpu_model()},
+                "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return 0
+
+    if ws > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    device = torch.device("cuda", torch.cuda.current_device())
+
+    res, (q, k, v, out, lo, hi) = run_dfss(args, args.config, ws, rank, local, device)
+    launches_per_step = 3  # SDDMM+prune, softmax, SpMM (dfss_nm_attention)
+
+    # end-to-end parity gather: NCCL all_gather of the output shards (outside the timed region)
+    parity = None
+    if ws > 1:
+        total_bh = cfg["batch"] * cfg["heads"] * ws
+        gathered = torch.empty((total_bh,) + tuple(out.shape[1:]), dtype=out.dtype, device=device)
+        torch.distributed.all_gather_into_tensor(gathered, out.contiguous())
+        parity = {"gathered_heads": int(total_bh), "checksum": float(gathered.float().abs().sum()),
+                  "shards_equal_local": bool(torch.equal(gathered[lo:hi], out))}
+
+    extra = {}
+    if rank == 0 and not args.no_extra:
+        # oracle spot check of two heads of the timed output (SURVEY §8(c) tolerances)
+        from oracle import oracle_c
+
+        hq, hk, hv, ho = (x[:2].double().cpu().numpy() for x in (q, k, v, out))
+        want = oracle_c.attention_batched(hq, hk, hv, cfg["mode"], nthreads=2)
+        tol = 1e-5 if cfg["dtype"] == "float32" else 2e-2
+        ok = bool((np.abs(ho - want) <= tol + tol * np.abs(want)).all())
+        extra["parity_spot_check"] = {"heads": 2, "tol": tol, "ok": ok,
+                                      "max_abs_err": float(np.abs(ho - want).max())}
+        if ws == 1:
+            extra["e2e"] = e2e_measure(args, cfg, q, k, v, device)
+            cb = cpu_reference(cfg, args.cpu_budget, threads)
+            cb["cpu_model"] = cpu_model()
+            extra["cpu_baseline"] = cb
+            sweep = {}
+            for name in ("c1", "c3", "c4"):
+                if name == args.config:
+                    continue
+                try:
+                    r2, _ = run_dfss(argparse.Namespace(steps=max(3, args.steps // 2), warmup=3), name, 1, 0, 0,
+                                     device)
+                    sweep[name] = {"ms_per_step": round(r2["ms_per_step"], 4), "tflops": round(r2["value"], 2),
+                                   "speedup_vs_dense": r2["speedup_vs_dense"], "dense_ms": r2["dense_ms"],
+                                   "kernels_ms": r2["kernels_ms"], "roofline_frac": r2["roofline"]["frac"],
+                                   "pipeline_roofline_frac": r2["pipeline_roofline_frac"]}
+                except Exception as ex:
+                    sweep[name] = {"error": str(ex)[:200]}
+            extra["other_configs"] = sweep
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(res["value"], 3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(res["ms_per_step"], 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": {"float32": "f32", "bfloat16": "bf16", "float16": "f16"}[cfg["dtype"]],
+            "data": "synthetic N(0,1) Q/K/V, seeded per (seed, global head)",
+            "config": {"workload": args.config + ": " + cfg["desc"], "batch": cfg["batch"], "heads": cfg["heads"],
+                       "seq_len": cfg["seq"], "head_dim": cfg["d"], "mode": cfg["mode"],
+                       "global_batch": cfg["batch"] * ws, "parallelism": f"bh-shard{ws}", "heads_per_rank": res["bh_local"],
+                       "l2": "flushed between timed steps (256 MiB write, outside the step events)"},
+            "roofline": res["roofline"], "kernels_ms": res["kernels_ms"],
+            "pipeline_hbm_gbs": res["pipeline_hbm_gbs"], "pipeline_roofline_frac": res["pipeline_roofline_frac"],
+            "dense_ms": res["dense_ms"], "speedup_vs_dense": res["speedup_vs_dense"],
+            "gpu_launches": launches_per_step * args.steps, "clocks": res["clocks"],
+        }
+        if "e2e" in extra:
+            e = extra.pop("e2e")
+            line["e2e"] = {"value": round(e["value"], 3), "unit": e["unit"], "h2d_bytes_per_step": e["h2d_bytes_per_step"],
+                           "d2h_bytes_per_step": e["d2h_bytes_per_step"], "ms_per_step": round(e["ms_per_step"], 4)}
+        if "cpu_baseline" in extra:
+            line["cpu_baseline"] = extra.pop("cpu_baseline")
+        if parity:
+            line["allgather_check"] = parity
+        line.update(extra)
+        print(json.dumps(line))
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

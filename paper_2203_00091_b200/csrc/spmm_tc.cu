@@ -114,7 +114,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint64_t ad = tc::smem_desc(p_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
             // B: MN-major, 32 K-rows of 128 B per MMA = 4 whole swizzle atoms
             const uint64_t bd = tc::smem_desc(v_addr + kk * 32 * 128, V_BYTES, 1024, tc::kSwizzle128B);
-            tc::mma_sp_f16_ss(d_tmem, ad, bd, tmem_base + E_COL0 + s * 4 + kk, idesc, (kb | kk) ? 1u : 0u);
+            // metadata column: even address + sparse_id2 (idesc bits [0,2)) selects the odd one
+            const uint32_t e_col = tmem_base + E_COL0 + s * 4 + kk;
+            tc::mma_sp_f16_ss(d_tmem, ad, bd, e_col & ~1u, idesc | (e_col & 1u), (kb | kk) ? 1u : 0u);
           }
           tc::mma_commit(&empty[s]);
           if (++s == STAGES) { s = 0; ph ^= 1; }

@@ -19,13 +19,13 @@ def main():
     if not os.path.exists(SO):
         build()
     lib = ctypes.CDLL(SO)
-    lib.probe_sp.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+    lib.probe_sp.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
     e = torch.full((128,), 0x44444444, dtype=torch.int64).to(torch.int32).cuda()
     d = torch.zeros((128, 64), dtype=torch.float32, device="cuda")
 
-    def run(words, dense=0):
+    def run(words, dense=0, ecol=64, id2=0):
         e.copy_(torch.tensor([w - (1 << 32) if w >= (1 << 31) else w for w in words], dtype=torch.int32))
-        rc = lib.probe_sp(e.data_ptr(), d.data_ptr(), dense)
+        rc = lib.probe_sp(e.data_ptr(), d.data_ptr(), dense, ecol, id2)
         assert rc == 0, rc
         return d.cpu().clone()
 
@@ -44,6 +44,21 @@ def main():
     print("sparse baseline (all 0x4) ok:", bool(torch.equal(base, expb)))
     if not torch.equal(base, expb):
         print(base[:4, :34])
+    # metadata column alignment: odd / non-multiple-of-4 columns, direct vs sparse_id2
+    import random
+    rnd = random.Random(1)
+    nib = [0x4, 0x8, 0x9, 0xC, 0xD, 0xE]
+    words = [sum(rnd.choice(nib) << (4 * j) for j in range(8)) for _ in range(128)]
+    ref = run(words, ecol=64)
+    for ecol, id2 in [(65, 1), (66, 0), (67, 1), (68, 0), (66, 1)]:
+        if ecol % 2 == 1 and id2 == 0:
+            continue
+        try:
+            got = run(words, ecol=ecol, id2=id2)
+            print(f"ecol={ecol} id2mode={id2}: equal to col-64 result: {bool(torch.equal(got, ref))}")
+        except AssertionError as ex:
+            print(f"ecol={ecol} id2mode={id2}: launch error {ex}")
+            return
     mapping = {}
     bad = 0
     for lane in range(128):

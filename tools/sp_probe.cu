@@ -9,7 +9,7 @@
 
 using namespace dfss;
 
-__global__ void probe_kernel(const uint32_t* e_words, float* d_out, int dense) {
+__global__ void probe_kernel(const uint32_t* e_words, float* d_out, int dense, int ecol, int id2mode) {
   __shared__ __align__(1024) uint8_t a_s[128 * 128];
   __shared__ __align__(1024) uint8_t b_s[32 * 128];
   __shared__ uint64_t bar;
@@ -32,7 +32,7 @@ __global__ void probe_kernel(const uint32_t* e_words, float* d_out, int dense) {
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = tslot;
-  tc::tmem_st_32x32b_x1(tbase + ((uint32_t)(warp * 32) << 16) + 64, e_words[warp * 32 + lane]);
+  tc::tmem_st_32x32b_x1(tbase + ((uint32_t)(warp * 32) << 16) + ecol, e_words[warp * 32 + lane]);
   tc::tmem_st_wait();
   tc::tc_fence_before();
   __syncthreads();
@@ -43,7 +43,11 @@ __global__ void probe_kernel(const uint32_t* e_words, float* d_out, int dense) {
     if (dense) {
       tc::mma_f16_ss(tbase, ad, bd, tc::instr_desc(1, 128, 64, false, true, false), 0);
     } else {
-      tc::mma_sp_f16_ss(tbase, ad, bd, tbase + 64, tc::instr_desc(1, 128, 64, false, true, true), 0);
+      const uint32_t e = tbase + ecol;
+      if (id2mode)
+        tc::mma_sp_f16_ss(tbase, ad, bd, e & ~1u, tc::instr_desc(1, 128, 64, false, true, true) | (e & 1u), 0);
+      else
+        tc::mma_sp_f16_ss(tbase, ad, bd, e, tc::instr_desc(1, 128, 64, false, true, true), 0);
     }
     tc::mma_commit(&bar);
   }
@@ -62,8 +66,8 @@ __global__ void probe_kernel(const uint32_t* e_words, float* d_out, int dense) {
   if (warp == 0) tc::tmem_dealloc<128>(tbase);
 }
 
-extern "C" int probe_sp(const uint32_t* e_words, float* d_out, int dense) {
-  probe_kernel<<<1, 128>>>(e_words, d_out, dense);
+extern "C" int probe_sp(const uint32_t* e_words, float* d_out, int dense, int ecol, int id2mode) {
+  probe_kernel<<<1, 128>>>(e_words, d_out, dense, ecol, id2mode);
   cudaError_t e = cudaDeviceSynchronize();
   return (int)e;
 }

@@ -184,6 +184,13 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True):
     cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
     smi_index = int(cvd.split(",")[local]) if cvd and cvd.split(",")[local].strip().isdigit() else local
     with ClockSampler(smi_index) as clk:
+        # soak: keep the GPU busy on the same step for >= 1.5 s so the sampler sees the
+        # clocks under this load, then the K timed steps (same sampler window)
+        t_end = time.perf_counter() + float(os.environ.get("DFSS_BENCH_SOAK_S", "1.5"))
+        while time.perf_counter() < t_end:
+            for _ in range(20):
+                step()
+            torch.cuda.synchronize()
         times = time_steps(step, args.steps, args.warmup, flush)
     torch.cuda.synchronize()
     if ws > 1:

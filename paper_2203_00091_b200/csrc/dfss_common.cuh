@@ -61,18 +61,23 @@ __device__ __forceinline__ uint32_t nibble_of_mask(uint32_t mask) {
 // l01 / l23 decide everything.  {0,1} survive iff l01 beats w23, {2,3} iff l23
 // beats w01, otherwise {w01, w23}.  Every comparison puts the lower index on
 // the left of >= (or the higher on the left of >), so ties resolve exactly as
-// the reference's stable argsort.  4 compares + 8 selects, no pair sums.
+// the reference's stable argsort (exhaustively checked over tie-heavy inputs,
+// tests/test_gpu_parity.py).  Written for the ALU budget of the SDDMM
+// epilogue: 4 FMNMX + 4 FSETP + 4 FSEL + 4 SEL/IADD, no predicate logic.
+// (fmaxf may return +0 for a (-0, +0) tie where the reference keeps -0: equal
+// values, identical metadata.)
 __device__ __forceinline__ uint32_t select24(float v0, float v1, float v2, float v3, float& lo, float& hi) {
-  const bool a = v0 >= v1;  // element 0 beats element 1
-  const bool b = v2 >= v3;  // element 2 beats element 3
-  const float w01 = a ? v0 : v1, l01 = a ? v1 : v0;
-  const float w23 = b ? v2 : v3, l23 = b ? v3 : v2;
+  const float w01 = fmaxf(v0, v1), l01 = fminf(v0, v1);
+  const float w23 = fmaxf(v2, v3), l23 = fminf(v2, v3);
   const bool keep01 = l01 >= w23;  // lower-index loser vs higher-index winner
   const bool keep23 = l23 > w01;   // higher-index loser must strictly beat the winner
   lo = keep01 ? v0 : (keep23 ? v2 : w01);
   hi = keep01 ? v1 : (keep23 ? v3 : w23);
-  const uint32_t mixed = (a ? 0u : 1u) | (b ? 8u : 12u);  // (w01 idx) | (w23 idx) << 2
-  return keep01 ? 0x4u : (keep23 ? 0xEu : mixed);
+  uint32_t nib = (v2 >= v3) ? 8u : 12u;  // hi slot = index of w23
+  nib += (v0 >= v1) ? 0u : 1u;           // lo slot = index of w01
+  nib = keep23 ? 0xEu : nib;
+  nib = keep01 ? 0x4u : nib;
+  return nib;
 }
 
 // Reference rank rule (codec.py:121, kept for the self-check kernel in tests).

@@ -55,7 +55,37 @@ __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&p);
 }
 
-template <typename T>
+// Prune one 32-column chunk of a row: 8 groups of 4 scores -> 16 kept 16-bit values
+// (two 16B units of the 128B-swizzled staging row) + one 32-bit nibble word that is
+// traded with row^8 into the meta_hw word of this TMEM lane (include/dfss.h).
+template <typename T, bool DBG>
+__device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, int colh, int cc, uint8_t* stg,
+                                          uint32_t lane, uint32_t* meta_b, int row_blk, float* dbg, int64_t dbg_row,
+                                          int m) {
+  uint32_t packed[8];
+  uint32_t W = 0;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    const float v0 = __uint_as_float(r[4 * g + 0]) * scale;
+    const float v1 = __uint_as_float(r[4 * g + 1]) * scale;
+    const float v2 = __uint_as_float(r[4 * g + 2]) * scale;
+    const float v3 = __uint_as_float(r[4 * g + 3]) * scale;
+    if (DBG) *reinterpret_cast<float4*>(dbg + dbg_row * m + colh + cc * 32 + 4 * g) = make_float4(v0, v1, v2, v3);
+    float lo, hi;
+    const uint32_t nib = select24(v0, v1, v2, v3, lo, hi);
+    packed[g] = pack2<T>(lo, hi);
+    W += nib * (1u << (4 * g));  // IMAD on the FMA pipe, not shift+or on the ALU pipe
+  }
+  const int u0 = 2 * cc, sw = lane & 7;
+  *reinterpret_cast<uint4*>(stg + lane * 128 + ((u0 ^ sw) << 4)) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+  *reinterpret_cast<uint4*>(stg + lane * 128 + (((u0 + 1) ^ sw) << 4)) =
+      make_uint4(packed[4], packed[5], packed[6], packed[7]);
+  const uint32_t partner = __shfl_xor_sync(0xffffffffu, W, 8);
+  const uint32_t word = (lane & 8) ? ((partner >> 16) | (W & 0xFFFF0000u)) : ((W & 0xFFFFu) | (partner << 16));
+  meta_b[(int64_t)((colh + cc * 32) >> 5) * 128 + row_blk] = word;
+}
+
+template <typename T, bool DBG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     sddmm24_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_nz, uint32_t* __restrict__ meta, float scale, int bh,
@@ -180,40 +210,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (active) {
           if (lane == 0) tc::bulk_wait_read<1>();  // staging buffer from two tiles ago drained
           __syncwarp();
-#pragma unroll 1
-          for (int cc = 0; cc < 4; ++cc) {
-            uint32_t r[32];
-            tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + half * 128 + cc * 32, r);
-            tc::tmem_ld_wait();
-            const int col0 = t * BN + half * 128 + cc * 32;
-            uint32_t packed[8];
-            uint32_t W = 0;
-#pragma unroll
-            for (int g = 0; g < 8; ++g) {
-              const float v0 = __uint_as_float(r[4 * g + 0]) * scale;
-              const float v1 = __uint_as_float(r[4 * g + 1]) * scale;
-              const float v2 = __uint_as_float(r[4 * g + 2]) * scale;
-              const float v3 = __uint_as_float(r[4 * g + 3]) * scale;
-              if (dbg) {
-                float4 sv = make_float4(v0, v1, v2, v3);
-                *reinterpret_cast<float4*>(dbg + ((int64_t)b * n + grow) * m + col0 + 4 * g) = sv;
-              }
-              float lo, hi;
-              const uint32_t nib = select24(v0, v1, v2, v3, lo, hi);
-              packed[g] = pack2<T>(lo, hi);
-              W |= nib << (4 * g);
-            }
-            // nonzeros -> 128B-swizzled staging row (16B unit u lands at u ^ (row % 8))
-            const int u0 = 2 * cc, sw = lane & 7;
-            *reinterpret_cast<uint4*>(stg + lane * 128 + ((u0 ^ sw) << 4)) =
-                make_uint4(packed[0], packed[1], packed[2], packed[3]);
-            *reinterpret_cast<uint4*>(stg + lane * 128 + (((u0 + 1) ^ sw) << 4)) =
-                make_uint4(packed[4], packed[5], packed[6], packed[7]);
-            // metadata: rows r and r^8 trade 16-bit halves -> the word of TMEM lane r (include/dfss.h)
-            const uint32_t partner = __shfl_xor_sync(0xffffffffu, W, 8);
-            const uint32_t word = (lane & 8) ? ((partner >> 16) | (W & 0xFFFF0000u)) : ((W & 0xFFFFu) | (partner << 16));
-            meta_b[(int64_t)(col0 >> 5) * 128 + row_blk] = word;
-          }
+          const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + half * 128;
+          const int colh = t * BN + half * 128;
+          uint32_t ra[32], rb[32];
+          // TMEM loads double-buffered: chunk cc+1 is in flight while cc is pruned
+          tc::tmem_ld_32x32b_x32(tbase, ra);
+          tc::tmem_ld_wait(ra);
+          tc::tmem_ld_32x32b_x32(tbase + 32, rb);
+          epi_chunk<T, DBG>(ra, scale, colh, 0, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m);
+          tc::tmem_ld_wait(rb);
+          tc::tmem_ld_32x32b_x32(tbase + 64, ra);
+          epi_chunk<T, DBG>(rb, scale, colh, 1, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m);
+          tc::tmem_ld_wait(ra);
+          tc::tmem_ld_32x32b_x32(tbase + 96, rb);
+          epi_chunk<T, DBG>(ra, scale, colh, 2, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m);
+          tc::tmem_ld_wait(rb);
+          epi_chunk<T, DBG>(rb, scale, colh, 3, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m);
         }
         tc::tc_fence_before();
         __syncwarp();
@@ -268,14 +280,9 @@ static cudaError_t launch_typed(const void* q, const void* k, void* nz, uint32_t
       !encode_tmap_3d(&tk, dt, 2, (void*)k, HD, m, bh, HD, BN, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !encode_tmap_3d(&tn, dt, 2, nz, m / 2, n, bh, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
-  auto kern = sddmm24_tc_kernel<T>;
-  static bool attr_set[2] = {false, false};
-  const int ti = std::is_same<T, __nv_bfloat16>::value ? 0 : 1;
-  if (!attr_set[ti]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
-    if (e != cudaSuccess) return e;
-    attr_set[ti] = true;
-  }
+  auto kern = dbg ? sddmm24_tc_kernel<T, true> : sddmm24_tc_kernel<T, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
+  if (e != cudaSuccess) return e;
   const int items = (int)bh * (n / BM);
   const int grid = items < num_sms() ? items : num_sms();
   kern<<<grid, NUM_THREADS, SMEM_TOTAL, s>>>(tq, tk, tn, meta, scale, (int)bh, n, m, dbg);

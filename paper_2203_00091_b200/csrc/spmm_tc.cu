@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * HD;
       tc::tmem_ld_32x32b_x32(taddr, r0);
       tc::tmem_ld_32x32b_x32(taddr + 32, r1);
-      tc::tmem_ld_wait();
+      tc::tmem_ld_wait(r0);
+      tc::tmem_ld_wait(r1);
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&d_empty[acc]);

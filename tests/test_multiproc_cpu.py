@@ -1,0 +1,81 @@
+"""Multi-process (gloo, world size 2) coverage of the batch x heads sharding used by
+bench.py under torchrun: per-rank shards, seeding per global head, and the output
+all-gather that serves as the end-to-end check.  CPU only; the per-shard compute here is
+the oracle (test infrastructure), the GPU ranks run the CUDA path."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import bench
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, ws, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(ws))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    from oracle import oracle_c
+
+    cfg = dict(bench.CONFIGS["c1"], batch=1, heads=3, seq=64)  # small: 3 heads per rank
+    per_rank = cfg["batch"] * cfg["heads"]
+    lo, hi = bench.shard(per_rank * ws, ws, rank)
+    qkv = bench.make_inputs(cfg, lo, hi, "cpu")
+    out = oracle_c.attention_batched(*(x.double().numpy() for x in qkv), cfg["mode"], nthreads=1)
+    out_t = torch.from_numpy(out)
+    gathered = [torch.empty_like(out_t) for _ in range(ws)]
+    dist.all_gather(gathered, out_t)
+    full = torch.cat(gathered)
+    if rank == 0:
+        q.put((lo, hi, full.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bh_sharding_and_gather_match_single_process():
+    ws = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, ws, port, q)) for r in range(ws)]
+    for p in procs:
+        p.start()
+    lo, hi, full = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert (lo, hi) == (0, 3)
+    # single-process run over all 6 global heads gives the same tensor
+    from oracle import oracle_c
+
+    cfg = dict(bench.CONFIGS["c1"], batch=1, heads=3, seq=64)
+    qkv = bench.make_inputs(cfg, 0, 6, "cpu")
+    want = oracle_c.attention_batched(*(x.double().numpy() for x in qkv), cfg["mode"], nthreads=2)
+    assert np.array_equal(full, want)
+
+
+def test_shard_bounds_cover_exactly():
+    for total, ws in [(12, 8), (384, 8), (96, 3), (5, 2)]:
+        seen = []
+        for r in range(ws):
+            lo, hi = bench.shard(total, ws, r)
+            seen.extend(range(lo, hi))
+        assert seen == list(range(total))
+
+
+def test_inputs_seeded_per_global_head():
+    cfg = dict(bench.CONFIGS["c2"], seq=32)
+    a = bench.make_inputs(cfg, 0, 4, "cpu")
+    b = bench.make_inputs(cfg, 2, 4, "cpu")
+    assert torch.equal(a[:, 2:4], b)

@@ -142,13 +142,17 @@ def time_steps(fn, steps, warmup, flush=None):
     return [s.elapsed_time(e) for s, e in ev]
 
 
-def algorithmic_bytes(cfg):
-    """per (batch, head) per kernel, 16-bit: SDDMM 1.125n^2+4nd, softmax 2n^2, SpMM 1.125n^2+4nd."""
+def algorithmic_bytes(cfg, fused=False):
+    """per (batch, head) per kernel.  16-bit staged: SDDMM 1.125n^2+4nd,
+    softmax 2n^2, SpMM 1.125n^2+4nd (total 4.25n^2+8nd).  Fused (softmax folded into the
+    SpMM): SDDMM 1.125n^2+4nd+8n (row maxima), SpMM 1.125n^2+4nd+8n (total 2.25n^2+8nd+16n)."""
     n, d = cfg["seq"], cfg["d"]
     eb = 4 if cfg["dtype"] == "float32" else 2
     gs = 2 if cfg["mode"] == "1:2" else 4
     nz = n * (n // 2) * eb
     meta = n * (n // gs) // 2
+    if fused:
+        return {"sddmm": nz + meta + 2 * n * d * eb + 8 * n, "spmm_softmax": nz + meta + 2 * n * d * eb + 8 * n}
     return {
         "sddmm": nz + meta + 2 * n * d * eb,
         "softmax": 2 * nz,
@@ -206,26 +210,35 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True):
     if not report_extra:
         return res
 
-    # ---- per-kernel breakdown on the same stream (dominant kernel -> roofline)
+    # ---- per-kernel breakdown on the same stream (the kernels dfss_attention launches)
     scale = 1.0 / math.sqrt(d)
-    nz_holder = {}
+    holder = {}
+    fused = cfg["mode"] == "2:4" and cfg["dtype"] != "float32" and d == 64 and n % 128 == 0
 
     def k_sddmm():
-        nz_holder["c"], _ = dfss.sddmm_prune(q, k, mode, scale)
+        holder["c"], _ = dfss.sddmm_prune(q, k, mode, scale, with_row_max=fused)
 
     def k_softmax():
-        nz_holder["p"] = dfss.softmax_rows(nz_holder["c"], check=False)
+        holder["p"] = dfss.softmax_rows(holder["c"], check=False)
 
     def k_spmm():
-        dfss.spmm(nz_holder["p"], v)
+        dfss.spmm(holder["p"], v)
+
+    def k_spmm_softmax():
+        dfss.spmm_softmax(holder["c"], v)
 
     k_sddmm(); k_softmax(); k_spmm()
     torch.cuda.synchronize()
+    stages = (("sddmm", k_sddmm), ("spmm_softmax", k_spmm_softmax)) if fused else \
+        (("sddmm", k_sddmm), ("softmax", k_softmax), ("spmm", k_spmm))
     kt = {}
-    for name, fn in (("sddmm", k_sddmm), ("softmax", k_softmax), ("spmm", k_spmm)):
+    for name, fn in stages:
         ts = time_steps(fn, max(3, args.steps), 2, flush)
         kt[name] = float(np.mean(ts))
-    ab = algorithmic_bytes(cfg)
+    # the standalone softmax_rows kernel (staged API), reported for reference
+    kt_info = {"softmax_rows_standalone": float(np.mean(time_steps(k_softmax, max(3, args.steps), 2, flush)))} \
+        if fused else {}
+    ab = algorithmic_bytes(cfg, fused)
     hbm_peak, tf_peak, peak_src = peaks()
     dom = max(kt, key=kt.get)
     achieved = ab[dom] * bh / (kt[dom] * 1e-3) / 1e9
@@ -233,10 +246,14 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True):
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(cfg_name, {}).get(dom)
+            t = json.load(open(prof)).get(cfg_name, {}).get(dom)
+            traffic = None if t is None else int(t)
         except Exception:
             traffic = None
     res["kernels_ms"] = kt
+    res["kernels_info_ms"] = kt_info
+    res["path"] = "fused: sddmm+prune+rowmax -> softmax-fused mma.sp SpMM" if fused else \
+        "staged: sddmm+prune -> softmax -> SpMM"
     res["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
                        "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
                        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
@@ -374,7 +391,7 @@ def main():
     device = torch.device("cuda", torch.cuda.current_device())
 
     res, (q, k, v, out, lo, hi) = run_dfss(args, args.config, ws, rank, local, device)
-    launches_per_step = 3  # SDDMM+prune, softmax, SpMM (dfss_nm_attention)
+    launches_per_step = len(res["kernels_ms"])  # kernels dfss_nm_attention launches per step
 
     # end-to-end parity gather: NCCL all_gather of the output shards (outside the timed region)
     parity = None
@@ -427,7 +444,8 @@ def main():
                        "seq_len": cfg["seq"], "head_dim": cfg["d"], "mode": cfg["mode"],
                        "global_batch": cfg["batch"] * ws, "parallelism": f"bh-shard{ws}", "heads_per_rank": res["bh_local"],
                        "l2": "flushed between timed steps (256 MiB write, outside the step events)"},
-            "roofline": res["roofline"], "kernels_ms": res["kernels_ms"],
+            "roofline": res["roofline"], "path": res["path"], "kernels_ms": res["kernels_ms"],
+            "kernels_info_ms": res["kernels_info_ms"],
             "pipeline_hbm_gbs": res["pipeline_hbm_gbs"], "pipeline_roofline_frac": res["pipeline_roofline_frac"],
             "dense_ms": res["dense_ms"], "speedup_vs_dense": res["speedup_vs_dense"],
             "gpu_launches": launches_per_step * args.steps, "clocks": res["clocks"],

@@ -84,11 +84,15 @@ int64_t dfss_meta_hw_words(int mode, int64_t bh, int64_t rows, int64_t cols);
  *   and left as zero nonzeros / nibble 0x4 padding.
  *   FusedStats (fused.py:22-38) are structural and computed by the host layer
  *   from the tile grid; dense_elems_written is 0 unless scores_dbg is given.
+ *   row_max (nullable, fp32 [bh, n_q, 2], tcgen05 path only): the two column-half
+ *   partial maxima of every row's kept scores (max over a row = its max over the
+ *   kept values, the row maximum always survives) -- the input that lets
+ *   dfss_spmm apply the softmax on the fly.
  */
 int dfss_sddmm_prune(const void* q, const void* k, void* nonzeros, uint32_t* meta_hw, float scale,
                      int mode, int in_dtype, int nz_dtype, int math, int64_t bh, int n_q, int n_k, int d,
                      const uint8_t* tile_keep, int tile_rows, int tile_cols, float* scores_dbg,
-                     void* stream);
+                     float* row_max, void* stream);
 
 /*
  * Softmax over each row's present nonzeros: replaces
@@ -114,16 +118,23 @@ int dfss_softmax_rows(const void* nz_in, void* p_out, int in_dtype, int out_dtyp
  *   16-bit P and V on aligned shapes run tcgen05.mma.sp with the metadata
  *   consumed straight from meta_hw; otherwise an FP32 FFMA gather kernel.
  *   tile_keep: optional BlockMask grid (masked tiles contribute zero).
+ *   row_max (nullable, [bh, rows, 2] from dfss_sddmm_prune): p holds RAW kept
+ *   scores and the softmax (sparse_ops.softmax_rows) is fused in: each staged
+ *   P tile is rewritten as exp(s - max_row) in shared memory before the MMA and
+ *   the output rows are divided by the row sums -- out = spmm(softmax_rows(p), v)
+ *   without the softmax's HBM round trip (tcgen05 path only).
  */
 int dfss_spmm(const void* p, const uint32_t* meta_hw, const void* v, void* out, int mode, int p_dtype,
               int v_dtype, int out_dtype, int64_t bh, int rows, int n_k, int d, const uint8_t* tile_keep,
-              int tile_rows, int tile_cols, void* stream);
+              int tile_rows, int tile_cols, const float* row_max, void* stream);
 
 /*
  * End-to-end DFSS attention: replaces pipeline.nm_attention (pipeline.py:15-32)
  * for [bh, n, d] q/k/v in `dtype`, scale = 1/sqrt(d) (fused.py:110).
  *   out [bh, n, d] in `dtype`.  `workspace` (device) must hold
- *   dfss_nm_attention_workspace_bytes(...) bytes for the compressed P and meta.
+ *   dfss_nm_attention_workspace_bytes(...) bytes for the compressed P, meta and
+ *   row maxima.  16-bit 2:4 on tiled shapes runs two kernels (SDDMM+prune+row
+ *   max, softmax-fused SpMM); everything else runs SDDMM -> softmax -> SpMM.
  */
 int64_t dfss_nm_attention_workspace_bytes(int mode, int dtype, int64_t bh, int n, int d);
 int dfss_nm_attention(const void* q, const void* k, const void* v, void* out, int mode, int dtype, int math,

@@ -32,9 +32,10 @@ _f32 = ctypes.c_float
 SIGNATURES = {
     "dfss_meta_hw_words": (_i64, [_i32, _i64, _i64, _i64]),
     "dfss_sddmm_prune": (_i32, [_vp, _vp, _vp, _vp, _f32, _i32, _i32, _i32, _i32, _i64, _i32, _i32, _i32, _vp, _i32,
-                                _i32, _vp, _vp]),
+                                _i32, _vp, _vp, _vp]),
     "dfss_softmax_rows": (_i32, [_vp, _vp, _i32, _i32, _i64, _i32, _i32, _vp, _i32, _i32, _vp, _vp]),
-    "dfss_spmm": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i64, _i32, _i32, _i32, _vp, _i32, _i32, _vp]),
+    "dfss_spmm": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i64, _i32, _i32, _i32, _vp, _i32, _i32, _vp,
+                         _vp]),
     "dfss_nm_attention_workspace_bytes": (_i64, [_i32, _i32, _i64, _i32, _i32]),
     "dfss_nm_attention": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i64, _i32, _i32, _vp, _i64, _vp]),
     "dfss_prune_scores": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i64, _i32, _vp]),

@@ -219,6 +219,8 @@ class CompressedSparse:
     meta_hw: torch.Tensor
     layout: Layout = Layout.LOGICAL
     block_mask: BlockMask | None = None
+    #: optional [..., rows, 2] fp32 partial row maxima recorded by the tcgen05 SDDMM
+    row_max: torch.Tensor | None = None
 
     def __post_init__(self) -> None:
         if self.rows < 1 or self.dense_cols < 1:

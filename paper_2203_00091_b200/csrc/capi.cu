@@ -70,7 +70,8 @@ int64_t dfss_meta_hw_words(int mode, int64_t bh, int64_t rows, int64_t cols) {
 
 int dfss_sddmm_prune(const void* q, const void* k, void* nonzeros, uint32_t* meta_hw, float scale, int mode,
                      int in_dtype, int nz_dtype, int math, int64_t bh, int n_q, int n_k, int d,
-                     const uint8_t* tile_keep, int tile_rows, int tile_cols, float* scores_dbg, void* stream) {
+                     const uint8_t* tile_keep, int tile_rows, int tile_cols, float* scores_dbg, float* row_max,
+                     void* stream) {
   if (!valid_mode(mode)) return fail(DFSS_ERR_INVALID, "unknown sparsity mode (expected 2 or 4)");
   if (!valid_dtype(in_dtype) || !valid_dtype(nz_dtype)) return fail(DFSS_ERR_INVALID, "unknown dtype");
   if (bh < 0 || n_q < 1 || n_k < 1 || d < 1) return fail(DFSS_ERR_INVALID, "shape dimensions must be positive");
@@ -83,11 +84,12 @@ int dfss_sddmm_prune(const void* q, const void* k, void* nonzeros, uint32_t* met
   if (math == DFSS_MATH_TF32) {
     if (in_dtype != DFSS_F32 || !tc_ok) return fail(DFSS_ERR_UNSUPPORTED, "tf32 path needs fp32 inputs on a tiled shape");
     return cuda_status(dfss::launch_sddmm_tc(q, k, nonzeros, meta_hw, scale, mode, in_dtype, bh, n_q, n_k, d,
-                                             scores_dbg, s));
+                                             scores_dbg, row_max, s));
   }
   if (math == DFSS_MATH_AUTO && in_dtype != DFSS_F32 && tc_ok)
     return cuda_status(dfss::launch_sddmm_tc(q, k, nonzeros, meta_hw, scale, mode, in_dtype, bh, n_q, n_k, d,
-                                             scores_dbg, s));
+                                             scores_dbg, row_max, s));
+  if (row_max) return fail(DFSS_ERR_UNSUPPORTED, "row_max is produced by the tcgen05 SDDMM only");
   return cuda_status(dfss::launch_sddmm_simt(q, k, nonzeros, meta_hw, scale, mode, in_dtype, nz_dtype, bh, n_q, n_k,
                                              d, tile_keep, tile_rows, tile_cols, scores_dbg, s));
 }
@@ -106,7 +108,7 @@ int dfss_softmax_rows(const void* nz_in, void* p_out, int in_dtype, int out_dtyp
 
 int dfss_spmm(const void* p, const uint32_t* meta_hw, const void* v, void* out, int mode, int p_dtype, int v_dtype,
               int out_dtype, int64_t bh, int rows, int n_k, int d, const uint8_t* tile_keep, int tile_rows,
-              int tile_cols, void* stream) {
+              int tile_cols, const float* row_max, void* stream) {
   if (!valid_mode(mode)) return fail(DFSS_ERR_INVALID, "unknown sparsity mode (expected 2 or 4)");
   if (!valid_dtype(p_dtype) || !valid_dtype(v_dtype) || !valid_dtype(out_dtype))
     return fail(DFSS_ERR_INVALID, "unknown dtype");
@@ -116,7 +118,8 @@ int dfss_spmm(const void* p, const uint32_t* meta_hw, const void* v, void* out, 
   if (!p || !meta_hw || !v || !out) return fail(DFSS_ERR_INVALID, "null tensor pointer");
   cudaStream_t s = (cudaStream_t)stream;
   if (!tile_keep && dfss::tc_spmm_supported(mode, p_dtype, v_dtype, out_dtype, rows, n_k, d) && dfss_has_tcgen05())
-    return cuda_status(dfss::launch_spmm_tc(p, meta_hw, v, out, mode, p_dtype, out_dtype, bh, rows, n_k, d, s));
+    return cuda_status(dfss::launch_spmm_tc(p, meta_hw, v, out, mode, p_dtype, out_dtype, bh, rows, n_k, d, row_max, s));
+  if (row_max) return fail(DFSS_ERR_UNSUPPORTED, "fused softmax SpMM needs the tcgen05 path (2:4, 16-bit, d=64)");
   if (d > 256) return fail(DFSS_ERR_UNSUPPORTED, "head dim > 256 not supported by the FFMA SpMM");
   return cuda_status(dfss::launch_spmm_simt(p, meta_hw, v, out, mode, p_dtype, v_dtype, out_dtype, bh, rows, n_k, d,
                                             tile_keep, tile_rows, tile_cols, s));
@@ -126,8 +129,8 @@ int64_t dfss_nm_attention_workspace_bytes(int mode, int dtype, int64_t bh, int n
   (void)d;
   if (!valid_mode(mode) || !valid_dtype(dtype) || bh < 0 || n < 1) return -1;
   const int64_t nz = bh * (int64_t)n * (n / 2) * dfss::dtype_bytes(dtype);
-  const int64_t nz_aligned = (nz + 255) / 256 * 256;
-  return nz_aligned + dfss_meta_hw_words(mode, bh, n, n) * 4 + 256;
+  const int64_t meta = dfss_meta_hw_words(mode, bh, n, n) * 4;
+  return (nz + 255) / 256 * 256 + (meta + 255) / 256 * 256 + bh * (int64_t)n * 2 * 4 + 256;
 }
 
 int dfss_nm_attention(const void* q, const void* k, const void* v, void* out, int mode, int dtype, int math,
@@ -140,16 +143,24 @@ int dfss_nm_attention(const void* q, const void* k, const void* v, void* out, in
   if (!workspace || workspace_bytes < need) return fail(DFSS_ERR_INVALID, "workspace too small");
   if (bh == 0) return DFSS_OK;
   const int64_t nz_bytes = bh * (int64_t)n * (n / 2) * dfss::dtype_bytes(dtype);
+  const int64_t meta_bytes = dfss_meta_hw_words(mode, bh, n, n) * 4;
   char* ws = (char*)workspace;
   void* nz = ws;
   uint32_t* meta = (uint32_t*)(ws + (nz_bytes + 255) / 256 * 256);
+  float* row_max = (float*)(ws + (nz_bytes + 255) / 256 * 256 + (meta_bytes + 255) / 256 * 256);
   const float scale = 1.0f / sqrtf((float)d);
+  // fused path: SDDMM+prune (+row max) -> SpMM with the softmax applied to the staged P tiles
+  const bool fused = math == DFSS_MATH_AUTO && dtype != DFSS_F32 &&
+                     dfss::tc_sddmm_supported(mode, dtype, dtype, n, n, d) &&
+                     dfss::tc_spmm_supported(mode, dtype, dtype, dtype, n, n, d) && dfss_has_tcgen05();
   int st = dfss_sddmm_prune(q, k, nz, meta, scale, mode, dtype, dtype, math, bh, n, n, d, nullptr, 0, 0, nullptr,
-                            stream);
+                            fused ? row_max : nullptr, stream);
   if (st) return st;
+  if (fused)
+    return dfss_spmm(nz, meta, v, out, mode, dtype, dtype, dtype, bh, n, n, d, nullptr, 0, 0, row_max, stream);
   st = dfss_softmax_rows(nz, nz, dtype, dtype, bh, n, n / 2, nullptr, 0, 0, nullptr, stream);
   if (st) return st;
-  return dfss_spmm(nz, meta, v, out, mode, dtype, dtype, dtype, bh, n, n, d, nullptr, 0, 0, stream);
+  return dfss_spmm(nz, meta, v, out, mode, dtype, dtype, dtype, bh, n, n, d, nullptr, 0, 0, nullptr, stream);
 }
 
 int dfss_prune_scores(const float* scores, void* nonzeros, uint8_t* meta_logical, uint8_t* kept, int mode,

@@ -80,6 +80,24 @@ __device__ __forceinline__ uint32_t select24(float v0, float v1, float v2, float
   return nib;
 }
 
+// Same, also folding the group's largest kept value (= max(w01, w23), the row
+// maximum is always kept) into a running maximum: one extra 3-input FMNMX.
+__device__ __forceinline__ uint32_t select24_max(float v0, float v1, float v2, float v3, float& lo, float& hi,
+                                                 float& run_max) {
+  const float w01 = fmaxf(v0, v1), l01 = fminf(v0, v1);
+  const float w23 = fmaxf(v2, v3), l23 = fminf(v2, v3);
+  run_max = fmaxf(run_max, fmaxf(w01, w23));
+  const bool keep01 = l01 >= w23;
+  const bool keep23 = l23 > w01;
+  lo = keep01 ? v0 : (keep23 ? v2 : w01);
+  hi = keep01 ? v1 : (keep23 ? v3 : w23);
+  uint32_t nib = (v2 >= v3) ? 8u : 12u;
+  nib += (v0 >= v1) ? 0u : 1u;
+  nib = keep23 ? 0xEu : nib;
+  nib = keep01 ? 0x4u : nib;
+  return nib;
+}
+
 // Reference rank rule (codec.py:121, kept for the self-check kernel in tests).
 __device__ __forceinline__ uint32_t select24_rank(float v0, float v1, float v2, float v3) {
   const int r0 = (v1 > v0) + (v2 > v0) + (v3 > v0);
@@ -154,9 +172,11 @@ cudaError_t launch_meta_logical_to_hw(const uint8_t* logical, uint32_t* hw, int 
                                       cudaStream_t s);
 // tcgen05 paths: return cudaErrorNotSupported when the shape is not covered.
 cudaError_t launch_sddmm_tc(const void* q, const void* k, void* nz, uint32_t* meta, float scale, int gs,
-                            int in_dtype, int64_t bh, int n, int m, int d, float* dbg, cudaStream_t s);
+                            int in_dtype, int64_t bh, int n, int m, int d, float* dbg, float* rowmax, cudaStream_t s);
+// rowmax (nullable): [bh, rows, 2] partial row maxima from the SDDMM; when given, the SpMM
+// applies softmax on the fly: P = exp(s - max) in smem, out = (P.V) / sum(P).
 cudaError_t launch_spmm_tc(const void* p, const uint32_t* meta, const void* v, void* out, int gs, int dtype,
-                           int out_dtype, int64_t bh, int rows, int n_k, int d, cudaStream_t s);
+                           int out_dtype, int64_t bh, int rows, int n_k, int d, const float* rowmax, cudaStream_t s);
 bool tc_sddmm_supported(int gs, int in_dtype, int nz_dtype, int n, int m, int d);
 bool tc_spmm_supported(int gs, int p_dtype, int v_dtype, int out_dtype, int rows, int n_k, int d);
 }  // namespace dfss

@@ -58,10 +58,10 @@ __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) {
 // Prune one 32-column chunk of a row: 8 groups of 4 scores -> 16 kept 16-bit values
 // (two 16B units of the 128B-swizzled staging row) + one 32-bit nibble word that is
 // traded with row^8 into the meta_hw word of this TMEM lane (include/dfss.h).
-template <typename T, bool DBG>
+template <typename T, bool DBG, bool RMAX>
 __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, int colh, int cc, uint8_t* stg,
                                           uint32_t lane, uint32_t* meta_b, int row_blk, float* dbg, int64_t dbg_row,
-                                          int m) {
+                                          int m, float& mx) {
   uint32_t packed[8];
   uint32_t W = 0;
 #pragma unroll
@@ -72,7 +72,7 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, 
     const float v3 = __uint_as_float(r[4 * g + 3]) * scale;
     if (DBG) *reinterpret_cast<float4*>(dbg + dbg_row * m + colh + cc * 32 + 4 * g) = make_float4(v0, v1, v2, v3);
     float lo, hi;
-    const uint32_t nib = select24(v0, v1, v2, v3, lo, hi);
+    const uint32_t nib = RMAX ? select24_max(v0, v1, v2, v3, lo, hi, mx) : select24(v0, v1, v2, v3, lo, hi);
     packed[g] = pack2<T>(lo, hi);
     W += nib * (1u << (4 * g));  // IMAD on the FMA pipe, not shift+or on the ALU pipe
   }
@@ -85,11 +85,11 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, 
   meta_b[(int64_t)((colh + cc * 32) >> 5) * 128 + row_blk] = word;
 }
 
-template <typename T, bool DBG>
+template <typename T, bool DBG, bool RMAX>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     sddmm24_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_nz, uint32_t* __restrict__ meta, float scale, int bh,
-                      int n, int m, float* __restrict__ dbg) {
+                      int n, int m, float* __restrict__ dbg, float* __restrict__ rowmax) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + SMEM_BAR);
@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int row_blk = quad * 32 + lane;  // row within the 128-row block
       const int grow = mb * BM + row_blk;    // row within the head
       uint32_t* meta_b = meta + ((int64_t)b * mblocks + mb) * chunks * 128;
+      float mx = -INFINITY;  // running max of this thread's row half (RMAX)
       for (int t = 0; t < ntiles; ++t) {
         const int width = min(BN, m - t * BN);
         const bool active = half * 128 < width;
@@ -217,15 +218,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc::tmem_ld_32x32b_x32(tbase, ra);
           tc::tmem_ld_wait(ra);
           tc::tmem_ld_32x32b_x32(tbase + 32, rb);
-          epi_chunk<T, DBG>(ra, scale, colh, 0, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m);
+          epi_chunk<T, DBG, RMAX>(ra, scale, colh, 0, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m, mx);
           tc::tmem_ld_wait(rb);
           tc::tmem_ld_32x32b_x32(tbase + 64, ra);
-          epi_chunk<T, DBG>(rb, scale, colh, 1, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m);
+          epi_chunk<T, DBG, RMAX>(rb, scale, colh, 1, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m, mx);
           tc::tmem_ld_wait(ra);
           tc::tmem_ld_32x32b_x32(tbase + 96, rb);
-          epi_chunk<T, DBG>(ra, scale, colh, 2, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m);
+          epi_chunk<T, DBG, RMAX>(ra, scale, colh, 2, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m, mx);
           tc::tmem_ld_wait(rb);
-          epi_chunk<T, DBG>(rb, scale, colh, 3, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m);
+          epi_chunk<T, DBG, RMAX>(rb, scale, colh, 3, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m, mx);
         }
         tc::tc_fence_before();
         __syncwarp();
@@ -241,6 +242,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (++acc == NACC) { acc = 0; aph ^= 1; }
       }
+      // per-row partial maxima of the two column halves: [bh, n, 2] fp32 (fused softmax input)
+      if (RMAX) rowmax[((int64_t)b * n + grow) * 2 + half] = mx;
     }
     if (lane == 0) tc::bulk_wait<0>();
   }
@@ -272,7 +275,7 @@ static int num_sms() {
 
 template <typename T>
 static cudaError_t launch_typed(const void* q, const void* k, void* nz, uint32_t* meta, float scale, int64_t bh, int n,
-                                int m, float* dbg, cudaStream_t s) {
+                                int m, float* dbg, float* rowmax, cudaStream_t s) {
   const CUtensorMapDataType dt =
       std::is_same<T, __nv_bfloat16>::value ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tn;
@@ -280,21 +283,22 @@ static cudaError_t launch_typed(const void* q, const void* k, void* nz, uint32_t
       !encode_tmap_3d(&tk, dt, 2, (void*)k, HD, m, bh, HD, BN, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !encode_tmap_3d(&tn, dt, 2, nz, m / 2, n, bh, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
-  auto kern = dbg ? sddmm24_tc_kernel<T, true> : sddmm24_tc_kernel<T, false>;
+  auto kern = dbg ? (rowmax ? sddmm24_tc_kernel<T, true, true> : sddmm24_tc_kernel<T, true, false>)
+                 : (rowmax ? sddmm24_tc_kernel<T, false, true> : sddmm24_tc_kernel<T, false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
   if (e != cudaSuccess) return e;
   const int items = (int)bh * (n / BM);
   const int grid = items < num_sms() ? items : num_sms();
-  kern<<<grid, NUM_THREADS, SMEM_TOTAL, s>>>(tq, tk, tn, meta, scale, (int)bh, n, m, dbg);
+  kern<<<grid, NUM_THREADS, SMEM_TOTAL, s>>>(tq, tk, tn, meta, scale, (int)bh, n, m, dbg, rowmax);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sddmm_tc(const void* q, const void* k, void* nz, uint32_t* meta, float scale, int gs, int in_dtype,
-                            int64_t bh, int n, int m, int d, float* dbg, cudaStream_t s) {
+                            int64_t bh, int n, int m, int d, float* dbg, float* rowmax, cudaStream_t s) {
   if (!tc_sddmm_supported(gs, in_dtype, in_dtype, n, m, d)) return cudaErrorNotSupported;
   if (bh == 0) return cudaSuccess;
-  if (in_dtype == DFSS_BF16) return launch_typed<__nv_bfloat16>(q, k, nz, meta, scale, bh, n, m, dbg, s);
-  return launch_typed<__half>(q, k, nz, meta, scale, bh, n, m, dbg, s);
+  if (in_dtype == DFSS_BF16) return launch_typed<__nv_bfloat16>(q, k, nz, meta, scale, bh, n, m, dbg, rowmax, s);
+  return launch_typed<__half>(q, k, nz, meta, scale, bh, n, m, dbg, rowmax, s);
 }
 
 }  // namespace dfss

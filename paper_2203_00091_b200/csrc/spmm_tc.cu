@@ -1,18 +1,25 @@
-// spmm_tc.cu -- compressed SpMM O = P_sparse . V on tcgen05.mma.sp (2:4, bf16/fp16, d = 64).
+// spmm_tc.cu -- compressed SpMM O = P_sparse . V on tcgen05.mma.sp (2:4, bf16/fp16, d = 64),
+// optionally with the row softmax fused in.
 //
 // Replaces _spmm_gather (_kernels_numba.py:91-103) for the 16-bit path.  The
 // compressed P rows ARE the sparse A operand (kept values in ascending column
 // order, K-major) and meta_hw words ARE the TMEM metadata columns, so nothing
 // is decoded: the SDDMM output is consumed as written.  Persistent,
 // warp-specialised, one CTA per SM:
-//   warp 0      TMA producer: P tile (128 rows x 64 stored = 128 logical K) and
-//               V tile (128 K-rows x 64, MN-major) per stage, STAGES-deep ring;
-//   warp 1      MMA issuer: 4 x tcgen05.mma.sp.kind::f16 (M=128, N=64, K=32) per
-//               stage, metadata column s*4+kk, accumulator double-buffered;
-//   warp 2      TMEM allocator;
-//   warps 4-7   metadata loaders: warp w copies the words of TMEM lanes
-//               32*(w%4).. for the stage's 4 K-chunks global -> tcgen05.st;
-//   warps 8-11  epilogue: TMEM -> registers -> 16-bit -> O rows.
+//   warp 0       TMA producer: P tile (128 rows x 64 stored = 128 logical K) and
+//                V tile (128 K-rows x 64, MN-major) per stage, STAGES-deep ring;
+//   warp 1       MMA issuer: 4 x tcgen05.mma.sp.kind::f16 (M=128, N=64, K=32) per
+//                stage, metadata column s*4+kk, accumulator double-buffered;
+//   warp 2       TMEM allocator;
+//   warps 4-7    metadata loaders: warp w copies the words of TMEM lanes
+//                32*(w%4).. for the stage's 4 K-chunks global -> tcgen05.st;
+//   warps 8-11   epilogue: TMEM -> registers (x 1/rowsum when fused) -> O rows;
+//   warps 12-15  (SOFTMAX only) transform: thread r rewrites row r of the staged
+//                P tile in smem as exp(s - m_r) (m_r = row max from the SDDMM
+//                epilogue, so no rescaling pass) and accumulates the row sum --
+//                softmax_rows (sparse_ops.py:18-37) fused between TMA and MMA.
+#include <math_constants.h>
+
 #include <type_traits>
 
 #include "dfss_common.cuh"
@@ -26,30 +33,65 @@ constexpr int HD = 64;
 constexpr int BKL = 128;  // logical K per stage
 constexpr int STAGES = 6;
 constexpr int NACC = 2;
-constexpr int NUM_THREADS = 12 * 32;
 constexpr int P_BYTES = BM * (BKL / 2) * 2;  // 16 KB
 constexpr int V_BYTES = BKL * HD * 2;        // 16 KB
 constexpr int SMEM_P = 0;
 constexpr int SMEM_V = SMEM_P + STAGES * P_BYTES;
-constexpr int SMEM_BAR = SMEM_V + STAGES * V_BYTES;
+constexpr int SMEM_L = SMEM_V + STAGES * V_BYTES;  // [NACC][128] row sums (fused softmax)
+constexpr int SMEM_BAR = SMEM_L + NACC * BM * 4;
 constexpr int SMEM_TOTAL = SMEM_BAR + 512 + 1024;
 constexpr int TMEM_COLS = 256;
 constexpr int E_COL0 = NACC * HD;  // metadata columns start after the accumulators
+constexpr float kLog2e = 1.4426950408889634f;
 }  // namespace
 
-template <typename T, typename TO>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <typename T>
+__device__ __forceinline__ float2 unpack2(uint32_t u);
+template <>
+__device__ __forceinline__ float2 unpack2<__nv_bfloat16>(uint32_t u) {
+  return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u));
+}
+template <>
+__device__ __forceinline__ float2 unpack2<__half>(uint32_t u) {
+  __half2 h = *reinterpret_cast<__half2*>(&u);
+  return __half22float2(h);
+}
+template <typename T>
+__device__ __forceinline__ uint32_t pack2f(float lo, float hi);
+template <>
+__device__ __forceinline__ uint32_t pack2f<__nv_bfloat16>(float lo, float hi) {
+  __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&p);
+}
+template <>
+__device__ __forceinline__ uint32_t pack2f<__half>(float lo, float hi) {
+  __half2 p = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&p);
+}
+
+template <typename T, typename TO, bool SOFTMAX>
+__global__ void __launch_bounds__(SOFTMAX ? 512 : 384, 1)
     spmm24_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_v,
-                     const uint32_t* __restrict__ meta, TO* __restrict__ out, int bh, int rows, int n_k) {
+                     const uint32_t* __restrict__ meta, TO* __restrict__ out, int bh, int rows, int n_k,
+                     const float* __restrict__ rowmax) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + SMEM_BAR);
   uint64_t* full = bars;                 // [STAGES] TMA bytes landed
   uint64_t* e_full = full + STAGES;      // [STAGES] metadata columns written (4 warps)
   uint64_t* empty = e_full + STAGES;     // [STAGES] MMAs of the stage retired
-  uint64_t* d_full = empty + STAGES;     // [NACC]
+  uint64_t* p_ready = empty + STAGES;    // [STAGES] (SOFTMAX) P tile rewritten as exp (4 warps)
+  uint64_t* d_full = p_ready + STAGES;   // [NACC]
   uint64_t* d_empty = d_full + NACC;     // [NACC] (4 epilogue warps)
-  uint32_t* tmem_slot = (uint32_t*)(d_empty + NACC);
+  uint64_t* l_full = d_empty + NACC;     // [NACC] (SOFTMAX) row sums in smem (4 warps)
+  uint32_t* tmem_slot = (uint32_t*)(l_full + NACC);
+  float* lsum = (float*)(smem + SMEM_L);
 
   const uint32_t warp = tc::warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -65,10 +107,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc::mbar_init(&full[i], 1);
       tc::mbar_init(&e_full[i], 4);
       tc::mbar_init(&empty[i], 1);
+      tc::mbar_init(&p_ready[i], 4);
     }
     for (int i = 0; i < NACC; ++i) {
       tc::mbar_init(&d_full[i], 1);
       tc::mbar_init(&d_empty[i], 4);
+      tc::mbar_init(&l_full[i], 4);
     }
     tc::fence_barrier_init();
   }
@@ -104,6 +148,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t d_tmem = tmem_base + acc * HD;
         for (int kb = 0; kb < kblocks; ++kb) {
           tc::mbar_wait(&full[s], ph);
+          if (SOFTMAX) tc::mbar_wait(&p_ready[s], ph);
           tc::mbar_wait(&e_full[s], ph);
           tc::tc_fence_after();
           const uint32_t p_addr = tc::smem_u32(smem + SMEM_P + s * P_BYTES);
@@ -148,14 +193,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 8 && warp < 12) {
     // ------------------------------------------------------------ epilogue
     const int quad = warp & 3;
+    const int r = quad * 32 + lane;
     int acc = 0;
     uint32_t aph = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       const int b = item / rblocks, rb = item % rblocks;
       tc::mbar_wait(&d_full[acc], aph);
+      float inv = 1.f;
+      if (SOFTMAX) {
+        tc::mbar_wait(&l_full[acc], aph);
+        inv = 1.0f / lsum[acc * BM + r];
+      }
       tc::tc_fence_after();
       uint32_t r0[32], r1[32];
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * HD;
@@ -166,30 +217,69 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&d_empty[acc]);
-      TO* orow = out + ((int64_t)b * rows + rb * BM + quad * 32 + lane) * HD;
+      TO* orow = out + ((int64_t)b * rows + rb * BM + r) * HD;
       if constexpr (std::is_same<TO, float>::value) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          reinterpret_cast<float4*>(orow)[j] = make_float4(__uint_as_float(r0[4 * j]), __uint_as_float(r0[4 * j + 1]),
-                                                           __uint_as_float(r0[4 * j + 2]), __uint_as_float(r0[4 * j + 3]));
+          reinterpret_cast<float4*>(orow)[j] =
+              make_float4(__uint_as_float(r0[4 * j]) * inv, __uint_as_float(r0[4 * j + 1]) * inv,
+                          __uint_as_float(r0[4 * j + 2]) * inv, __uint_as_float(r0[4 * j + 3]) * inv);
           reinterpret_cast<float4*>(orow)[8 + j] =
-              make_float4(__uint_as_float(r1[4 * j]), __uint_as_float(r1[4 * j + 1]), __uint_as_float(r1[4 * j + 2]),
-                          __uint_as_float(r1[4 * j + 3]));
+              make_float4(__uint_as_float(r1[4 * j]) * inv, __uint_as_float(r1[4 * j + 1]) * inv,
+                          __uint_as_float(r1[4 * j + 2]) * inv, __uint_as_float(r1[4 * j + 3]) * inv);
         }
       } else {
         uint32_t pk[32];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          TO lo = DT<TO>::from_f(__uint_as_float(r0[2 * j])), hi = DT<TO>::from_f(__uint_as_float(r0[2 * j + 1]));
-          pk[j] = (uint32_t)(*reinterpret_cast<uint16_t*>(&lo)) | ((uint32_t)(*reinterpret_cast<uint16_t*>(&hi)) << 16);
-          TO lo2 = DT<TO>::from_f(__uint_as_float(r1[2 * j])), hi2 = DT<TO>::from_f(__uint_as_float(r1[2 * j + 1]));
-          pk[16 + j] =
-              (uint32_t)(*reinterpret_cast<uint16_t*>(&lo2)) | ((uint32_t)(*reinterpret_cast<uint16_t*>(&hi2)) << 16);
+          pk[j] = pack2f<TO>(__uint_as_float(r0[2 * j]) * inv, __uint_as_float(r0[2 * j + 1]) * inv);
+          pk[16 + j] = pack2f<TO>(__uint_as_float(r1[2 * j]) * inv, __uint_as_float(r1[2 * j + 1]) * inv);
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           reinterpret_cast<uint4*>(orow)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
       }
+      if (++acc == NACC) { acc = 0; aph ^= 1; }
+    }
+  } else if (SOFTMAX && warp >= 12) {
+    // ------------------------------------------------------------ softmax transform
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;  // row within the 128-row block == TMEM lane
+    int s = 0, acc = 0;
+    uint32_t ph = 0, aph = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+      const int b = item / rblocks, rb = item % rblocks;
+      const float2 mp = *reinterpret_cast<const float2*>(rowmax + ((int64_t)b * rows + rb * BM + r) * 2);
+      const float mb = fmaxf(mp.x, mp.y) * kLog2e;
+      float l = 0.f;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        tc::mbar_wait(&full[s], ph);
+        uint8_t* prow = smem + SMEM_P + s * P_BYTES + r * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint4* u = reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4));
+          uint4 x = *u;
+          uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 f = unpack2<T>(w[j]);
+            const float e0 = ex2_approx(fmaf(f.x, kLog2e, -mb));
+            const float e1 = ex2_approx(fmaf(f.y, kLog2e, -mb));
+            l += e0 + e1;
+            w[j] = pack2f<T>(e0, e1);
+          }
+          *u = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        tc::fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&p_ready[s]);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+      // hand the row sum to the epilogue (buffer acc is free once its previous O was drained)
+      tc::mbar_wait(&d_empty[acc], aph ^ 1);
+      lsum[acc * BM + r] = l;
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&l_full[acc]);
       if (++acc == NACC) { acc = 0; aph ^= 1; }
     }
   }
@@ -219,31 +309,39 @@ static int num_sms_spmm() {
 
 template <typename T, typename TO>
 static cudaError_t spmm_launch_typed(const void* p, const uint32_t* meta, const void* v, void* out, int64_t bh, int rows,
-                                     int n_k, cudaStream_t s) {
+                                     int n_k, const float* rowmax, cudaStream_t s) {
   const CUtensorMapDataType dt =
       std::is_same<T, __nv_bfloat16>::value ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tp, tv;
   if (!encode_tmap_3d(&tp, dt, 2, (void*)p, n_k / 2, rows, bh, BKL / 2, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !encode_tmap_3d(&tv, dt, 2, (void*)v, HD, n_k, bh, HD, BKL, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
-  auto kern = spmm24_tc_kernel<T, TO>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
-  if (e != cudaSuccess) return e;
   const int items = (int)bh * (rows / BM);
   const int grid = items < num_sms_spmm() ? items : num_sms_spmm();
-  kern<<<grid, NUM_THREADS, SMEM_TOTAL, s>>>(tp, tv, meta, (TO*)out, (int)bh, rows, n_k);
+  if (rowmax) {
+    auto kern = spmm24_tc_kernel<T, TO, true>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, 512, SMEM_TOTAL, s>>>(tp, tv, meta, (TO*)out, (int)bh, rows, n_k, rowmax);
+  } else {
+    auto kern = spmm24_tc_kernel<T, TO, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, 384, SMEM_TOTAL, s>>>(tp, tv, meta, (TO*)out, (int)bh, rows, n_k, nullptr);
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_spmm_tc(const void* p, const uint32_t* meta, const void* v, void* out, int gs, int dtype,
-                           int out_dtype, int64_t bh, int rows, int n_k, int d, cudaStream_t s) {
+                           int out_dtype, int64_t bh, int rows, int n_k, int d, const float* rowmax, cudaStream_t s) {
   if (!tc_spmm_supported(gs, dtype, dtype, out_dtype, rows, n_k, d)) return cudaErrorNotSupported;
   if (bh == 0) return cudaSuccess;
   if (dtype == DFSS_BF16)
-    return out_dtype == DFSS_F32 ? spmm_launch_typed<__nv_bfloat16, float>(p, meta, v, out, bh, rows, n_k, s)
-                                 : spmm_launch_typed<__nv_bfloat16, __nv_bfloat16>(p, meta, v, out, bh, rows, n_k, s);
-  return out_dtype == DFSS_F32 ? spmm_launch_typed<__half, float>(p, meta, v, out, bh, rows, n_k, s)
-                               : spmm_launch_typed<__half, __half>(p, meta, v, out, bh, rows, n_k, s);
+    return out_dtype == DFSS_F32
+               ? spmm_launch_typed<__nv_bfloat16, float>(p, meta, v, out, bh, rows, n_k, rowmax, s)
+               : spmm_launch_typed<__nv_bfloat16, __nv_bfloat16>(p, meta, v, out, bh, rows, n_k, rowmax, s);
+  return out_dtype == DFSS_F32 ? spmm_launch_typed<__half, float>(p, meta, v, out, bh, rows, n_k, rowmax, s)
+                               : spmm_launch_typed<__half, __half>(p, meta, v, out, bh, rows, n_k, rowmax, s);
 }
 
 }  // namespace dfss

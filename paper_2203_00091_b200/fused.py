@@ -60,6 +60,7 @@ def sddmm_prune(
     nz_dtype: torch.dtype | None = None,
     math_mode: str = "auto",
     scores_out: torch.Tensor | None = None,
+    with_row_max: bool = False,
 ) -> tuple[CompressedSparse, FusedStats]:
     """compress(Q K^T * scale) without materialising the scores (fused.py:41-96).
 
@@ -67,6 +68,8 @@ def sddmm_prune(
     is bit-exact to the reference rule on the fp32 post-scale scores the
     epilogue sees; ``scores_out`` (fp32 [..., n, m]) receives exactly those
     scores for parity checks (it is the only dense write, off by default).
+    ``with_row_max`` also records each row's maximum (tcgen05 path), which lets
+    ``spmm_softmax`` fuse the row softmax into the SpMM.
     """
     mode = as_mode(mode)
     qt, kt = as_tensor(q), as_tensor(k)
@@ -108,14 +111,16 @@ def sddmm_prune(
         if scores_out.dtype != torch.float32 or tuple(scores_out.shape) != batch + (n, m) or not scores_out.is_contiguous():
             raise ValueError("scores_out must be a contiguous float32 tensor of shape (..., n, m)")
     dev_keep = block_mask.device_keep(qt.device) if block_mask is not None else None
+    row_max = torch.empty(batch + (n, 2), dtype=torch.float32, device=qt.device) if with_row_max else None
     lib = _lib.load()
     _lib.check(
         lib.dfss_sddmm_prune(_lib.ptr(qt), _lib.ptr(kt), _lib.ptr(nz), _lib.ptr(meta), float(scale), gs,
                              _lib.dtype_id(qt.dtype), _lib.dtype_id(nz_dtype), _MATH[math_mode], bh, n, m, d,
-                             _lib.ptr(dev_keep), tile_rows, tile_cols, _lib.ptr(scores_out), _lib.stream_of(qt)),
+                             _lib.ptr(dev_keep), tile_rows, tile_cols, _lib.ptr(scores_out), _lib.ptr(row_max),
+                             _lib.stream_of(qt)),
         "sddmm_prune",
     )
-    compressed = CompressedSparse(n, m, mode, nz, meta, block_mask=block_mask)
+    compressed = CompressedSparse(n, m, mode, nz, meta, block_mask=block_mask, row_max=row_max)
     return compressed, _stats(n, m, gs, tile_rows, tile_cols, keep)
 
 

@@ -77,5 +77,32 @@ def spmm(a: CompressedSparse, v, block_mask: BlockMask | None = None, out_dtype:
     lib = _lib.load()
     _lib.check(lib.dfss_spmm(_lib.ptr(a.nonzeros), _lib.ptr(a.meta_hw), _lib.ptr(vt), _lib.ptr(out), a.mode.group_size,
                              _lib.dtype_id(a.nonzeros.dtype), _lib.dtype_id(vt.dtype), _lib.dtype_id(out_dtype), a.bh,
-                             a.rows, a.dense_cols, d, _lib.ptr(keep), tr, tc, _lib.stream_of(out)), "spmm")
+                             a.rows, a.dense_cols, d, _lib.ptr(keep), tr, tc, None, _lib.stream_of(out)), "spmm")
+    return DenseMatrix(out, check_finite=False)
+
+
+def spmm_softmax(a: CompressedSparse, v, out_dtype: torch.dtype | None = None) -> DenseMatrix:
+    """``spmm(softmax_rows(a), v)`` in one kernel: the row softmax is applied to each staged
+    P tile in shared memory (exp(s - row max)) and the output rows are divided by the row
+    sums -- no HBM round trip for the probabilities.  Needs ``a`` from
+    ``sddmm_prune(..., with_row_max=True)`` (tcgen05 path: 2:4, 16-bit, d = 64)."""
+    if a.row_max is None:
+        raise ValueError("spmm_softmax needs the row maxima: call sddmm_prune(..., with_row_max=True)")
+    if a.layout is not Layout.LOGICAL or a.block_mask is not None:
+        raise ValueError("spmm_softmax requires the logical layout without a block mask")
+    vt = as_tensor(v)
+    if a.dense_cols != vt.shape[-2]:
+        raise ValueError(
+            f"shape mismatch: sparse operand is {a.rows}x{a.dense_cols}, dense operand has {vt.shape[-2]} rows"
+        )
+    _lib.require_cuda(vt)
+    vt = vt.contiguous()
+    d = vt.shape[-1]
+    out_dtype = out_dtype or vt.dtype
+    out = torch.empty(a.batch_shape + (a.rows, d), dtype=out_dtype, device=a.device)
+    lib = _lib.load()
+    _lib.check(lib.dfss_spmm(_lib.ptr(a.nonzeros), _lib.ptr(a.meta_hw), _lib.ptr(vt), _lib.ptr(out), a.mode.group_size,
+                             _lib.dtype_id(a.nonzeros.dtype), _lib.dtype_id(vt.dtype), _lib.dtype_id(out_dtype), a.bh,
+                             a.rows, a.dense_cols, d, None, 0, 0, _lib.ptr(a.row_max), _lib.stream_of(out)),
+               "spmm_softmax")
     return DenseMatrix(out, check_finite=False)

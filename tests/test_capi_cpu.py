@@ -51,10 +51,10 @@ def test_status_strings():
 def test_c_abi_validation_rejects_before_launch():
     lib = _lib.load()
     # bad mode, misaligned columns, null pointers: all DFSS_ERR_INVALID without a device
-    assert lib.dfss_sddmm_prune(None, None, None, None, 1.0, 3, 0, 0, 0, 1, 8, 8, 4, None, 0, 0, None, None) == -1
-    assert lib.dfss_sddmm_prune(None, None, None, None, 1.0, 4, 0, 0, 0, 1, 8, 6, 4, None, 0, 0, None, None) == -1
+    assert lib.dfss_sddmm_prune(None, None, None, None, 1.0, 3, 0, 0, 0, 1, 8, 8, 4, None, 0, 0, None, None, None) == -1
+    assert lib.dfss_sddmm_prune(None, None, None, None, 1.0, 4, 0, 0, 0, 1, 8, 6, 4, None, 0, 0, None, None, None) == -1
     assert b"group-aligned" in lib.dfss_last_error()
-    assert lib.dfss_spmm(None, None, None, None, 2, 0, 0, 0, 1, 4, 4, 2, None, 0, 0, None) == -1
+    assert lib.dfss_spmm(None, None, None, None, 2, 0, 0, 0, 1, 4, 4, 2, None, 0, 0, None, None) == -1
     assert lib.dfss_nm_attention_workspace_bytes(4, 1, 2, 512, 64) >= 2 * 512 * 256 * 2 + 2 * 512 * 512 // 8
 
 

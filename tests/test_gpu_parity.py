@@ -303,11 +303,27 @@ def test_c1_fp32_attention_within_1e5():
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("mode", ["2:4", "1:2"])
-def test_16bit_attention_within_2e2(dtype, mode):
-    (q, k, v), (q64, k64, v64) = seeded_qkv((2, 3, 512, 64), dtype, seed=1)
+@pytest.mark.parametrize("n", [512, 384])
+def test_16bit_attention_within_2e2(dtype, mode, n):
+    (q, k, v), (q64, k64, v64) = seeded_qkv((2, 3, n, 64), dtype, seed=1)
     out = dfss.dfss_attention(q, k, v, mode)
     want = oracle_attention(q64, k64, v64, mode)
-    assert_close(_np(out), want, 2e-2, 2e-2, f"{dtype} {mode}")
+    assert_close(_np(out), want, 2e-2, 2e-2, f"{dtype} {mode} n={n}")
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_fused_softmax_spmm_matches_staged_and_oracle(dtype):
+    """spmm_softmax(sddmm_prune(with_row_max)) == spmm(softmax_rows(.)) == reference nm_attention."""
+    (q, k, v), (q64, k64, v64) = seeded_qkv((2, 2, 640, 64), dtype, seed=4)
+    dbg = torch.empty((2, 2, 640, 640), dtype=torch.float32, device="cuda")
+    c, _ = dfss.sddmm_prune(q, k, "2:4", 0.125, with_row_max=True, scores_out=dbg)
+    # the recorded row maximum is the exact fp32 max of the row's scores (always a kept value)
+    assert torch.equal(c.row_max.amax(-1), dbg.amax(-1))
+    fused = _np(dfss.spmm_softmax(c, v).data)
+    staged = _np(dfss.spmm(dfss.softmax_rows(c), v).data)
+    assert_close(fused, staged, 2e-2, 2e-2, "fused vs staged")
+    want = oracle_attention(q64, k64, v64, "2:4")
+    assert_close(fused, want, 2e-2, 2e-2, "fused vs oracle")
 
 
 def test_golden_pipeline_cases_fp32():

@@ -62,20 +62,28 @@ __device__ __forceinline__ uint32_t nibble_of_mask(uint32_t mask) {
 // beats w01, otherwise {w01, w23}.  Every comparison puts the lower index on
 // the left of >= (or the higher on the left of >), so ties resolve exactly as
 // the reference's stable argsort (exhaustively checked over tie-heavy inputs,
-// tests/test_gpu_parity.py).  Written for the ALU budget of the SDDMM
-// epilogue: 4 FMNMX + 4 FSETP + 4 FSEL + 4 SEL/IADD, no predicate logic.
-// (fmaxf may return +0 for a (-0, +0) tie where the reference keeps -0: equal
-// values, identical metadata.)
-__device__ __forceinline__ uint32_t select24(float v0, float v1, float v2, float v3, float& lo, float& hi) {
+// tests/test_gpu_parity.py).
+//
+// Cost model (the SDDMM epilogue is ALU-pipe bound): 4 FMNMX + 2 FSETP +
+// 4 FSEL + 2 SEL on the ALU pipe; the "mixed" nibble (w01 idx) | (w23 idx) << 2
+// comes from the sign bits of v0 - v1 and v2 - v3 on the FMA pipe
+// (FADD + IMAD.HI by `two` == 2, a runtime value so the compiler cannot turn
+// it into an ALU shift).  The sign trick needs canonical zeros (no -0.0):
+// callers produce the inputs with fma(x, s, +0.0f) / x + 0.0f, which maps
+// -0 to +0 -- equal values, identical ordering and ties.
+__device__ __forceinline__ uint32_t sign_bit(float x, uint32_t two) { return __umulhi(__float_as_uint(x), two); }
+
+__device__ __forceinline__ uint32_t select24(float v0, float v1, float v2, float v3, float& lo, float& hi,
+                                             uint32_t two) {
   const float w01 = fmaxf(v0, v1), l01 = fminf(v0, v1);
   const float w23 = fmaxf(v2, v3), l23 = fminf(v2, v3);
   const bool keep01 = l01 >= w23;  // lower-index loser vs higher-index winner
   const bool keep23 = l23 > w01;   // higher-index loser must strictly beat the winner
   lo = keep01 ? v0 : (keep23 ? v2 : w01);
   hi = keep01 ? v1 : (keep23 ? v3 : w23);
-  uint32_t nib = (v2 >= v3) ? 8u : 12u;  // hi slot = index of w23
-  nib += (v0 >= v1) ? 0u : 1u;           // lo slot = index of w01
-  nib = keep23 ? 0xEu : nib;
+  // w01 index = [v0 < v1], w23 index = 2 + [v2 < v3]  (ties keep the lower index)
+  const uint32_t mixed = 8u + sign_bit(v0 - v1, two) + 4u * sign_bit(v2 - v3, two);
+  uint32_t nib = keep23 ? 0xEu : mixed;
   nib = keep01 ? 0x4u : nib;
   return nib;
 }
@@ -83,7 +91,7 @@ __device__ __forceinline__ uint32_t select24(float v0, float v1, float v2, float
 // Same, also folding the group's largest kept value (= max(w01, w23), the row
 // maximum is always kept) into a running maximum: one extra 3-input FMNMX.
 __device__ __forceinline__ uint32_t select24_max(float v0, float v1, float v2, float v3, float& lo, float& hi,
-                                                 float& run_max) {
+                                                 float& run_max, uint32_t two) {
   const float w01 = fmaxf(v0, v1), l01 = fminf(v0, v1);
   const float w23 = fmaxf(v2, v3), l23 = fminf(v2, v3);
   run_max = fmaxf(run_max, fmaxf(w01, w23));
@@ -91,11 +99,17 @@ __device__ __forceinline__ uint32_t select24_max(float v0, float v1, float v2, f
   const bool keep23 = l23 > w01;
   lo = keep01 ? v0 : (keep23 ? v2 : w01);
   hi = keep01 ? v1 : (keep23 ? v3 : w23);
-  uint32_t nib = (v2 >= v3) ? 8u : 12u;
-  nib += (v0 >= v1) ? 0u : 1u;
-  nib = keep23 ? 0xEu : nib;
+  const uint32_t mixed = 8u + sign_bit(v0 - v1, two) + 4u * sign_bit(v2 - v3, two);
+  uint32_t nib = keep23 ? 0xEu : mixed;
   nib = keep01 ? 0x4u : nib;
   return nib;
+}
+
+// canonical-zero scaling used before every select: x*s + (+0) turns -0 into +0
+__device__ __forceinline__ float scale_canon(float x, float s) {
+  float y;
+  asm("fma.rn.f32 %0, %1, %2, 0f00000000;" : "=f"(y) : "f"(x), "f"(s));
+  return y;
 }
 
 // Reference rank rule (codec.py:121, kept for the self-check kernel in tests).

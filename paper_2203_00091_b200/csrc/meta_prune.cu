@@ -9,7 +9,7 @@ namespace dfss {
 template <typename TNz, int GS>
 __global__ void prune_scores_kernel(const float* __restrict__ scores, TNz* __restrict__ nz,
                                     uint8_t* __restrict__ meta, uint8_t* __restrict__ kept, int64_t rows,
-                                    int cols) {
+                                    int cols, uint32_t two) {
   const int groups = cols / GS;
   const int64_t total = rows * groups;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -19,7 +19,9 @@ __global__ void prune_scores_kernel(const float* __restrict__ scores, TNz* __res
     uint32_t nib;
     if (GS == 4) {
       float lo, hi;
-      nib = select24(s[0], s[1], s[2], s[3], lo, hi);
+      // same routine as the SDDMM epilogue; +0 canonicalises -0 (equal values, same ties)
+      nib = select24(scale_canon(s[0], 1.f), scale_canon(s[1], 1.f), scale_canon(s[2], 1.f), scale_canon(s[3], 1.f),
+                     lo, hi, two);
       if (nz) {
         nz[r * (cols / 2) + 2 * g] = DT<TNz>::from_f(lo);
         nz[r * (cols / 2) + 2 * g + 1] = DT<TNz>::from_f(hi);
@@ -47,14 +49,14 @@ static cudaError_t prune_dispatch(const float* scores, void* nz, uint8_t* meta, 
   if (blocks == 0) return cudaSuccess;
   switch (nz_dtype) {
     case DFSS_F32:
-      prune_scores_kernel<float, GS><<<blocks, threads, 0, s>>>(scores, (float*)nz, meta, kept, rows, cols);
+      prune_scores_kernel<float, GS><<<blocks, threads, 0, s>>>(scores, (float*)nz, meta, kept, rows, cols, 2u);
       break;
     case DFSS_BF16:
       prune_scores_kernel<__nv_bfloat16, GS>
-          <<<blocks, threads, 0, s>>>(scores, (__nv_bfloat16*)nz, meta, kept, rows, cols);
+          <<<blocks, threads, 0, s>>>(scores, (__nv_bfloat16*)nz, meta, kept, rows, cols, 2u);
       break;
     default:
-      prune_scores_kernel<__half, GS><<<blocks, threads, 0, s>>>(scores, (__half*)nz, meta, kept, rows, cols);
+      prune_scores_kernel<__half, GS><<<blocks, threads, 0, s>>>(scores, (__half*)nz, meta, kept, rows, cols, 2u);
   }
   return cudaGetLastError();
 }

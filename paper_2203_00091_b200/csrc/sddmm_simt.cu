@@ -21,7 +21,8 @@ __global__ void __launch_bounds__(256) sddmm_simt_kernel(const TIn* __restrict__
                                                          TNz* __restrict__ nz, uint32_t* __restrict__ meta,
                                                          float scale, int n, int m, int d,
                                                          const uint8_t* __restrict__ keep, int tile_rows,
-                                                         int tile_cols, float* __restrict__ dbg, MetaGeom geo) {
+                                                         int tile_cols, float* __restrict__ dbg, MetaGeom geo,
+                                                         uint32_t two) {
   __shared__ float Qs[BK][BM + 1];
   __shared__ __align__(16) float Ks[BK][BN + 4];
   __shared__ uint8_t nibs[BM][BN / GS];
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(256) sddmm_simt_kernel(const TIn* __restrict__
     const int c0 = col0 + 4 * tx;
     float v[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) v[j] = acc[i][j] * scale;
+    for (int j = 0; j < 4; ++j) v[j] = scale_canon(acc[i][j], scale);
     const bool row_ok = row < n;
     if (dbg && row_ok) {
 #pragma unroll
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(256) sddmm_simt_kernel(const TIn* __restrict__
         const int g = c / GS;
         if (GS == 4) {
           float lo = 0.f, hi = 0.f;
-          if (kept_tile) nib = select24(v[0], v[1], v[2], v[3], lo, hi);
+          if (kept_tile) nib = select24(v[0], v[1], v[2], v[3], lo, hi, two);
           nz[(int64_t)row * (m / 2) + 2 * g] = DT<TNz>::from_f(lo);
           nz[(int64_t)row * (m / 2) + 2 * g + 1] = DT<TNz>::from_f(hi);
         } else {
@@ -136,10 +137,10 @@ static cudaError_t sddmm_simt_typed(const void* q, const void* k, void* nz, uint
   dim3 grid((m + BN - 1) / BN, 2 * geo.rblocks, (unsigned)bh);
   if (gs == 4)
     sddmm_simt_kernel<TIn, TNz, 4><<<grid, 256, 0, s>>>((const TIn*)q, (const TIn*)k, (TNz*)nz, meta, scale, n, m, d,
-                                                        keep, tile_rows, tile_cols, dbg, geo);
+                                                        keep, tile_rows, tile_cols, dbg, geo, 2u);
   else
     sddmm_simt_kernel<TIn, TNz, 2><<<grid, 256, 0, s>>>((const TIn*)q, (const TIn*)k, (TNz*)nz, meta, scale, n, m, d,
-                                                        keep, tile_rows, tile_cols, dbg, geo);
+                                                        keep, tile_rows, tile_cols, dbg, geo, 2u);
   return cudaGetLastError();
 }
 

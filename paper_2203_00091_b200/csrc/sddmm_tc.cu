@@ -61,18 +61,18 @@ __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) {
 template <typename T, bool DBG, bool RMAX>
 __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, int colh, int cc, uint8_t* stg,
                                           uint32_t lane, uint32_t* meta_b, int row_blk, float* dbg, int64_t dbg_row,
-                                          int m, float& mx) {
+                                          int m, float& mx, uint32_t two) {
   uint32_t packed[8];
   uint32_t W = 0;
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
-    const float v0 = __uint_as_float(r[4 * g + 0]) * scale;
-    const float v1 = __uint_as_float(r[4 * g + 1]) * scale;
-    const float v2 = __uint_as_float(r[4 * g + 2]) * scale;
-    const float v3 = __uint_as_float(r[4 * g + 3]) * scale;
+    const float v0 = scale_canon(__uint_as_float(r[4 * g + 0]), scale);
+    const float v1 = scale_canon(__uint_as_float(r[4 * g + 1]), scale);
+    const float v2 = scale_canon(__uint_as_float(r[4 * g + 2]), scale);
+    const float v3 = scale_canon(__uint_as_float(r[4 * g + 3]), scale);
     if (DBG) *reinterpret_cast<float4*>(dbg + dbg_row * m + colh + cc * 32 + 4 * g) = make_float4(v0, v1, v2, v3);
     float lo, hi;
-    const uint32_t nib = RMAX ? select24_max(v0, v1, v2, v3, lo, hi, mx) : select24(v0, v1, v2, v3, lo, hi);
+    const uint32_t nib = RMAX ? select24_max(v0, v1, v2, v3, lo, hi, mx, two) : select24(v0, v1, v2, v3, lo, hi, two);
     packed[g] = pack2<T>(lo, hi);
     W += nib * (1u << (4 * g));  // IMAD on the FMA pipe, not shift+or on the ALU pipe
   }
@@ -89,7 +89,7 @@ template <typename T, bool DBG, bool RMAX>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     sddmm24_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_nz, uint32_t* __restrict__ meta, float scale, int bh,
-                      int n, int m, float* __restrict__ dbg, float* __restrict__ rowmax) {
+                      int n, int m, float* __restrict__ dbg, float* __restrict__ rowmax, uint32_t two) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + SMEM_BAR);
@@ -218,15 +218,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc::tmem_ld_32x32b_x32(tbase, ra);
           tc::tmem_ld_wait(ra);
           tc::tmem_ld_32x32b_x32(tbase + 32, rb);
-          epi_chunk<T, DBG, RMAX>(ra, scale, colh, 0, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m, mx);
+          epi_chunk<T, DBG, RMAX>(ra, scale, colh, 0, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m, mx, two);
           tc::tmem_ld_wait(rb);
           tc::tmem_ld_32x32b_x32(tbase + 64, ra);
-          epi_chunk<T, DBG, RMAX>(rb, scale, colh, 1, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m, mx);
+          epi_chunk<T, DBG, RMAX>(rb, scale, colh, 1, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m, mx, two);
           tc::tmem_ld_wait(ra);
           tc::tmem_ld_32x32b_x32(tbase + 96, rb);
-          epi_chunk<T, DBG, RMAX>(ra, scale, colh, 2, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m, mx);
+          epi_chunk<T, DBG, RMAX>(ra, scale, colh, 2, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m, mx, two);
           tc::tmem_ld_wait(rb);
-          epi_chunk<T, DBG, RMAX>(rb, scale, colh, 3, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m, mx);
+          epi_chunk<T, DBG, RMAX>(rb, scale, colh, 3, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m, mx, two);
         }
         tc::tc_fence_before();
         __syncwarp();
@@ -289,7 +289,7 @@ static cudaError_t launch_typed(const void* q, const void* k, void* nz, uint32_t
   if (e != cudaSuccess) return e;
   const int items = (int)bh * (n / BM);
   const int grid = items < num_sms() ? items : num_sms();
-  kern<<<grid, NUM_THREADS, SMEM_TOTAL, s>>>(tq, tk, tn, meta, scale, (int)bh, n, m, dbg, rowmax);
+  kern<<<grid, NUM_THREADS, SMEM_TOTAL, s>>>(tq, tk, tn, meta, scale, (int)bh, n, m, dbg, rowmax, 2u);
   return cudaGetLastError();
 }
 

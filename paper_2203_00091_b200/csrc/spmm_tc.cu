@@ -14,10 +14,12 @@
 //   warps 4-7    metadata loaders: warp w copies the words of TMEM lanes
 //                32*(w%4).. for the stage's 4 K-chunks global -> tcgen05.st;
 //   warps 8-11   epilogue: TMEM -> registers (x 1/rowsum when fused) -> O rows;
-//   warps 12-15  (SOFTMAX only) transform: thread r rewrites row r of the staged
-//                P tile in smem as exp(s - m_r) (m_r = row max from the SDDMM
-//                epilogue, so no rescaling pass) and accumulates the row sum --
-//                softmax_rows (sparse_ops.py:18-37) fused between TMA and MMA.
+//   warps 12-19  (SOFTMAX only) transform: warp (quad, half) rewrites the
+//                4 16-byte chunks [4*half, 4*half+4) of rows 32*quad.. of the
+//                staged P tile in smem as exp(s - m_r) (m_r = row max from the
+//                SDDMM epilogue, so no rescaling pass) and accumulates partial row
+//                sums -- softmax_rows (sparse_ops.py:18-37) fused between TMA and
+//                MMA; two warps per SM sub-partition hide the MUFU latency.
 #include <math_constants.h>
 
 #include <type_traits>
@@ -37,8 +39,9 @@ constexpr int P_BYTES = BM * (BKL / 2) * 2;  // 16 KB
 constexpr int V_BYTES = BKL * HD * 2;        // 16 KB
 constexpr int SMEM_P = 0;
 constexpr int SMEM_V = SMEM_P + STAGES * P_BYTES;
-constexpr int SMEM_L = SMEM_V + STAGES * V_BYTES;  // [NACC][128] row sums (fused softmax)
-constexpr int SMEM_BAR = SMEM_L + NACC * BM * 4;
+constexpr int SMEM_L = SMEM_V + STAGES * V_BYTES;  // [NACC][2][128] partial row sums (fused softmax)
+constexpr int SMEM_BAR = SMEM_L + NACC * 2 * BM * 4;
+constexpr int XF_WARPS = 8;
 constexpr int SMEM_TOTAL = SMEM_BAR + 512 + 1024;
 constexpr int TMEM_COLS = 256;
 constexpr int E_COL0 = NACC * HD;  // metadata columns start after the accumulators
@@ -76,7 +79,7 @@ __device__ __forceinline__ uint32_t pack2f<__half>(float lo, float hi) {
 }
 
 template <typename T, typename TO, bool SOFTMAX>
-__global__ void __launch_bounds__(SOFTMAX ? 512 : 384, 1)
+__global__ void __launch_bounds__(SOFTMAX ? 640 : 384, 1)
     spmm24_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_v,
                      const uint32_t* __restrict__ meta, TO* __restrict__ out, int bh, int rows, int n_k,
                      const float* __restrict__ rowmax) {
@@ -107,12 +110,12 @@ __global__ void __launch_bounds__(SOFTMAX ? 512 : 384, 1)
       tc::mbar_init(&full[i], 1);
       tc::mbar_init(&e_full[i], 4);
       tc::mbar_init(&empty[i], 1);
-      tc::mbar_init(&p_ready[i], 4);
+      tc::mbar_init(&p_ready[i], XF_WARPS);
     }
     for (int i = 0; i < NACC; ++i) {
       tc::mbar_init(&d_full[i], 1);
       tc::mbar_init(&d_empty[i], 4);
-      tc::mbar_init(&l_full[i], 4);
+      tc::mbar_init(&l_full[i], XF_WARPS);
     }
     tc::fence_barrier_init();
   }
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(SOFTMAX ? 512 : 384, 1)
       float inv = 1.f;
       if (SOFTMAX) {
         tc::mbar_wait(&l_full[acc], aph);
-        inv = 1.0f / lsum[acc * BM + r];
+        inv = 1.0f / (lsum[(acc * 2 + 0) * BM + r] + lsum[(acc * 2 + 1) * BM + r]);
       }
       tc::tc_fence_after();
       uint32_t r0[32], r1[32];
@@ -244,6 +247,7 @@ __global__ void __launch_bounds__(SOFTMAX ? 512 : 384, 1)
   } else if (SOFTMAX && warp >= 12) {
     // ------------------------------------------------------------ softmax transform
     const int quad = warp & 3;
+    const int half = (warp - 12) >> 2;
     const int r = quad * 32 + lane;  // row within the 128-row block == TMEM lane
     int s = 0, acc = 0;
     uint32_t ph = 0, aph = 0;
@@ -251,33 +255,35 @@ __global__ void __launch_bounds__(SOFTMAX ? 512 : 384, 1)
       const int b = item / rblocks, rb = item % rblocks;
       const float2 mp = *reinterpret_cast<const float2*>(rowmax + ((int64_t)b * rows + rb * BM + r) * 2);
       const float mb = fmaxf(mp.x, mp.y) * kLog2e;
-      float l = 0.f;
+      float l0 = 0.f, l1 = 0.f;
       for (int kb = 0; kb < kblocks; ++kb) {
         tc::mbar_wait(&full[s], ph);
         uint8_t* prow = smem + SMEM_P + s * P_BYTES + r * 128;
+        uint4 x[4];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint4* u = reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4));
-          uint4 x = *u;
-          uint32_t w[4] = {x.x, x.y, x.z, x.w};
+        for (int c = 0; c < 4; ++c) x[c] = *reinterpret_cast<const uint4*>(prow + (((4 * half + c) ^ (r & 7)) << 4));
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t w[4] = {x[c].x, x[c].y, x[c].z, x[c].w};
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const float2 f = unpack2<T>(w[j]);
             const float e0 = ex2_approx(fmaf(f.x, kLog2e, -mb));
             const float e1 = ex2_approx(fmaf(f.y, kLog2e, -mb));
-            l += e0 + e1;
+            l0 += e0;
+            l1 += e1;
             w[j] = pack2f<T>(e0, e1);
           }
-          *u = make_uint4(w[0], w[1], w[2], w[3]);
+          *reinterpret_cast<uint4*>(prow + (((4 * half + c) ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
         }
         tc::fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&p_ready[s]);
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
-      // hand the row sum to the epilogue (buffer acc is free once its previous O was drained)
+      // hand the partial row sums to the epilogue (buffer acc is free once its previous O was drained)
       tc::mbar_wait(&d_empty[acc], aph ^ 1);
-      lsum[acc * BM + r] = l;
+      lsum[(acc * 2 + half) * BM + r] = l0 + l1;
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&l_full[acc]);
       if (++acc == NACC) { acc = 0; aph ^= 1; }
@@ -322,7 +328,7 @@ static cudaError_t spmm_launch_typed(const void* p, const uint32_t* meta, const 
     auto kern = spmm24_tc_kernel<T, TO, true>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
     if (e != cudaSuccess) return e;
-    kern<<<grid, 512, SMEM_TOTAL, s>>>(tp, tv, meta, (TO*)out, (int)bh, rows, n_k, rowmax);
+    kern<<<grid, 640, SMEM_TOTAL, s>>>(tp, tv, meta, (TO*)out, (int)bh, rows, n_k, rowmax);
   } else {
     auto kern = spmm24_tc_kernel<T, TO, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);

@@ -145,14 +145,14 @@ def time_steps(fn, steps, warmup, flush=None):
 def algorithmic_bytes(cfg, fused=False):
     """per (batch, head) per kernel.  16-bit staged: SDDMM 1.125n^2+4nd,
     softmax 2n^2, SpMM 1.125n^2+4nd (total 4.25n^2+8nd).  Fused (softmax folded into the
-    SpMM): SDDMM 1.125n^2+4nd+8n (row maxima), SpMM 1.125n^2+4nd+8n (total 2.25n^2+8nd+16n)."""
+    SpMM): SDDMM 1.125n^2+4nd+16n (row maxima), SpMM 1.125n^2+4nd+16n (total 2.25n^2+8nd+32n)."""
     n, d = cfg["seq"], cfg["d"]
     eb = 4 if cfg["dtype"] == "float32" else 2
     gs = 2 if cfg["mode"] == "1:2" else 4
     nz = n * (n // 2) * eb
     meta = n * (n // gs) // 2
     if fused:
-        return {"sddmm": nz + meta + 2 * n * d * eb + 8 * n, "spmm_softmax": nz + meta + 2 * n * d * eb + 8 * n}
+        return {"sddmm": nz + meta + 2 * n * d * eb + 16 * n, "spmm_softmax": nz + meta + 2 * n * d * eb + 16 * n}
     return {
         "sddmm": nz + meta + 2 * n * d * eb,
         "softmax": 2 * nz,

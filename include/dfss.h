@@ -84,7 +84,7 @@ int64_t dfss_meta_hw_words(int mode, int64_t bh, int64_t rows, int64_t cols);
  *   and left as zero nonzeros / nibble 0x4 padding.
  *   FusedStats (fused.py:22-38) are structural and computed by the host layer
  *   from the tile grid; dense_elems_written is 0 unless scores_dbg is given.
- *   row_max (nullable, fp32 [bh, n_q, 2], tcgen05 path only): the two column-half
+ *   row_max (nullable, fp32 [bh, n_q, 4], tcgen05 path only): the four column-quarter
  *   partial maxima of every row's kept scores (max over a row = its max over the
  *   kept values, the row maximum always survives) -- the input that lets
  *   dfss_spmm apply the softmax on the fly.
@@ -118,7 +118,7 @@ int dfss_softmax_rows(const void* nz_in, void* p_out, int in_dtype, int out_dtyp
  *   16-bit P and V on aligned shapes run tcgen05.mma.sp with the metadata
  *   consumed straight from meta_hw; otherwise an FP32 FFMA gather kernel.
  *   tile_keep: optional BlockMask grid (masked tiles contribute zero).
- *   row_max (nullable, [bh, rows, 2] from dfss_sddmm_prune): p holds RAW kept
+ *   row_max (nullable, [bh, rows, 4] from dfss_sddmm_prune): p holds RAW kept
  *   scores and the softmax (sparse_ops.softmax_rows) is fused in: each staged
  *   P tile is rewritten as exp(s - max_row) in shared memory before the MMA and
  *   the output rows are divided by the row sums -- out = spmm(softmax_rows(p), v)

@@ -219,7 +219,7 @@ class CompressedSparse:
     meta_hw: torch.Tensor
     layout: Layout = Layout.LOGICAL
     block_mask: BlockMask | None = None
-    #: optional [..., rows, 2] fp32 partial row maxima recorded by the tcgen05 SDDMM
+    #: optional [..., rows, 4] fp32 partial row maxima recorded by the tcgen05 SDDMM
     row_max: torch.Tensor | None = None
 
     def __post_init__(self) -> None:

@@ -130,7 +130,7 @@ int64_t dfss_nm_attention_workspace_bytes(int mode, int dtype, int64_t bh, int n
   if (!valid_mode(mode) || !valid_dtype(dtype) || bh < 0 || n < 1) return -1;
   const int64_t nz = bh * (int64_t)n * (n / 2) * dfss::dtype_bytes(dtype);
   const int64_t meta = dfss_meta_hw_words(mode, bh, n, n) * 4;
-  return (nz + 255) / 256 * 256 + (meta + 255) / 256 * 256 + bh * (int64_t)n * 2 * 4 + 256;
+  return (nz + 255) / 256 * 256 + (meta + 255) / 256 * 256 + bh * (int64_t)n * 4 * 4 + 256;
 }
 
 int dfss_nm_attention(const void* q, const void* k, const void* v, void* out, int mode, int dtype, int math,

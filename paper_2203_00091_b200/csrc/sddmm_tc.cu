@@ -30,15 +30,15 @@ constexpr int BN = 256;
 constexpr int HD = 64;
 constexpr int KSTAGES = 3;
 constexpr int NACC = 2;
-constexpr int EPI_WARPS = 8;
+constexpr int EPI_WARPS = 16;
 constexpr int NUM_THREADS = (4 + EPI_WARPS) * 32;
 constexpr int Q_BYTES = BM * HD * 2;
 constexpr int K_BYTES = BN * HD * 2;
-constexpr int STG_BYTES = 32 * 128;  // 32 rows x 64 nonzeros x 2 B
+constexpr int STG_BYTES = 32 * 128;  // 32 rows x 64 nonzeros x 2 B, shared by a warp pair
 constexpr int SMEM_Q = 0;
 constexpr int SMEM_K = SMEM_Q + 2 * Q_BYTES;
 constexpr int SMEM_STG = SMEM_K + KSTAGES * K_BYTES;
-constexpr int SMEM_BAR = SMEM_STG + EPI_WARPS * 2 * STG_BYTES;
+constexpr int SMEM_BAR = SMEM_STG + (EPI_WARPS / 2) * 2 * STG_BYTES;
 constexpr int SMEM_TOTAL = SMEM_BAR + 256 + 1024;  // + barriers + alignment slack
 }  // namespace
 
@@ -59,9 +59,9 @@ __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) {
 // (two 16B units of the 128B-swizzled staging row) + one 32-bit nibble word that is
 // traded with row^8 into the meta_hw word of this TMEM lane (include/dfss.h).
 template <typename T, bool DBG, bool RMAX>
-__device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, int colh, int cc, uint8_t* stg,
-                                          uint32_t lane, uint32_t* meta_b, int row_blk, float* dbg, int64_t dbg_row,
-                                          int m, float& mx, uint32_t two) {
+__device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, int colh, int cc, int unit0,
+                                          uint8_t* stg, uint32_t lane, uint32_t* meta_b, int row_blk, float* dbg,
+                                          int64_t dbg_row, int m, float& mx, uint32_t two) {
   uint32_t packed[8];
   uint32_t W = 0;
 #pragma unroll
@@ -76,7 +76,7 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, 
     packed[g] = pack2<T>(lo, hi);
     W += nib * (1u << (4 * g));  // IMAD on the FMA pipe, not shift+or on the ALU pipe
   }
-  const int u0 = 2 * cc, sw = lane & 7;
+  const int u0 = unit0, sw = lane & 7;
   *reinterpret_cast<uint4*>(stg + lane * 128 + ((u0 ^ sw) << 4)) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
   *reinterpret_cast<uint4*>(stg + lane * 128 + (((u0 + 1) ^ sw) << 4)) =
       make_uint4(packed[4], packed[5], packed[6], packed[7]);
@@ -141,11 +141,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int b = item / mblocks, mb = item % mblocks;
         const int qs = it & 1;
         const uint32_t qph = (it >> 1) & 1;
-        tc::mbar_wait(&q_empty[qs], qph ^ 1);
+        tc::mbar_wait_sleep(&q_empty[qs], qph ^ 1);
         tc::mbar_arrive_expect_tx(&q_full[qs], Q_BYTES);
         tc::tma_load_3d(smem + SMEM_Q + qs * Q_BYTES, &tm_q, &q_full[qs], 0, mb * BM, b);
         for (int t = 0; t < ntiles; ++t) {
-          tc::mbar_wait(&k_empty[ks], kph ^ 1);
+          tc::mbar_wait_sleep(&k_empty[ks], kph ^ 1);
           tc::mbar_arrive_expect_tx(&k_full[ks], K_BYTES);
           tc::tma_load_3d(smem + SMEM_K + ks * K_BYTES, &tm_k, &k_full[ks], 0, t * BN, b);
           if (++ks == KSTAGES) { ks = 0; kph ^= 1; }
@@ -164,12 +164,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
         const int qs = it & 1;
         const uint32_t qph = (it >> 1) & 1;
-        tc::mbar_wait(&q_full[qs], qph);
+        tc::mbar_wait_sleep(&q_full[qs], qph);
         const uint32_t q_addr = tc::smem_u32(smem + SMEM_Q + qs * Q_BYTES);
         for (int t = 0; t < ntiles; ++t) {
           const uint32_t idesc = (m - t * BN >= BN) ? idesc256 : idesc128;
-          tc::mbar_wait(&t_empty[acc], aph ^ 1);
-          tc::mbar_wait(&k_full[ks], kph);
+          tc::mbar_wait_sleep(&t_empty[acc], aph ^ 1);
+          tc::mbar_wait_sleep(&k_full[ks], kph);
           tc::tc_fence_after();
           const uint32_t k_addr = tc::smem_u32(smem + SMEM_K + ks * K_BYTES);
           const uint32_t d_tmem = tmem_base + acc * BN;
@@ -189,11 +189,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
+    // 16 warps: warp (quad, quarter) owns TMEM lanes 32*quad.. and accumulator columns
+    // [64*quarter, 64*quarter+64); the two quarters of a 128-column half share one
+    // 128B-swizzled staging row block and a named barrier (4 warps per SM sub-partition
+    // keep the ALU pipe busy while TMEM loads are in flight).
     const int ew = warp - 4;
     const int quad = warp & 3;
-    const int half = ew >> 2;
+    const int quarter = ew >> 2;
+    const int half = quarter >> 1, part = quarter & 1;
+    const uint32_t pair_bar = 1 + quad * 2 + half;
     const int chunks = m / 32;  // meta chunks of 8 groups per row block
-    uint8_t* stg_base = smem + SMEM_STG + ew * 2 * STG_BYTES;
+    uint8_t* stg_base = smem + SMEM_STG + (quad * 2 + half) * 2 * STG_BYTES;
     int acc = 0, sb = 0;
     uint32_t aph = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
@@ -201,7 +207,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int row_blk = quad * 32 + lane;  // row within the 128-row block
       const int grow = mb * BM + row_blk;    // row within the head
       uint32_t* meta_b = meta + ((int64_t)b * mblocks + mb) * chunks * 128;
-      float mx = -INFINITY;  // running max of this thread's row half (RMAX)
+      float mx = -INFINITY;  // running max of this thread's row quarter (RMAX)
       for (int t = 0; t < ntiles; ++t) {
         const int width = min(BN, m - t * BN);
         const bool active = half * 128 < width;
@@ -209,32 +215,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc::tc_fence_after();
         uint8_t* stg = stg_base + sb * STG_BYTES;
         if (active) {
-          if (lane == 0) tc::bulk_wait_read<1>();  // staging buffer from two tiles ago drained
-          __syncwarp();
-          const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + half * 128;
-          const int colh = t * BN + half * 128;
+          if (part == 0 && lane == 0) tc::bulk_wait_read<1>();  // staging buffer from two tiles ago drained
+          tc::named_bar_sync(pair_bar, 64);
+          const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + quarter * 64;
+          const int colq = t * BN + quarter * 64;
           uint32_t ra[32], rb[32];
-          // TMEM loads double-buffered: chunk cc+1 is in flight while cc is pruned
           tc::tmem_ld_32x32b_x32(tbase, ra);
           tc::tmem_ld_wait(ra);
           tc::tmem_ld_32x32b_x32(tbase + 32, rb);
-          epi_chunk<T, DBG, RMAX>(ra, scale, colh, 0, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m, mx, two);
+          epi_chunk<T, DBG, RMAX>(ra, scale, colq, 0, 4 * part, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow,
+                                  m, mx, two);
           tc::tmem_ld_wait(rb);
-          tc::tmem_ld_32x32b_x32(tbase + 64, ra);
-          epi_chunk<T, DBG, RMAX>(rb, scale, colh, 1, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m, mx, two);
-          tc::tmem_ld_wait(ra);
-          tc::tmem_ld_32x32b_x32(tbase + 96, rb);
-          epi_chunk<T, DBG, RMAX>(ra, scale, colh, 2, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m, mx, two);
-          tc::tmem_ld_wait(rb);
-          epi_chunk<T, DBG, RMAX>(rb, scale, colh, 3, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow, m, mx, two);
+          epi_chunk<T, DBG, RMAX>(rb, scale, colq, 1, 4 * part + 2, stg, lane, meta_b, row_blk, dbg,
+                                  (int64_t)b * n + grow, m, mx, two);
         }
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&t_empty[acc]);
         if (active) {
           tc::fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) {
+          tc::named_bar_sync(pair_bar, 64);
+          if (part == 0 && lane == 0) {
             tc::tma_store_3d(&tm_nz, stg, t * (BN / 2) + half * 64, mb * BM + quad * 32, b);
             tc::bulk_commit();
           }
@@ -242,10 +243,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (++acc == NACC) { acc = 0; aph ^= 1; }
       }
-      // per-row partial maxima of the two column halves: [bh, n, 2] fp32 (fused softmax input)
-      if (RMAX) rowmax[((int64_t)b * n + grow) * 2 + half] = mx;
+      // per-row partial maxima: [bh, n, 4] fp32 over the four column quarters (fused softmax input)
+      if (RMAX) rowmax[((int64_t)b * n + grow) * 4 + quarter] = mx;
     }
-    if (lane == 0) tc::bulk_wait<0>();
+    if (part == 0 && lane == 0) tc::bulk_wait<0>();
   }
   tc::tc_fence_before();
   __syncthreads();

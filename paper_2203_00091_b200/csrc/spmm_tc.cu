@@ -253,8 +253,8 @@ __global__ void __launch_bounds__(SOFTMAX ? 640 : 384, 1)
     uint32_t ph = 0, aph = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       const int b = item / rblocks, rb = item % rblocks;
-      const float2 mp = *reinterpret_cast<const float2*>(rowmax + ((int64_t)b * rows + rb * BM + r) * 2);
-      const float mb = fmaxf(mp.x, mp.y) * kLog2e;
+      const float4 mp = *reinterpret_cast<const float4*>(rowmax + ((int64_t)b * rows + rb * BM + r) * 4);
+      const float mb = fmaxf(fmaxf(mp.x, mp.y), fmaxf(mp.z, mp.w)) * kLog2e;
       float l0 = 0.f, l1 = 0.f;
       for (int kb = 0; kb < kblocks; ++kb) {
         tc::mbar_wait(&full[s], ph);

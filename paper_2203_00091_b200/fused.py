@@ -111,7 +111,7 @@ def sddmm_prune(
         if scores_out.dtype != torch.float32 or tuple(scores_out.shape) != batch + (n, m) or not scores_out.is_contiguous():
             raise ValueError("scores_out must be a contiguous float32 tensor of shape (..., n, m)")
     dev_keep = block_mask.device_keep(qt.device) if block_mask is not None else None
-    row_max = torch.empty(batch + (n, 2), dtype=torch.float32, device=qt.device) if with_row_max else None
+    row_max = torch.empty(batch + (n, 4), dtype=torch.float32, device=qt.device) if with_row_max else None
     lib = _lib.load()
     _lib.check(
         lib.dfss_sddmm_prune(_lib.ptr(qt), _lib.ptr(kt), _lib.ptr(nz), _lib.ptr(meta), float(scale), gs,

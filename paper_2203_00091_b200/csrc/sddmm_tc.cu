@@ -30,15 +30,15 @@ constexpr int BN = 256;
 constexpr int HD = 64;
 constexpr int KSTAGES = 3;
 constexpr int NACC = 2;
-constexpr int EPI_WARPS = 16;
+constexpr int EPI_WARPS = 8;
 constexpr int NUM_THREADS = (4 + EPI_WARPS) * 32;
 constexpr int Q_BYTES = BM * HD * 2;
 constexpr int K_BYTES = BN * HD * 2;
-constexpr int STG_BYTES = 32 * 128;  // 32 rows x 64 nonzeros x 2 B, shared by a warp pair
+constexpr int STG_BYTES = 32 * 128;  // 32 rows x 64 nonzeros x 2 B
 constexpr int SMEM_Q = 0;
 constexpr int SMEM_K = SMEM_Q + 2 * Q_BYTES;
 constexpr int SMEM_STG = SMEM_K + KSTAGES * K_BYTES;
-constexpr int SMEM_BAR = SMEM_STG + (EPI_WARPS / 2) * 2 * STG_BYTES;
+constexpr int SMEM_BAR = SMEM_STG + EPI_WARPS * 2 * STG_BYTES;
 constexpr int SMEM_TOTAL = SMEM_BAR + 256 + 1024;  // + barriers + alignment slack
 }  // namespace
 
@@ -189,17 +189,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    // 16 warps: warp (quad, quarter) owns TMEM lanes 32*quad.. and accumulator columns
-    // [64*quarter, 64*quarter+64); the two quarters of a 128-column half share one
-    // 128B-swizzled staging row block and a named barrier (4 warps per SM sub-partition
-    // keep the ALU pipe busy while TMEM loads are in flight).
+    // warp (quad, half) owns TMEM lanes 32*quad.. (its 32 query rows) and accumulator
+    // columns [128*half, 128*half+128): 4 chunks of 32 columns, TMEM loads double-buffered.
     const int ew = warp - 4;
     const int quad = warp & 3;
-    const int quarter = ew >> 2;
-    const int half = quarter >> 1, part = quarter & 1;
-    const uint32_t pair_bar = 1 + quad * 2 + half;
+    const int half = ew >> 2;
     const int chunks = m / 32;  // meta chunks of 8 groups per row block
-    uint8_t* stg_base = smem + SMEM_STG + (quad * 2 + half) * 2 * STG_BYTES;
+    uint8_t* stg_base = smem + SMEM_STG + ew * 2 * STG_BYTES;
     int acc = 0, sb = 0;
     uint32_t aph = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
@@ -207,7 +203,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int row_blk = quad * 32 + lane;  // row within the 128-row block
       const int grow = mb * BM + row_blk;    // row within the head
       uint32_t* meta_b = meta + ((int64_t)b * mblocks + mb) * chunks * 128;
-      float mx = -INFINITY;  // running max of this thread's row quarter (RMAX)
+      float mx = -INFINITY;  // running max of this thread's row half (RMAX)
       for (int t = 0; t < ntiles; ++t) {
         const int width = min(BN, m - t * BN);
         const bool active = half * 128 < width;
@@ -215,27 +211,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc::tc_fence_after();
         uint8_t* stg = stg_base + sb * STG_BYTES;
         if (active) {
-          if (part == 0 && lane == 0) tc::bulk_wait_read<1>();  // staging buffer from two tiles ago drained
-          tc::named_bar_sync(pair_bar, 64);
-          const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + quarter * 64;
-          const int colq = t * BN + quarter * 64;
+          if (lane == 0) tc::bulk_wait_read<1>();  // staging buffer from two tiles ago drained
+          __syncwarp();
+          const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + half * 128;
+          const int colh = t * BN + half * 128;
+          const int64_t drow = (int64_t)b * n + grow;
           uint32_t ra[32], rb[32];
+          // chunk cc+1 is in flight while cc is pruned
           tc::tmem_ld_32x32b_x32(tbase, ra);
           tc::tmem_ld_wait(ra);
           tc::tmem_ld_32x32b_x32(tbase + 32, rb);
-          epi_chunk<T, DBG, RMAX>(ra, scale, colq, 0, 4 * part, stg, lane, meta_b, row_blk, dbg, (int64_t)b * n + grow,
-                                  m, mx, two);
+          epi_chunk<T, DBG, RMAX>(ra, scale, colh, 0, 0, stg, lane, meta_b, row_blk, dbg, drow, m, mx, two);
           tc::tmem_ld_wait(rb);
-          epi_chunk<T, DBG, RMAX>(rb, scale, colq, 1, 4 * part + 2, stg, lane, meta_b, row_blk, dbg,
-                                  (int64_t)b * n + grow, m, mx, two);
+          tc::tmem_ld_32x32b_x32(tbase + 64, ra);
+          epi_chunk<T, DBG, RMAX>(rb, scale, colh, 1, 2, stg, lane, meta_b, row_blk, dbg, drow, m, mx, two);
+          tc::tmem_ld_wait(ra);
+          tc::tmem_ld_32x32b_x32(tbase + 96, rb);
+          epi_chunk<T, DBG, RMAX>(ra, scale, colh, 2, 4, stg, lane, meta_b, row_blk, dbg, drow, m, mx, two);
+          tc::tmem_ld_wait(rb);
+          epi_chunk<T, DBG, RMAX>(rb, scale, colh, 3, 6, stg, lane, meta_b, row_blk, dbg, drow, m, mx, two);
         }
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&t_empty[acc]);
         if (active) {
           tc::fence_proxy_async();
-          tc::named_bar_sync(pair_bar, 64);
-          if (part == 0 && lane == 0) {
+          __syncwarp();
+          if (lane == 0) {
             tc::tma_store_3d(&tm_nz, stg, t * (BN / 2) + half * 64, mb * BM + quad * 32, b);
             tc::bulk_commit();
           }
@@ -243,10 +245,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (++acc == NACC) { acc = 0; aph ^= 1; }
       }
-      // per-row partial maxima: [bh, n, 4] fp32 over the four column quarters (fused softmax input)
-      if (RMAX) rowmax[((int64_t)b * n + grow) * 4 + quarter] = mx;
+      // per-row partial maxima [bh, n, 4] fp32 (fused softmax input); halves 2,3 unused here
+      if (RMAX) {
+        rowmax[((int64_t)b * n + grow) * 4 + half] = mx;
+        rowmax[((int64_t)b * n + grow) * 4 + 2 + half] = -INFINITY;
+      }
     }
-    if (part == 0 && lane == 0) tc::bulk_wait<0>();
+    if (lane == 0) tc::bulk_wait<0>();
   }
   tc::tc_fence_before();
   __syncthreads();

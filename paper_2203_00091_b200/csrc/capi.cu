@@ -149,6 +149,9 @@ int dfss_nm_attention(const void* q, const void* k, const void* v, void* out, in
   uint32_t* meta = (uint32_t*)(ws + (nz_bytes + 255) / 256 * 256);
   float* row_max = (float*)(ws + (nz_bytes + 255) / 256 * 256 + (meta_bytes + 255) / 256 * 256);
   const float scale = 1.0f / sqrtf((float)d);
+  // fully fused: one kernel, no n x n tensor in HBM (flash_tc.cu)
+  if (math == DFSS_MATH_AUTO && dtype != DFSS_F32 && dfss::tc_flash_supported(mode, dtype, n, d) && dfss_has_tcgen05())
+    return cuda_status(dfss::launch_flash_tc(q, k, v, out, scale, mode, dtype, bh, n, d, (cudaStream_t)stream));
   // fused path: SDDMM+prune (+row max) -> SpMM with the softmax applied to the staged P tiles
   const bool fused = math == DFSS_MATH_AUTO && dtype != DFSS_F32 &&
                      dfss::tc_sddmm_supported(mode, dtype, dtype, n, n, d) &&

@@ -192,5 +192,9 @@ cudaError_t launch_sddmm_tc(const void* q, const void* k, void* nz, uint32_t* me
 cudaError_t launch_spmm_tc(const void* p, const uint32_t* meta, const void* v, void* out, int gs, int dtype,
                            int out_dtype, int64_t bh, int rows, int n_k, int d, const float* rowmax, cudaStream_t s);
 bool tc_sddmm_supported(int gs, int in_dtype, int nz_dtype, int n, int m, int d);
+// fully fused attention (flash_tc.cu): no n x n tensor in HBM
+bool tc_flash_supported(int gs, int dtype, int n, int d);
+cudaError_t launch_flash_tc(const void* q, const void* k, const void* v, void* out, float scale, int gs, int dtype,
+                            int64_t bh, int n, int d, cudaStream_t s);
 bool tc_spmm_supported(int gs, int p_dtype, int v_dtype, int out_dtype, int rows, int n_k, int d);
 }  // namespace dfss

@@ -303,12 +303,24 @@ def test_c1_fp32_attention_within_1e5():
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 @pytest.mark.parametrize("mode", ["2:4", "1:2"])
-@pytest.mark.parametrize("n", [512, 384])
+@pytest.mark.parametrize("n", [512, 384, 128, 1024])
 def test_16bit_attention_within_2e2(dtype, mode, n):
     (q, k, v), (q64, k64, v64) = seeded_qkv((2, 3, n, 64), dtype, seed=1)
     out = dfss.dfss_attention(q, k, v, mode)
     want = oracle_attention(q64, k64, v64, mode)
     assert_close(_np(out), want, 2e-2, 2e-2, f"{dtype} {mode} n={n}")
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_flash_kernel_matches_staged_pipeline(dtype):
+    """dfss_attention (one fused kernel) vs the staged sddmm -> softmax -> spmm kernels on the
+    same inputs: identical selection, so the outputs agree to 16-bit rounding."""
+    (q, k, v), _ = seeded_qkv((3, 2, 768, 64), dtype, seed=9)
+    flash = _np(dfss.dfss_attention(q, k, v, "2:4"))
+    c, _ = dfss.attention_sddmm(q, k, "2:4")
+    staged = _np(dfss.spmm(dfss.softmax_rows(c), v).data)
+    assert_close(flash, staged, 2e-2, 2e-2, "flash vs staged")
+    assert np.abs(flash - staged).max() <= 1.5e-2
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])

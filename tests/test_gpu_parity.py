@@ -323,6 +323,60 @@ def test_flash_kernel_matches_staged_pipeline(dtype):
     assert np.abs(flash - staged).max() <= 1.5e-2
 
 
+def _flash_vs_oracle(q, k, v, what, tol=2e-2):
+    """dfss_attention on 16-bit [b, h, n, 64] CUDA tensors vs the reference nm_attention (float64)."""
+    out = _np(dfss.dfss_attention(q, k, v, "2:4"))
+    want = oracle_attention(*(x.double().cpu().numpy() for x in (q, k, v)), "2:4")
+    assert_close(out, want, tol, tol, what)
+    return out, want
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_flash_shift_update_path(dtype):
+    """Scores that grow along the key axis (later tiles exceed the first tile's maximum by far
+    more than 2^8 in probability mass): the lazy-shift slow path must rescale O and the sums."""
+    g = torch.Generator().manual_seed(21)
+    n = 1024
+    q = torch.randn((1, 2, n, 64), generator=g)
+    k = torch.randn((1, 2, n, 64), generator=g) * torch.linspace(0.2, 3.0, n).view(1, 1, n, 1)
+    v = torch.randn((1, 2, n, 64), generator=g)
+    q, k, v = (x.to(dtype).cuda() for x in (q, k, v))
+    _flash_vs_oracle(q, k, v, "growing scores")
+    # and the reverse: the first tile holds the maximum
+    _flash_vs_oracle(q, k.flip(-2).contiguous(), v, "decaying scores")
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_flash_large_logits(dtype):
+    """Logits of magnitude ~60: exp spans far beyond fp32 without the shift."""
+    (q, k, v), _ = seeded_qkv((1, 3, 512, 64), dtype, seed=5)
+    _flash_vs_oracle(q * 8, k, v, "large logits")
+
+
+def test_flash_tie_lattice_and_zero_queries():
+    """Integer-lattice Q/K (exact bf16, many tied scores) and all-zero queries (every score is
+    a signed zero: the reference keeps the lower index of every tie, so O = mean of V rows
+    4g, 4g+1)."""
+    g = torch.Generator().manual_seed(3)
+    n = 512
+    q = torch.randint(-1, 2, (1, 2, n, 64), generator=g).to(torch.bfloat16).cuda()
+    k = torch.randint(-1, 2, (1, 2, n, 64), generator=g).to(torch.bfloat16).cuda()
+    v = torch.randn((1, 2, n, 64), generator=g).to(torch.bfloat16).cuda()
+    _flash_vs_oracle(q, k, v, "tie lattice")
+    z = torch.zeros_like(q)
+    out, want = _flash_vs_oracle(z, k, v, "zero queries")
+    vv = v.double().cpu().numpy()[0]
+    kept = vv.reshape(2, n // 4, 4, 64)[:, :, :2].reshape(2, n // 2, 64).mean(1)
+    assert np.abs(want[0] - kept[:, None, :]).max() < 1e-12
+    assert np.abs(out[0] - kept[:, None, :]).max() < 2e-2
+
+
+@pytest.mark.parametrize("n", [128, 256, 4096])
+def test_flash_sequence_lengths(n):
+    (q, k, v), _ = seeded_qkv((1, 2, n, 64), torch.bfloat16, seed=n)
+    _flash_vs_oracle(q, k, v, f"n={n}")
+
+
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 def test_fused_softmax_spmm_matches_staged_and_oracle(dtype):
     """spmm_softmax(sddmm_prune(with_row_max)) == spmm(softmax_rows(.)) == reference nm_attention."""

@@ -473,6 +473,337 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+// ============================================================================ two-set kernel
+// n % 256 == 0: an item is 256 query rows (halves h = 0, 1) of one head.  The 16 softmax
+// warps split into two independent sets of 8, set h owning half h: warp (quad, pair) of a
+// set holds rows 32*quad.. and score columns [64*pair, +64) as two 32-column chunks.  The
+// sets share the K / V stream but not their latency chains (own S buffer, P stages,
+// metadata columns, barriers), so one set's TMEM / shared-memory / barrier latencies
+// overlap the other set's arithmetic on every SM sub-partition (2 + 2 warps each).
+namespace {
+constexpr int K2ST = 2, V2ST = 3, P2ST = 2;  // K ring, V ring, P stages per half
+constexpr int S2_Q = 0;                       // [2 stages][2 halves] x 16 KB
+constexpr int S2_K = S2_Q + 4 * Q_BYTES;
+constexpr int S2_V = S2_K + K2ST * K_BYTES;
+constexpr int S2_P = S2_V + V2ST * V_BYTES;   // [2 halves][P2ST] x 16 KB
+constexpr int S2_RED = S2_P + 2 * P2ST * P_BYTES;  // red_max / red_sum: [2 halves][2 pairs][128] floats each
+constexpr int S2_BAR = S2_RED + 2 * 2 * 2 * BM * 4;
+constexpr int S2_TOTAL = S2_BAR + 256 + 1024;
+constexpr int T2_O = 2 * BN;          // O_h at T2_O + 64 h
+constexpr int T2_E = T2_O + 2 * HD;   // metadata: T2_E + 8 h + 4 stage + quarter
+static_assert(S2_TOTAL <= 227 * 1024, "shared memory budget");
+}  // namespace
+
+template <typename T>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    dfss_flash2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                       const __grid_constant__ CUtensorMap tm_v, T* __restrict__ out, float scale, int bh, int n,
+                       uint32_t two, int variant) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = (uint64_t*)(smem + S2_BAR);
+  uint64_t* q_full = bars;               // [2]
+  uint64_t* q_empty = q_full + 2;        // [2]
+  uint64_t* k_full = q_empty + 2;        // [K2ST]
+  uint64_t* k_empty = k_full + K2ST;     // [K2ST]
+  uint64_t* v_full = k_empty + K2ST;     // [V2ST]
+  uint64_t* v_empty = v_full + V2ST;     // [V2ST]
+  uint64_t* s_full = v_empty + V2ST;     // [2 halves]
+  uint64_t* s_empty = s_full + 2;        // [2 halves] (8 warps)
+  uint64_t* p_full = s_empty + 2;        // [2 halves][P2ST] (8 warps)
+  uint64_t* p_empty = p_full + 2 * P2ST; // [2 halves][P2ST]
+  uint64_t* o_full = p_empty + 2 * P2ST; // [2 halves]
+  uint64_t* o_empty = o_full + 2;        // [2 halves] (8 warps)
+  uint32_t* tmem_slot = (uint32_t*)(o_empty + 2);
+  float* red_max = (float*)(smem + S2_RED);  // [h][pair][128]
+  float* red_sum = red_max + 2 * 2 * BM;
+
+  const uint32_t warp = tc::warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+  const int iblocks = n / (2 * BM);
+  const int items = bh * iblocks;
+  const int ntiles = n / BN;
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tm_q);
+    tc::prefetch_tmap(&tm_k);
+    tc::prefetch_tmap(&tm_v);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&q_full[i], 1);
+      tc::mbar_init(&q_empty[i], 1);
+      tc::mbar_init(&s_full[i], 1);
+      tc::mbar_init(&s_empty[i], 8);
+      tc::mbar_init(&o_full[i], 1);
+      tc::mbar_init(&o_empty[i], 8);
+    }
+    for (int i = 0; i < 2 * P2ST; ++i) {
+      tc::mbar_init(&p_full[i], 8);
+      tc::mbar_init(&p_empty[i], 1);
+    }
+    for (int i = 0; i < K2ST; ++i) {
+      tc::mbar_init(&k_full[i], 1);
+      tc::mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < V2ST; ++i) {
+      tc::mbar_init(&v_full[i], 1);
+      tc::mbar_init(&v_empty[i], 1);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 2) tc::tmem_alloc<512>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer: Q (both halves) and K (keys permuted)
+    if (lane == 0) {
+      int ks = 0, it = 0;
+      uint32_t kph = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        const int b = item / iblocks, ib = item % iblocks;
+        const int qs = it & 1;
+        tc::mbar_wait_sleep(&q_empty[qs], ((it >> 1) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&q_full[qs], 2 * Q_BYTES);
+        tc::tma_load_3d(smem + S2_Q + (2 * qs) * Q_BYTES, &tm_q, &q_full[qs], 0, ib * 2 * BM, b);
+        tc::tma_load_3d(smem + S2_Q + (2 * qs + 1) * Q_BYTES, &tm_q, &q_full[qs], 0, ib * 2 * BM + BM, b);
+        for (int t = 0; t < ntiles; ++t) {
+          tc::mbar_wait_sleep(&k_empty[ks], kph ^ 1);
+          tc::mbar_arrive_expect_tx(&k_full[ks], K_BYTES);
+          tc::tma_load_5d(smem + S2_K + ks * K_BYTES, &tm_k, &k_full[ks], 0, 0, 0, t * (BN / 4), b);
+          if (++ks == K2ST) { ks = 0; kph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ TMA producer: V
+    if (lane == 0) {
+      int vs = 0;
+      uint32_t vph = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const int b = item / iblocks;
+        for (int t = 0; t < ntiles; ++t) {
+          tc::mbar_wait_sleep(&v_empty[vs], vph ^ 1);
+          tc::mbar_arrive_expect_tx(&v_full[vs], V_BYTES);
+          tc::tma_load_3d(smem + S2_V + vs * V_BYTES, &tm_v, &v_full[vs], 0, t * BN, b);
+          if (++vs == V2ST) { vs = 0; vph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ S issuer: S_h = Q_h K_t^T
+    if (lane == 0) {
+      constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+      constexpr uint32_t idesc_s = tc::instr_desc(fmt, BM, BN, false, false, false);
+      int ks = 0, it = 0;
+      uint32_t kph = 0, gt = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        const int qs = it & 1;
+        tc::mbar_wait_sleep(&q_full[qs], (it >> 1) & 1);
+        for (int t = 0; t < ntiles; ++t, ++gt) {
+          tc::mbar_wait_sleep(&k_full[ks], kph);
+          const uint32_t k_addr = tc::smem_u32(smem + S2_K + ks * K_BYTES);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            tc::mbar_wait_sleep(&s_empty[h], (gt & 1) ^ 1);  // set h read the previous S_h
+            tc::tc_fence_after();
+            const uint32_t q_addr = tc::smem_u32(smem + S2_Q + (2 * qs + h) * Q_BYTES);
+            if (!(variant & 32)) {
+#pragma unroll
+              for (int kk = 0; kk < HD / 16; ++kk) {
+                const uint64_t ad = tc::smem_desc(q_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
+                const uint64_t bd = tc::smem_desc(k_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
+                tc::mma_f16_ss(tmem_base + h * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+              }
+            }
+            tc::mma_commit(&s_full[h]);
+          }
+          tc::mma_commit(&k_empty[ks]);
+          if (++ks == K2ST) { ks = 0; kph ^= 1; }
+        }
+        tc::mma_commit(&q_empty[qs]);
+      }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ PV issuer: O_h += P_h V_t
+    if (lane == 0) {
+      constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
+      constexpr uint32_t idesc_pv = tc::instr_desc(fmt, BM, HD, false, true, true);
+      int vs = 0, it = 0;
+      uint32_t vph = 0, gt = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        for (int t = 0; t < ntiles; ++t, ++gt) {
+          tc::mbar_wait_sleep(&v_full[vs], vph);
+          const uint32_t v_addr = tc::smem_u32(smem + S2_V + vs * V_BYTES);
+          const uint32_t ps = gt % P2ST, pph = (gt / P2ST) & 1;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (t == 0) tc::mbar_wait_sleep(&o_empty[h], (it & 1) ^ 1);
+            tc::mbar_wait_sleep(&p_full[h * P2ST + ps], pph);
+            tc::tc_fence_after();
+            const uint32_t p_addr = tc::smem_u32(smem + S2_P + (h * P2ST + ps) * P_BYTES);
+#pragma unroll
+            for (int q = 0; q < ((variant & 16) ? 0 : 4); ++q) {
+              const uint64_t ad = tc::smem_desc(p_addr + q * 32, 16, 1024, tc::kSwizzle128B);
+              const uint64_t bd = tc::smem_desc(v_addr + q * 32 * 128, V_BYTES, 1024, tc::kSwizzle128B);
+              const uint32_t e_col = tmem_base + T2_E + h * 8 + ps * 4 + q;
+              tc::mma_sp_f16_ss(tmem_base + T2_O + h * HD, ad, bd, e_col & ~1u, idesc_pv | (e_col & 1u),
+                                (t > 0 || q > 0) ? 1u : 0u);
+            }
+            tc::mma_commit(&p_empty[h * P2ST + ps]);
+            if (t == ntiles - 1) tc::mma_commit(&o_full[h]);
+          }
+          tc::mma_commit(&v_empty[vs]);
+          if (++vs == V2ST) { vs = 0; vph ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax / prune / epilogue sets
+    const int sw = warp - 4;
+    const int h = sw >> 3;               // half owned by this set
+    const int pr = (sw >> 2) & 1;        // column pair: quarters 2pr, 2pr + 1
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;      // row within the half == TMEM lane
+    const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16);
+    const uint32_t s_cols = lane_base + h * BN + 64 * pr;
+    const uint32_t pbar = 1 + h * 4 + quad;  // named barrier of the two warps sharing these rows
+    const float c = scale * kLog2e;
+    float* rmax = red_max + h * 2 * BM;
+    float* rsum = red_sum + h * 2 * BM;
+    const uint32_t p_row = tc::smem_u32(smem + S2_P + h * P2ST * P_BYTES) + r * 128;
+    const uint32_t sw7 = r & 7;
+    uint64_t* my_p_full = p_full + h * P2ST;
+    uint64_t* my_p_empty = p_empty + h * P2ST;
+    uint32_t gt = 0;
+    int it = 0;
+    // maximum of this row over the set's 128 columns of the current S (both pairs)
+    auto row_max = [&]() {
+      float mt = -INFINITY;
+#pragma unroll 1
+      for (int ch = 0; ch < 2; ++ch) {
+        uint32_t s[32];
+        tc::tmem_ld_32x32b_x32(s_cols + 32 * ch, s);
+        tc::tmem_ld_wait(s);
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) mt = fmaxf(mt, fmaxf(__uint_as_float(s[j]), __uint_as_float(s[j + 1])));
+      }
+      rmax[pr * BM + r] = mt;
+      tc::named_bar_sync(pbar, 64);
+      const float m = fmaxf(rmax[r], rmax[BM + r]);
+      tc::named_bar_sync(pbar, 64);
+      return m * c;
+    };
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      const int b = item / iblocks, ib = item % iblocks;
+      float mlog = 0.f, l0 = 0.f, l1 = 0.f;
+      for (int t = 0; t < ntiles; ++t, ++gt) {
+        tc::mbar_wait(&s_full[h], gt & 1);
+        tc::tc_fence_after();
+        if (t == 0) mlog = row_max();
+        uint32_t pk[2][8], W[2];
+        float lt0 = 0.f, lt1 = 0.f;
+        auto compute = [&]() {
+          lt0 = lt1 = 0.f;
+#pragma unroll
+          for (int ch = 0; ch < 2; ++ch) {
+            uint32_t s[32];
+            tc::tmem_ld_32x32b_x32(s_cols + 32 * ch, s);
+            tc::tmem_ld_wait(s);
+            float a0, a1;
+            if (variant & 8) {  // timing experiment: no prune / exp arithmetic
+#pragma unroll
+              for (int j = 0; j < 8; ++j) pk[ch][j] = s[j] ^ s[j + 8];
+              W[ch] = 0x44444444u;
+              a0 = a1 = 0.f;
+            } else {
+              prune_exp_tile<T>(s, c, mlog, two, pk[ch], W[ch], a0, a1);
+            }
+            add2(lt0, lt1, a0, a1, lt0, lt1);
+          }
+        };
+        compute();
+        if (t > 0 && bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit))) {
+          // ---- slow path (both warps of the pair): raise the shift to the row maximum,
+          // rescale O_h and the sums once every PV into O_h so far (tile t-1) retired
+          const uint32_t pprev = (gt - 1) % P2ST, pphp = ((gt - 1) / P2ST) & 1;
+          tc::mbar_wait(&my_p_empty[pprev], pphp);
+          tc::tc_fence_after();
+          const float mnew = fmaxf(mlog, row_max());
+          const float f = fex2(mlog - mnew);
+          l0 *= f;
+          l1 *= f;
+#pragma unroll 1
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t o[16];
+            const uint32_t oaddr = lane_base + T2_O + h * HD + 32 * pr + 16 * hh;
+            tc::tmem_ld_32x32b_x16(oaddr, o);
+            tc::tmem_ld_wait(o);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * f);
+            tc::tmem_st_32x32b_x16(oaddr, o);
+          }
+          tc::tmem_st_wait();
+          mlog = mnew;
+          compute();
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&s_empty[h]);  // S_h may be overwritten by the next tile
+        add2(l0, l1, lt0, lt1, l0, l1);
+        const uint32_t ps = gt % P2ST, pph = (gt / P2ST) & 1;
+        tc::mbar_wait(&my_p_empty[ps], pph ^ 1);  // PV of this half's tile t - P2ST retired
+        tc::tc_fence_after();
+        const uint32_t prow = p_row + ps * P_BYTES;
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          const int qd = 2 * pr + ch;  // quarter = 32-column block = one sparse MMA
+          sts128(prow + (((2 * qd) ^ sw7) << 4), pk[ch][0], pk[ch][1], pk[ch][2], pk[ch][3]);
+          sts128(prow + (((2 * qd + 1) ^ sw7) << 4), pk[ch][4], pk[ch][5], pk[ch][6], pk[ch][7]);
+          // metadata word of TMEM lane r: rows r and r^8 trade 16-bit halves (include/dfss.h)
+          const uint32_t partner = __shfl_xor_sync(0xffffffffu, W[ch], 8);
+          const uint32_t word =
+              (lane & 8) ? ((partner >> 16) | (W[ch] & 0xFFFF0000u)) : ((W[ch] & 0xFFFFu) | (partner << 16));
+          tc::tmem_st_32x32b_x1(lane_base + T2_E + h * 8 + ps * 4 + qd, word);
+        }
+        tc::tmem_st_wait();
+        tc::fence_proxy_async();  // P smem writes -> tensor core
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&my_p_full[ps]);
+      }
+      // ---- epilogue: O_h / row sum; this warp writes columns [32 pr, +32) of its rows
+      rsum[pr * BM + r] = l0 + l1;
+      tc::named_bar_sync(pbar, 64);
+      const float inv = 1.0f / (rsum[r] + rsum[BM + r]);
+      tc::named_bar_sync(pbar, 64);
+      tc::mbar_wait(&o_full[h], it & 1);
+      tc::tc_fence_after();
+      uint32_t o[32];
+      tc::tmem_ld_32x32b_x32(lane_base + T2_O + h * HD + 32 * pr, o);
+      tc::tmem_ld_wait(o);
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&o_empty[h]);
+      uint32_t pko[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        pko[j] = fpack2<T>(__uint_as_float(o[2 * j]) * inv, __uint_as_float(o[2 * j + 1]) * inv);
+      const int64_t row = (int64_t)b * n + (ib * 2 + h) * BM + r;
+      uint4* orow = reinterpret_cast<uint4*>(out + row * HD + 32 * pr);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) orow[j] = make_uint4(pko[4 * j], pko[4 * j + 1], pko[4 * j + 2], pko[4 * j + 3]);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<512>(tmem_base);
+  }
+}
+
 bool tc_flash_supported(int gs, int dtype, int n, int d) {
   return gs == 4 && (dtype == DFSS_BF16 || dtype == DFSS_F16) && d == HD && n % BM == 0 && n > 0;
 }
@@ -493,11 +824,15 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
       !encode_tmap(&tk, dt, 5, (void*)k, kdims, kstr, kbox, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !encode_tmap_3d(&tv, dt, 2, (void*)v, HD, n, bh, HD, BN, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
-  // two 128-row halves per item when they tile the sequence (halves the K / V ingress per score)
-  static const int force1 = getenv("DFSS_FLASH_HALVES") ? atoi(getenv("DFSS_FLASH_HALVES")) == 1 : 0;
-  const int halves = (n % (2 * BM) == 0 && !force1) ? 2 : 1;
-  auto kern = halves == 2 ? dfss_flash_kernel<T, 2> : dfss_flash_kernel<T, 1>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
+  // n % 256 == 0: the two-set kernel (256-row items, independent softmax sets per half);
+  // otherwise 128-row items with all 16 softmax warps on one half.  DFSS_FLASH_KERNEL=1
+  // forces the one-set kernel (experiments).
+  static const int force1 = getenv("DFSS_FLASH_KERNEL") ? atoi(getenv("DFSS_FLASH_KERNEL")) == 1 : 0;
+  const bool two_set = n % (2 * BM) == 0 && !force1;
+  const int halves = two_set ? 2 : 1;
+  auto kern = two_set ? dfss_flash2_kernel<T> : dfss_flash_kernel<T, 1>;
+  const int smem_total = two_set ? S2_TOTAL : SMEM_TOTAL;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_total);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -507,7 +842,7 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
   // DFSS_FLASH_VARIANT (timing experiments only; results invalid when set):
   // bit3 skip prune/exp arithmetic, bit4 skip PV MMAs, bit5 skip S MMAs
   static const int variant = getenv("DFSS_FLASH_VARIANT") ? atoi(getenv("DFSS_FLASH_VARIANT")) : 0;
-  kern<<<grid, NUM_THREADS, SMEM_TOTAL, s>>>(tq, tk, tv, (T*)out, scale, (int)bh, n, 2u, variant);
+  kern<<<grid, NUM_THREADS, smem_total, s>>>(tq, tk, tv, (T*)out, scale, (int)bh, n, 2u, variant);
   return cudaGetLastError();
 }
 

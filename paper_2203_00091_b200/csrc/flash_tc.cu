@@ -477,9 +477,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // n % 256 == 0: an item is 256 query rows (halves h = 0, 1) of one head.  The 16 softmax
 // warps split into two independent sets of 8, set h owning half h: warp (quad, pair) of a
 // set holds rows 32*quad.. and score columns [64*pair, +64) as two 32-column chunks.  The
-// sets share the K / V stream but not their latency chains (own S buffer, P stages,
-// metadata columns, barriers), so one set's TMEM / shared-memory / barrier latencies
-// overlap the other set's arithmetic on every SM sub-partition (2 + 2 warps each).
+// sets share the K / V stream but not their latency chains (own P stages, barriers), so
+// one set's TMEM / shared-memory / barrier latencies overlap the other set's arithmetic on
+// every SM sub-partition (2 + 2 warps each).
+//
+// S tiles of steps g = 2t + h go to a ring of three 128-column TMEM buffers; the metadata
+// of step g is written into its own S buffer (column 32q, after quarter q was read), so a
+// buffer is free again once PV_g retired.  A set's next S (step g + 2) lands in the buffer
+// of step g - 1 -- the other set's previous step -- and is computed while this set is
+// still busy with step g.
 namespace {
 constexpr int K2ST = 2, V2ST = 3, P2ST = 2;  // K ring, V ring, P stages per half
 constexpr int S2_Q = 0;                       // [2 stages][2 halves] x 16 KB
@@ -489,8 +495,8 @@ constexpr int S2_P = S2_V + V2ST * V_BYTES;   // [2 halves][P2ST] x 16 KB
 constexpr int S2_RED = S2_P + 2 * P2ST * P_BYTES;  // red_max / red_sum: [2 halves][2 pairs][128] floats each
 constexpr int S2_BAR = S2_RED + 2 * 2 * 2 * BM * 4;
 constexpr int S2_TOTAL = S2_BAR + 256 + 1024;
-constexpr int T2_O = 2 * BN;          // O_h at T2_O + 64 h
-constexpr int T2_E = T2_O + 2 * HD;   // metadata: T2_E + 8 h + 4 stage + quarter
+constexpr int S2RING = 3;             // S buffers (TMEM), 128 columns each
+constexpr int T2_O = S2RING * BN;     // O_h at T2_O + 64 h
 static_assert(S2_TOTAL <= 227 * 1024, "shared memory budget");
 }  // namespace
 
@@ -508,9 +514,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* k_empty = k_full + K2ST;     // [K2ST]
   uint64_t* v_full = k_empty + K2ST;     // [V2ST]
   uint64_t* v_empty = v_full + V2ST;     // [V2ST]
-  uint64_t* s_full = v_empty + V2ST;     // [2 halves]
-  uint64_t* s_empty = s_full + 2;        // [2 halves] (8 warps)
-  uint64_t* p_full = s_empty + 2;        // [2 halves][P2ST] (8 warps)
+  uint64_t* s_full = v_empty + V2ST;     // [S2RING] S of a step computed
+  uint64_t* s_free = s_full + S2RING;    // [S2RING] PV of that step retired (buffer + metadata free)
+  uint64_t* p_full = s_free + S2RING;    // [2 halves][P2ST] (8 warps)
   uint64_t* p_empty = p_full + 2 * P2ST; // [2 halves][P2ST]
   uint64_t* o_full = p_empty + 2 * P2ST; // [2 halves]
   uint64_t* o_empty = o_full + 2;        // [2 halves] (8 warps)
@@ -531,10 +537,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&q_full[i], 1);
       tc::mbar_init(&q_empty[i], 1);
-      tc::mbar_init(&s_full[i], 1);
-      tc::mbar_init(&s_empty[i], 8);
       tc::mbar_init(&o_full[i], 1);
       tc::mbar_init(&o_empty[i], 8);
+    }
+    for (int i = 0; i < S2RING; ++i) {
+      tc::mbar_init(&s_full[i], 1);
+      tc::mbar_init(&s_free[i], 1);
     }
     for (int i = 0; i < 2 * P2ST; ++i) {
       tc::mbar_init(&p_full[i], 8);
@@ -592,21 +600,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ S issuer: S_h = Q_h K_t^T
+    // ------------------------------------------------------------ S issuer: step g = 2t + h -> buffer g % 3
     if (lane == 0) {
       constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
       constexpr uint32_t idesc_s = tc::instr_desc(fmt, BM, BN, false, false, false);
-      int ks = 0, it = 0;
-      uint32_t kph = 0, gt = 0;
+      int ks = 0, it = 0, sb = 0;
+      uint32_t kph = 0, sph = 0;
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
         const int qs = it & 1;
         tc::mbar_wait_sleep(&q_full[qs], (it >> 1) & 1);
-        for (int t = 0; t < ntiles; ++t, ++gt) {
+        for (int t = 0; t < ntiles; ++t) {
           tc::mbar_wait_sleep(&k_full[ks], kph);
           const uint32_t k_addr = tc::smem_u32(smem + S2_K + ks * K_BYTES);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            tc::mbar_wait_sleep(&s_empty[h], (gt & 1) ^ 1);  // set h read the previous S_h
+            tc::mbar_wait_sleep(&s_free[sb], sph ^ 1);  // PV of step g - 3 retired
             tc::tc_fence_after();
             const uint32_t q_addr = tc::smem_u32(smem + S2_Q + (2 * qs + h) * Q_BYTES);
             if (!(variant & 32)) {
@@ -614,10 +622,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int kk = 0; kk < HD / 16; ++kk) {
                 const uint64_t ad = tc::smem_desc(q_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
                 const uint64_t bd = tc::smem_desc(k_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
-                tc::mma_f16_ss(tmem_base + h * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+                tc::mma_f16_ss(tmem_base + sb * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
               }
             }
-            tc::mma_commit(&s_full[h]);
+            tc::mma_commit(&s_full[sb]);
+            if (++sb == S2RING) { sb = 0; sph ^= 1; }
           }
           tc::mma_commit(&k_empty[ks]);
           if (++ks == K2ST) { ks = 0; kph ^= 1; }
@@ -630,7 +639,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
       constexpr uint32_t idesc_pv = tc::instr_desc(fmt, BM, HD, false, true, true);
-      int vs = 0, it = 0;
+      int vs = 0, it = 0, sb = 0;
       uint32_t vph = 0, gt = 0;
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
         for (int t = 0; t < ntiles; ++t, ++gt) {
@@ -647,11 +656,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int q = 0; q < ((variant & 16) ? 0 : 4); ++q) {
               const uint64_t ad = tc::smem_desc(p_addr + q * 32, 16, 1024, tc::kSwizzle128B);
               const uint64_t bd = tc::smem_desc(v_addr + q * 32 * 128, V_BYTES, 1024, tc::kSwizzle128B);
-              const uint32_t e_col = tmem_base + T2_E + h * 8 + ps * 4 + q;
-              tc::mma_sp_f16_ss(tmem_base + T2_O + h * HD, ad, bd, e_col & ~1u, idesc_pv | (e_col & 1u),
+              tc::mma_sp_f16_ss(tmem_base + T2_O + h * HD, ad, bd, tmem_base + sb * BN + 32 * q, idesc_pv,
                                 (t > 0 || q > 0) ? 1u : 0u);
             }
             tc::mma_commit(&p_empty[h * P2ST + ps]);
+            tc::mma_commit(&s_free[sb]);
+            if (++sb == S2RING) sb = 0;
             if (t == ntiles - 1) tc::mma_commit(&o_full[h]);
           }
           tc::mma_commit(&v_empty[vs]);
@@ -667,7 +677,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int quad = warp & 3;
     const int r = quad * 32 + lane;      // row within the half == TMEM lane
     const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16);
-    const uint32_t s_cols = lane_base + h * BN + 64 * pr;
+    const uint32_t s_cols = lane_base + 64 * pr;  // + buffer * BN
     const uint32_t pbar = 1 + h * 4 + quad;  // named barrier of the two warps sharing these rows
     const float c = scale * kLog2e;
     float* rmax = red_max + h * 2 * BM;
@@ -679,12 +689,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t gt = 0;
     int it = 0;
     // maximum of this row over the set's 128 columns of the current S (both pairs)
+    uint32_t sbuf = 0;  // S buffer of the current step
     auto row_max = [&]() {
       float mt = -INFINITY;
 #pragma unroll 1
       for (int ch = 0; ch < 2; ++ch) {
         uint32_t s[32];
-        tc::tmem_ld_32x32b_x32(s_cols + 32 * ch, s);
+        tc::tmem_ld_32x32b_x32(s_cols + sbuf * BN + 32 * ch, s);
         tc::tmem_ld_wait(s);
 #pragma unroll
         for (int j = 0; j < 32; j += 2) mt = fmaxf(mt, fmaxf(__uint_as_float(s[j]), __uint_as_float(s[j + 1])));
@@ -699,7 +710,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int b = item / iblocks, ib = item % iblocks;
       float mlog = 0.f, l0 = 0.f, l1 = 0.f;
       for (int t = 0; t < ntiles; ++t, ++gt) {
-        tc::mbar_wait(&s_full[h], gt & 1);
+        const uint32_t g = 2 * gt + h;  // global step
+        sbuf = g % S2RING;
+        tc::mbar_wait(&s_full[sbuf], (g / S2RING) & 1);
         tc::tc_fence_after();
         if (t == 0) mlog = row_max();
         uint32_t pk[2][8], W[2];
@@ -709,7 +722,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int ch = 0; ch < 2; ++ch) {
             uint32_t s[32];
-            tc::tmem_ld_32x32b_x32(s_cols + 32 * ch, s);
+            tc::tmem_ld_32x32b_x32(s_cols + sbuf * BN + 32 * ch, s);
             tc::tmem_ld_wait(s);
             float a0, a1;
             if (variant & 8) {  // timing experiment: no prune / exp arithmetic
@@ -748,9 +761,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mlog = mnew;
           compute();
         }
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&s_empty[h]);  // S_h may be overwritten by the next tile
         add2(l0, l1, lt0, lt1, l0, l1);
         const uint32_t ps = gt % P2ST, pph = (gt / P2ST) & 1;
         tc::mbar_wait(&my_p_empty[ps], pph ^ 1);  // PV of this half's tile t - P2ST retired
@@ -765,7 +775,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t partner = __shfl_xor_sync(0xffffffffu, W[ch], 8);
           const uint32_t word =
               (lane & 8) ? ((partner >> 16) | (W[ch] & 0xFFFF0000u)) : ((W[ch] & 0xFFFFu) | (partner << 16));
-          tc::tmem_st_32x32b_x1(lane_base + T2_E + h * 8 + ps * 4 + qd, word);
+          tc::tmem_st_32x32b_x1(lane_base + sbuf * BN + 32 * qd, word);  // own columns, already read
         }
         tc::tmem_st_wait();
         tc::fence_proxy_async();  // P smem writes -> tensor core

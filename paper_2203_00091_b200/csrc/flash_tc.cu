@@ -474,29 +474,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 // ============================================================================ two-set kernel
-// n % 256 == 0: an item is 256 query rows (halves h = 0, 1) of one head.  The 16 softmax
-// warps split into two independent sets of 8, set h owning half h: warp (quad, pair) of a
-// set holds rows 32*quad.. and score columns [64*pair, +64) as two 32-column chunks.  The
-// sets share the K / V stream but not their latency chains (own P stages, barriers), so
-// one set's TMEM / shared-memory / barrier latencies overlap the other set's arithmetic on
-// every SM sub-partition (2 + 2 warps each).
+// n % 256 == 0: an item is 256 query rows (halves h = 0, 1) of one head, keys stream in
+// 64-key tiles.  The 16 softmax warps split into two independent sets of 8, set h owning
+// half h: warp (quad, pair) of a set holds rows 32*quad.. and score columns [32*pair, +32)
+// of every tile (= one K = 32 tcgen05.mma.sp).  The sets share the K / V stream but not
+// their latency chains (own S ring, P stages, barriers), so one set's TMEM / shared-memory
+// / barrier latencies overlap the other set's arithmetic on every SM sub-partition (2 + 2
+// warps each).
 //
-// S tiles of steps g = 2t + h go to a ring of three 128-column TMEM buffers; the metadata
-// of step g is written into its own S buffer (column 32q, after quarter q was read), so a
-// buffer is free again once PV_g retired.  A set's next S (step g + 2) lands in the buffer
-// of step g - 1 -- the other set's previous step -- and is computed while this set is
-// still busy with step g.
+// Each half has a ring of three 64-column S buffers.  The compressed P of a tile (16 kept
+// values per row and quarter = 8 columns of 16-bit pairs) and its metadata are written with
+// tcgen05.st back into the tile's own S buffer (quarter q: metadata at column 32q, P at
+// 32q + 16, both already read), and the sparse PV reads A straight from TMEM -- no shared
+// memory staging and no generic -> async proxy fence on the per-tile path.  A buffer is
+// free again once the tile's PV retired; S of tiles t+1, t+2 are computed while tile t is
+// pruned.
 namespace {
-constexpr int K2ST = 2, V2ST = 3, P2ST = 2;  // K ring, V ring, P stages per half
-constexpr int S2_Q = 0;                       // [2 stages][2 halves] x 16 KB
+constexpr int BN2 = 64;                         // keys per tile
+constexpr int K2ST = 4, V2ST = 4;               // K ring, V ring
+constexpr int K2_BYTES = BN2 * HD * 2;          // 8 KB
+constexpr int V2_BYTES = BN2 * HD * 2;          // 8 KB
+constexpr int S2_Q = 0;                          // [2 stages][2 halves] x 16 KB
 constexpr int S2_K = S2_Q + 4 * Q_BYTES;
-constexpr int S2_V = S2_K + K2ST * K_BYTES;
-constexpr int S2_P = S2_V + V2ST * V_BYTES;   // [2 halves][P2ST] x 16 KB
-constexpr int S2_RED = S2_P + 2 * P2ST * P_BYTES;  // red_max / red_sum: [2 halves][2 pairs][128] floats each
+constexpr int S2_V = S2_K + K2ST * K2_BYTES;
+constexpr int S2_RED = S2_V + V2ST * V2_BYTES;   // red_max / red_sum: [2 halves][2 pairs][128] floats each
 constexpr int S2_BAR = S2_RED + 2 * 2 * 2 * BM * 4;
-constexpr int S2_TOTAL = S2_BAR + 256 + 1024;
-constexpr int S2RING = 3;             // S buffers (TMEM), 128 columns each
-constexpr int T2_O = S2RING * BN;     // O_h at T2_O + 64 h
+constexpr int S2_TOTAL = S2_BAR + 512 + 1024;
+constexpr int S2RING = 3;                        // S buffers per half (TMEM), 64 columns each
+constexpr int T2_O = 2 * S2RING * BN2;           // O_h at T2_O + 64 h
+static_assert(T2_O + 2 * HD <= 512, "TMEM budget");
 static_assert(S2_TOTAL <= 227 * 1024, "shared memory budget");
 }  // namespace
 
@@ -508,27 +514,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + S2_BAR);
-  uint64_t* q_full = bars;               // [2]
-  uint64_t* q_empty = q_full + 2;        // [2]
-  uint64_t* k_full = q_empty + 2;        // [K2ST]
-  uint64_t* k_empty = k_full + K2ST;     // [K2ST]
-  uint64_t* v_full = k_empty + K2ST;     // [V2ST]
-  uint64_t* v_empty = v_full + V2ST;     // [V2ST]
-  uint64_t* s_full = v_empty + V2ST;     // [S2RING] S of a step computed
-  uint64_t* s_free = s_full + S2RING;    // [S2RING] PV of that step retired (buffer + metadata free)
-  uint64_t* p_full = s_free + S2RING;    // [2 halves][P2ST] (8 warps)
-  uint64_t* p_empty = p_full + 2 * P2ST; // [2 halves][P2ST]
-  uint64_t* o_full = p_empty + 2 * P2ST; // [2 halves]
-  uint64_t* o_empty = o_full + 2;        // [2 halves] (8 warps)
+  uint64_t* q_full = bars;                    // [2]
+  uint64_t* q_empty = q_full + 2;             // [2]
+  uint64_t* k_full = q_empty + 2;             // [K2ST]
+  uint64_t* k_empty = k_full + K2ST;          // [K2ST]
+  uint64_t* v_full = k_empty + K2ST;          // [V2ST]
+  uint64_t* v_empty = v_full + V2ST;          // [V2ST]
+  uint64_t* s_full = v_empty + V2ST;          // [2 halves][S2RING] S tile computed
+  uint64_t* s_free = s_full + 2 * S2RING;     // [2 halves][S2RING] PV of that tile retired
+  uint64_t* p_full = s_free + 2 * S2RING;     // [2 halves][S2RING] P + metadata written (8 warps)
+  uint64_t* o_full = p_full + 2 * S2RING;     // [2 halves]
+  uint64_t* o_empty = o_full + 2;             // [2 halves] (8 warps)
   uint32_t* tmem_slot = (uint32_t*)(o_empty + 2);
-  float* red_max = (float*)(smem + S2_RED);  // [h][pair][128]
+  float* red_max = (float*)(smem + S2_RED);   // [h][pair][128]
   float* red_sum = red_max + 2 * 2 * BM;
 
   const uint32_t warp = tc::warp_id();
   const uint32_t lane = threadIdx.x & 31;
   const int iblocks = n / (2 * BM);
   const int items = bh * iblocks;
-  const int ntiles = n / BN;
+  const int ntiles = n / BN2;
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tm_q);
@@ -540,13 +545,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc::mbar_init(&o_full[i], 1);
       tc::mbar_init(&o_empty[i], 8);
     }
-    for (int i = 0; i < S2RING; ++i) {
+    for (int i = 0; i < 2 * S2RING; ++i) {
       tc::mbar_init(&s_full[i], 1);
       tc::mbar_init(&s_free[i], 1);
-    }
-    for (int i = 0; i < 2 * P2ST; ++i) {
       tc::mbar_init(&p_full[i], 8);
-      tc::mbar_init(&p_empty[i], 1);
     }
     for (int i = 0; i < K2ST; ++i) {
       tc::mbar_init(&k_full[i], 1);
@@ -578,8 +580,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc::tma_load_3d(smem + S2_Q + (2 * qs + 1) * Q_BYTES, &tm_q, &q_full[qs], 0, ib * 2 * BM + BM, b);
         for (int t = 0; t < ntiles; ++t) {
           tc::mbar_wait_sleep(&k_empty[ks], kph ^ 1);
-          tc::mbar_arrive_expect_tx(&k_full[ks], K_BYTES);
-          tc::tma_load_5d(smem + S2_K + ks * K_BYTES, &tm_k, &k_full[ks], 0, 0, 0, t * (BN / 4), b);
+          tc::mbar_arrive_expect_tx(&k_full[ks], K2_BYTES);
+          tc::tma_load_5d(smem + S2_K + ks * K2_BYTES, &tm_k, &k_full[ks], 0, 0, 0, t * (BN2 / 4), b);
           if (++ks == K2ST) { ks = 0; kph ^= 1; }
         }
       }
@@ -593,17 +595,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int b = item / iblocks;
         for (int t = 0; t < ntiles; ++t) {
           tc::mbar_wait_sleep(&v_empty[vs], vph ^ 1);
-          tc::mbar_arrive_expect_tx(&v_full[vs], V_BYTES);
-          tc::tma_load_3d(smem + S2_V + vs * V_BYTES, &tm_v, &v_full[vs], 0, t * BN, b);
+          tc::mbar_arrive_expect_tx(&v_full[vs], V2_BYTES);
+          tc::tma_load_3d(smem + S2_V + vs * V2_BYTES, &tm_v, &v_full[vs], 0, t * BN2, b);
           if (++vs == V2ST) { vs = 0; vph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ S issuer: step g = 2t + h -> buffer g % 3
+    // ------------------------------------------------------------ S issuer: S = Q_h K_t^T into ring slot t % 3 of half h
     if (lane == 0) {
       constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
-      constexpr uint32_t idesc_s = tc::instr_desc(fmt, BM, BN, false, false, false);
+      constexpr uint32_t idesc_s = tc::instr_desc(fmt, BM, BN2, false, false, false);
       int ks = 0, it = 0, sb = 0;
       uint32_t kph = 0, sph = 0;
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
@@ -611,10 +613,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc::mbar_wait_sleep(&q_full[qs], (it >> 1) & 1);
         for (int t = 0; t < ntiles; ++t) {
           tc::mbar_wait_sleep(&k_full[ks], kph);
-          const uint32_t k_addr = tc::smem_u32(smem + S2_K + ks * K_BYTES);
+          const uint32_t k_addr = tc::smem_u32(smem + S2_K + ks * K2_BYTES);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            tc::mbar_wait_sleep(&s_free[sb], sph ^ 1);  // PV of step g - 3 retired
+            tc::mbar_wait_sleep(&s_free[h * S2RING + sb], sph ^ 1);  // tile t - 3 of half h retired
             tc::tc_fence_after();
             const uint32_t q_addr = tc::smem_u32(smem + S2_Q + (2 * qs + h) * Q_BYTES);
             if (!(variant & 32)) {
@@ -622,50 +624,47 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int kk = 0; kk < HD / 16; ++kk) {
                 const uint64_t ad = tc::smem_desc(q_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
                 const uint64_t bd = tc::smem_desc(k_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
-                tc::mma_f16_ss(tmem_base + sb * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+                tc::mma_f16_ss(tmem_base + (h * S2RING + sb) * BN2, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
               }
             }
-            tc::mma_commit(&s_full[sb]);
-            if (++sb == S2RING) { sb = 0; sph ^= 1; }
+            tc::mma_commit(&s_full[h * S2RING + sb]);
           }
           tc::mma_commit(&k_empty[ks]);
           if (++ks == K2ST) { ks = 0; kph ^= 1; }
+          if (++sb == S2RING) { sb = 0; sph ^= 1; }
         }
         tc::mma_commit(&q_empty[qs]);
       }
     }
   } else if (warp == 2) {
-    // ------------------------------------------------------------ PV issuer: O_h += P_h V_t
+    // ------------------------------------------------------------ PV issuer: O_h += P V_t (2 sparse K=32 MMAs per half)
     if (lane == 0) {
       constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
       constexpr uint32_t idesc_pv = tc::instr_desc(fmt, BM, HD, false, true, true);
       int vs = 0, it = 0, sb = 0;
-      uint32_t vph = 0, gt = 0;
+      uint32_t vph = 0, sph = 0;
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-        for (int t = 0; t < ntiles; ++t, ++gt) {
+        for (int t = 0; t < ntiles; ++t) {
           tc::mbar_wait_sleep(&v_full[vs], vph);
-          const uint32_t v_addr = tc::smem_u32(smem + S2_V + vs * V_BYTES);
-          const uint32_t ps = gt % P2ST, pph = (gt / P2ST) & 1;
+          const uint32_t v_addr = tc::smem_u32(smem + S2_V + vs * V2_BYTES);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             if (t == 0) tc::mbar_wait_sleep(&o_empty[h], (it & 1) ^ 1);
-            tc::mbar_wait_sleep(&p_full[h * P2ST + ps], pph);
+            tc::mbar_wait_sleep(&p_full[h * S2RING + sb], sph);
             tc::tc_fence_after();
-            const uint32_t p_addr = tc::smem_u32(smem + S2_P + (h * P2ST + ps) * P_BYTES);
+            const uint32_t s_col = tmem_base + (h * S2RING + sb) * BN2;
 #pragma unroll
-            for (int q = 0; q < ((variant & 16) ? 0 : 4); ++q) {
-              const uint64_t ad = tc::smem_desc(p_addr + q * 32, 16, 1024, tc::kSwizzle128B);
-              const uint64_t bd = tc::smem_desc(v_addr + q * 32 * 128, V_BYTES, 1024, tc::kSwizzle128B);
-              tc::mma_sp_f16_ss(tmem_base + T2_O + h * HD, ad, bd, tmem_base + sb * BN + 32 * q, idesc_pv,
+            for (int q = 0; q < ((variant & 16) ? 0 : 2); ++q) {
+              const uint64_t bd = tc::smem_desc(v_addr + q * 32 * 128, V2_BYTES, 1024, tc::kSwizzle128B);
+              tc::mma_sp_f16_ts(tmem_base + T2_O + h * HD, s_col + 32 * q + 16, bd, s_col + 32 * q, idesc_pv,
                                 (t > 0 || q > 0) ? 1u : 0u);
             }
-            tc::mma_commit(&p_empty[h * P2ST + ps]);
-            tc::mma_commit(&s_free[sb]);
-            if (++sb == S2RING) sb = 0;
+            tc::mma_commit(&s_free[h * S2RING + sb]);
             if (t == ntiles - 1) tc::mma_commit(&o_full[h]);
           }
           tc::mma_commit(&v_empty[vs]);
           if (++vs == V2ST) { vs = 0; vph ^= 1; }
+          if (++sb == S2RING) { sb = 0; sph ^= 1; }
         }
       }
     }
@@ -673,33 +672,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------ softmax / prune / epilogue sets
     const int sw = warp - 4;
     const int h = sw >> 3;               // half owned by this set
-    const int pr = (sw >> 2) & 1;        // column pair: quarters 2pr, 2pr + 1
+    const int pr = (sw >> 2) & 1;        // quarter of the 64-key tile = sparse MMA index
     const int quad = warp & 3;
     const int r = quad * 32 + lane;      // row within the half == TMEM lane
     const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16);
-    const uint32_t s_cols = lane_base + 64 * pr;  // + buffer * BN
+    const uint32_t s_col0 = lane_base + h * S2RING * BN2 + 32 * pr;  // + slot * BN2
     const uint32_t pbar = 1 + h * 4 + quad;  // named barrier of the two warps sharing these rows
     const float c = scale * kLog2e;
     float* rmax = red_max + h * 2 * BM;
     float* rsum = red_sum + h * 2 * BM;
-    const uint32_t p_row = tc::smem_u32(smem + S2_P + h * P2ST * P_BYTES) + r * 128;
-    const uint32_t sw7 = r & 7;
-    uint64_t* my_p_full = p_full + h * P2ST;
-    uint64_t* my_p_empty = p_empty + h * P2ST;
-    uint32_t gt = 0;
-    int it = 0;
-    // maximum of this row over the set's 128 columns of the current S (both pairs)
-    uint32_t sbuf = 0;  // S buffer of the current step
-    auto row_max = [&]() {
+    uint64_t* my_s_full = s_full + h * S2RING;
+    uint64_t* my_s_free = s_free + h * S2RING;
+    uint64_t* my_p_full = p_full + h * S2RING;
+    int sb = 0, it = 0;
+    uint32_t sph = 0;
+    // maximum of this row over the set's 64 columns of the current S
+    auto row_max = [&](const uint32_t (&s)[32]) {
       float mt = -INFINITY;
-#pragma unroll 1
-      for (int ch = 0; ch < 2; ++ch) {
-        uint32_t s[32];
-        tc::tmem_ld_32x32b_x32(s_cols + sbuf * BN + 32 * ch, s);
-        tc::tmem_ld_wait(s);
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) mt = fmaxf(mt, fmaxf(__uint_as_float(s[j]), __uint_as_float(s[j + 1])));
-      }
+      for (int j = 0; j < 32; j += 2) mt = fmaxf(mt, fmaxf(__uint_as_float(s[j]), __uint_as_float(s[j + 1])));
       rmax[pr * BM + r] = mt;
       tc::named_bar_sync(pbar, 64);
       const float m = fmaxf(rmax[r], rmax[BM + r]);
@@ -709,79 +700,63 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
       const int b = item / iblocks, ib = item % iblocks;
       float mlog = 0.f, l0 = 0.f, l1 = 0.f;
-      for (int t = 0; t < ntiles; ++t, ++gt) {
-        const uint32_t g = 2 * gt + h;  // global step
-        sbuf = g % S2RING;
-        tc::mbar_wait(&s_full[sbuf], (g / S2RING) & 1);
+      for (int t = 0; t < ntiles; ++t) {
+        tc::mbar_wait(&my_s_full[sb], sph);
         tc::tc_fence_after();
-        if (t == 0) mlog = row_max();
-        uint32_t pk[2][8], W[2];
-        float lt0 = 0.f, lt1 = 0.f;
-        auto compute = [&]() {
-          lt0 = lt1 = 0.f;
+        uint32_t s[32];
+        tc::tmem_ld_32x32b_x32(s_col0 + sb * BN2, s);
+        tc::tmem_ld_wait(s);
+        uint32_t pk[8], W;
+        float lt0, lt1;
+        if (t == 0) {
+          mlog = row_max(s);  // the shift starts at the row maximum of the item's first tile
+          prune_exp_tile<T>(s, c, mlog, two, pk, W, lt0, lt1);
+        } else {
+          if (variant & 8) {  // timing experiment: no prune / exp arithmetic
 #pragma unroll
-          for (int ch = 0; ch < 2; ++ch) {
-            uint32_t s[32];
-            tc::tmem_ld_32x32b_x32(s_cols + sbuf * BN + 32 * ch, s);
-            tc::tmem_ld_wait(s);
-            float a0, a1;
-            if (variant & 8) {  // timing experiment: no prune / exp arithmetic
-#pragma unroll
-              for (int j = 0; j < 8; ++j) pk[ch][j] = s[j] ^ s[j + 8];
-              W[ch] = 0x44444444u;
-              a0 = a1 = 0.f;
-            } else {
-              prune_exp_tile<T>(s, c, mlog, two, pk[ch], W[ch], a0, a1);
-            }
-            add2(lt0, lt1, a0, a1, lt0, lt1);
+            for (int j = 0; j < 8; ++j) pk[j] = s[j] ^ s[j + 8];
+            W = 0x44444444u;
+            lt0 = lt1 = 0.f;
+          } else {
+            prune_exp_tile<T>(s, c, mlog, two, pk, W, lt0, lt1);
           }
-        };
-        compute();
-        if (t > 0 && bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit))) {
-          // ---- slow path (both warps of the pair): raise the shift to the row maximum,
-          // rescale O_h and the sums once every PV into O_h so far (tile t-1) retired
-          const uint32_t pprev = (gt - 1) % P2ST, pphp = ((gt - 1) / P2ST) & 1;
-          tc::mbar_wait(&my_p_empty[pprev], pphp);
-          tc::tc_fence_after();
-          const float mnew = fmaxf(mlog, row_max());
-          const float f = fex2(mlog - mnew);
-          l0 *= f;
-          l1 *= f;
+          if (bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit))) {
+            // ---- slow path (both warps of the pair): raise the shift to the row maximum,
+            // rescale O_h and the sums once every PV into O_h so far (tile t-1) retired
+            const int sprev = sb == 0 ? S2RING - 1 : sb - 1;
+            tc::mbar_wait(&my_s_free[sprev], sb == 0 ? sph ^ 1 : sph);
+            tc::tc_fence_after();
+            const float mnew = fmaxf(mlog, row_max(s));
+            const float f = fex2(mlog - mnew);
+            l0 *= f;
+            l1 *= f;
 #pragma unroll 1
-          for (int hh = 0; hh < 2; ++hh) {
-            uint32_t o[16];
-            const uint32_t oaddr = lane_base + T2_O + h * HD + 32 * pr + 16 * hh;
-            tc::tmem_ld_32x32b_x16(oaddr, o);
-            tc::tmem_ld_wait(o);
+            for (int hh = 0; hh < 2; ++hh) {
+              uint32_t o[16];
+              const uint32_t oaddr = lane_base + T2_O + h * HD + 32 * pr + 16 * hh;
+              tc::tmem_ld_32x32b_x16(oaddr, o);
+              tc::tmem_ld_wait(o);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * f);
-            tc::tmem_st_32x32b_x16(oaddr, o);
+              for (int j = 0; j < 16; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * f);
+              tc::tmem_st_32x32b_x16(oaddr, o);
+            }
+            tc::tmem_st_wait();
+            mlog = mnew;
+            prune_exp_tile<T>(s, c, mlog, two, pk, W, lt0, lt1);
           }
-          tc::tmem_st_wait();
-          mlog = mnew;
-          compute();
         }
         add2(l0, l1, lt0, lt1, l0, l1);
-        const uint32_t ps = gt % P2ST, pph = (gt / P2ST) & 1;
-        tc::mbar_wait(&my_p_empty[ps], pph ^ 1);  // PV of this half's tile t - P2ST retired
-        tc::tc_fence_after();
-        const uint32_t prow = p_row + ps * P_BYTES;
-#pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
-          const int qd = 2 * pr + ch;  // quarter = 32-column block = one sparse MMA
-          sts128(prow + (((2 * qd) ^ sw7) << 4), pk[ch][0], pk[ch][1], pk[ch][2], pk[ch][3]);
-          sts128(prow + (((2 * qd + 1) ^ sw7) << 4), pk[ch][4], pk[ch][5], pk[ch][6], pk[ch][7]);
-          // metadata word of TMEM lane r: rows r and r^8 trade 16-bit halves (include/dfss.h)
-          const uint32_t partner = __shfl_xor_sync(0xffffffffu, W[ch], 8);
-          const uint32_t word =
-              (lane & 8) ? ((partner >> 16) | (W[ch] & 0xFFFF0000u)) : ((W[ch] & 0xFFFFu) | (partner << 16));
-          tc::tmem_st_32x32b_x1(lane_base + sbuf * BN + 32 * qd, word);  // own columns, already read
-        }
+        // P (8 columns of 16-bit pairs) and the metadata word of TMEM lane r into the tile's own,
+        // already read S columns; rows r and r^8 trade metadata halves (include/dfss.h)
+        const uint32_t partner = __shfl_xor_sync(0xffffffffu, W, 8);
+        const uint32_t word = (lane & 8) ? ((partner >> 16) | (W & 0xFFFF0000u)) : ((W & 0xFFFFu) | (partner << 16));
+        tc::tmem_st_32x32b_x8(s_col0 + sb * BN2 + 16, pk);
+        tc::tmem_st_32x32b_x1(s_col0 + sb * BN2, word);
         tc::tmem_st_wait();
-        tc::fence_proxy_async();  // P smem writes -> tensor core
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&my_p_full[ps]);
+        if (lane == 0) tc::mbar_arrive(&my_p_full[sb]);
+        if (++sb == S2RING) { sb = 0; sph ^= 1; }
       }
       // ---- epilogue: O_h / row sum; this warp writes columns [32 pr, +32) of its rows
       rsum[pr * BM + r] = l0 + l1;
@@ -829,16 +804,18 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
   const uint64_t row = HD * 2;
   const uint64_t kdims[5] = {(uint64_t)HD, 2, 2, (uint64_t)n / 4, (uint64_t)bh};
   const uint64_t kstr[4] = {2 * row, row, 4 * row, (uint64_t)n * row};
-  const uint32_t kbox[5] = {(uint32_t)HD, 2, 2, BN / 4, 1};
-  if (!encode_tmap_3d(&tq, dt, 2, (void*)q, HD, n, bh, HD, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !encode_tmap(&tk, dt, 5, (void*)k, kdims, kstr, kbox, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !encode_tmap_3d(&tv, dt, 2, (void*)v, HD, n, bh, HD, BN, CU_TENSOR_MAP_SWIZZLE_128B))
-    return cudaErrorInvalidValue;
-  // n % 256 == 0: the two-set kernel (256-row items, independent softmax sets per half);
-  // otherwise 128-row items with all 16 softmax warps on one half.  DFSS_FLASH_KERNEL=1
-  // forces the one-set kernel (experiments).
+  uint32_t kbox[5] = {(uint32_t)HD, 2, 2, BN / 4, 1};
+  // n % 256 == 0: the two-set kernel (256-row items, 64-key tiles, independent softmax sets
+  // per half); otherwise 128-row items and 128-key tiles with all 16 softmax warps on one
+  // half.  DFSS_FLASH_KERNEL=1 forces the one-set kernel (experiments).
   static const int force1 = getenv("DFSS_FLASH_KERNEL") ? atoi(getenv("DFSS_FLASH_KERNEL")) == 1 : 0;
   const bool two_set = n % (2 * BM) == 0 && !force1;
+  const uint32_t kvbox = two_set ? BN2 : BN;
+  kbox[3] = kvbox / 4;
+  if (!encode_tmap_3d(&tq, dt, 2, (void*)q, HD, n, bh, HD, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !encode_tmap(&tk, dt, 5, (void*)k, kdims, kstr, kbox, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !encode_tmap_3d(&tv, dt, 2, (void*)v, HD, n, bh, HD, kvbox, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
   const int halves = two_set ? 2 : 1;
   auto kern = two_set ? dfss_flash2_kernel<T> : dfss_flash_kernel<T, 1>;
   const int smem_total = two_set ? S2_TOTAL : SMEM_TOTAL;

@@ -40,8 +40,9 @@
 // TMEM (512 columns): S buffers at 0 / 128 (step parity), O_h at 256 + 64h, metadata of
 // P stage p at 384 + 4p + quarter.
 //
-// Warp roles (one CTA per SM, persistent over items): warp 0 TMA Q/K, warp 1 S issuer,
-// warp 2 TMEM allocator + PV issuer, warp 3 TMA V, warps 4-19 softmax / prune / epilogue.
+// Warp roles (one CTA per SM, persistent over items): warps 0-15 softmax / prune / epilogue,
+// warp 16 TMA Q/K, warp 17 S issuer, warp 18 TMEM allocator + PV issuer, warp 19 TMA V.
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <type_traits>
@@ -60,6 +61,11 @@ constexpr int VST = 3;    // V ring
 constexpr int PST = 2;    // P stages (smem) / metadata stages (TMEM)
 constexpr int SM_WARPS = 16;
 constexpr int NUM_THREADS = (4 + SM_WARPS) * 32;
+// Role warps sit at the highest warp ids (16..19): the sub-partition scheduler prefers high
+// warp ids, so a single-thread TMA producer / MMA issuer is served as soon as it is ready
+// instead of waiting for a stall of the four arithmetic warps sharing its sub-partition.
+constexpr uint32_t W_QK = SM_WARPS, W_S = SM_WARPS + 1, W_PV = SM_WARPS + 2, W_V = SM_WARPS + 3;
+constexpr uint32_t W_PV1 = W_V;  // two-set kernel: PV issuer of half 1 (V is loaded by W_QK there)
 constexpr int Q_BYTES = BM * HD * 2;        // 16 KB per half
 constexpr int K_BYTES = BN * HD * 2;        // 16 KB
 constexpr int V_BYTES = BN * HD * 2;        // 16 KB
@@ -124,6 +130,14 @@ __device__ __forceinline__ bool bar_any(uint32_t id, uint32_t count, bool pred) 
       : "r"((uint32_t)pred), "r"(id), "r"(count)
       : "memory");
   return r != 0;
+}
+
+// role-warp wait: sleeping try_wait, or spinning with variant bit 10 (experiment)
+__device__ __forceinline__ void wait_role(int variant, uint64_t* bar, uint32_t parity) {
+  if (variant & 1024)
+    tc::mbar_wait(bar, parity);
+  else
+    tc::mbar_wait_sleep(bar, parity);
 }
 
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -199,7 +213,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int items = bh * iblocks;
   const int ntiles = n / BN;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == W_QK && lane == 0) {
     tc::prefetch_tmap(&tm_q);
     tc::prefetch_tmap(&tm_k);
     tc::prefetch_tmap(&tm_v);
@@ -225,13 +239,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc::mbar_init(o_empty, SM_WARPS);
     tc::fence_barrier_init();
   }
-  if (warp == 2) tc::tmem_alloc<512>(tmem_slot);
+  if (warp == W_PV) tc::tmem_alloc<512>(tmem_slot);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == W_QK) {
     // ------------------------------------------------------------ TMA producer: Q (all halves) and K (keys permuted)
     if (lane == 0) {
       int ks = 0, it = 0;
@@ -252,7 +266,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else if (warp == 3) {
+  } else if (warp == W_V) {
     // ------------------------------------------------------------ TMA producer: V
     if (lane == 0) {
       int vs = 0;
@@ -267,7 +281,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == W_S) {
     // ------------------------------------------------------------ S issuer: step g = (t, h) -> S buffer g & 1
     if (lane == 0) {
       constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
@@ -302,7 +316,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc::mma_commit(&q_empty[qs]);
       }
     }
-  } else if (warp == 2) {
+  } else if (warp == W_PV) {
     // ------------------------------------------------------------ PV issuer: O_h += P V_t (4 sparse K=32 MMAs)
     if (lane == 0) {
       constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
@@ -341,7 +355,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else {
     // ------------------------------------------------------------ softmax / prune / epilogue warps
     const int quad = warp & 3;
-    const int quarter = (warp - 4) >> 2;
+    const int quarter = warp >> 2;
     const int r = quad * 32 + lane;  // row within the half == TMEM lane
     const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16);
     const uint32_t qbar = 1 + quad;  // named barrier of the four warps sharing these rows
@@ -467,44 +481,52 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == W_PV) {
     tc::tc_fence_after();
     tc::tmem_dealloc<512>(tmem_base);
   }
 }
 
 // ============================================================================ two-set kernel
-// n % 256 == 0: an item is 256 query rows (halves h = 0, 1) of one head, keys stream in
-// 64-key tiles.  The 16 softmax warps split into two independent sets of 8, set h owning
-// half h: warp (quad, pair) of a set holds rows 32*quad.. and score columns [32*pair, +32)
-// of every tile (= one K = 32 tcgen05.mma.sp).  The sets share the K / V stream but not
-// their latency chains (own S ring, P stages, barriers), so one set's TMEM / shared-memory
-// / barrier latencies overlap the other set's arithmetic on every SM sub-partition (2 + 2
-// warps each).
+// n % 256 == 0: an item is 256 query rows (halves h = 0, 1) of one head.  The 16 softmax
+// warps split into two independent sets of 8, set h owning half h: warp (quad, pair) of a
+// set holds rows 32*quad.. and score columns [64*pair, +64) of every 128-key tile as two
+// 32-column chunks (= two K = 32 tcgen05.mma.sp).  The sets share the K / V stream but
+// not their latency chains, so one set's TMEM / barrier latencies overlap the other set's
+// arithmetic on every SM sub-partition (2 + 2 warps each).
 //
-// Each half has a ring of three 64-column S buffers.  The compressed P of a tile (16 kept
-// values per row and quarter = 8 columns of 16-bit pairs) and its metadata are written with
-// tcgen05.st back into the tile's own S buffer (quarter q: metadata at column 32q, P at
-// 32q + 16, both already read), and the sparse PV reads A straight from TMEM -- no shared
-// memory staging and no generic -> async proxy fence on the per-tile path.  A buffer is
-// free again once the tile's PV retired; S of tiles t+1, t+2 are computed while tile t is
-// pruned.
+// Steps g = 2t + h use a ring of three 128-column TMEM S buffers.  The compressed P of a
+// step (16 kept values per row and quarter = 8 columns of 16-bit pairs) and its metadata
+// are written with tcgen05.st back into the step's own S buffer (quarter q: metadata at
+// column 32q, P at 32q + 16, both already read) and the sparse PV reads A straight from
+// TMEM: no shared-memory staging and no generic -> async proxy fence per tile.  A buffer
+// is free again once its PV retired; a set's next S (step g + 2) lands in the buffer of
+// step g - 1 and is computed while the set is still pruning step g.
+//
+// Tensor cost per 128 x 128 step (measured, tools/mma_probe.cu): 4 x 64 clk for S (SS,
+// N = 128) + 4 x 46 clk for the sparse PV (A in TMEM) -- an M = 128 MMA costs >= ~46 clk
+// whatever its N, so 128-key tiles, not 64, keep the tensor pipe under the epilogue.
 namespace {
-constexpr int BN2 = 64;                         // keys per tile
-constexpr int K2ST = 4, V2ST = 4;               // K ring, V ring
-constexpr int K2_BYTES = BN2 * HD * 2;          // 8 KB
-constexpr int V2_BYTES = BN2 * HD * 2;          // 8 KB
-constexpr int S2_Q = 0;                          // [2 stages][2 halves] x 16 KB
+constexpr int K2ST = 4, V2ST = 4;             // K ring, V ring (128-key tiles, 16 KB each)
+constexpr int S2_Q = 0;                        // [2 stages][2 halves] x 16 KB
 constexpr int S2_K = S2_Q + 4 * Q_BYTES;
-constexpr int S2_V = S2_K + K2ST * K2_BYTES;
-constexpr int S2_RED = S2_V + V2ST * V2_BYTES;   // red_max / red_sum: [2 halves][2 pairs][128] floats each
+constexpr int S2_V = S2_K + K2ST * K_BYTES;
+constexpr int S2_RED = S2_V + V2ST * V_BYTES;  // red_max / red_sum: [2 halves][2 pairs][128] floats each
 constexpr int S2_BAR = S2_RED + 2 * 2 * 2 * BM * 4;
 constexpr int S2_TOTAL = S2_BAR + 512 + 1024;
-constexpr int S2RING = 3;                        // S buffers per half (TMEM), 64 columns each
-constexpr int T2_O = 2 * S2RING * BN2;           // O_h at T2_O + 64 h
+constexpr int S2RING = 3;                      // S buffers (TMEM), 128 columns each
+constexpr int T2_O = S2RING * BN;              // O_h at T2_O + 64 h
 static_assert(T2_O + 2 * HD <= 512, "TMEM budget");
 static_assert(S2_TOTAL <= 227 * 1024, "shared memory budget");
 }  // namespace
+
+// bring-up timeline (DFSS_FLASH_TRACE=<file>): clock64 at pipeline events of CTA 0, first 2 items
+__device__ unsigned long long* g_flash_trace = nullptr;
+#define FTRACE(slot, it_, t_, h_)                                                                  \
+  do {                                                                                             \
+    if (trace && (it_) < 2 && (t_) < 64)                                                           \
+      trace[((((slot) * 2 + (it_)) * 64 + (t_)) * 2 + (h_))] = clock64();                          \
+  } while (0)
 
 template <typename T>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -514,28 +536,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + S2_BAR);
-  uint64_t* q_full = bars;                    // [2]
-  uint64_t* q_empty = q_full + 2;             // [2]
-  uint64_t* k_full = q_empty + 2;             // [K2ST]
-  uint64_t* k_empty = k_full + K2ST;          // [K2ST]
-  uint64_t* v_full = k_empty + K2ST;          // [V2ST]
-  uint64_t* v_empty = v_full + V2ST;          // [V2ST]
-  uint64_t* s_full = v_empty + V2ST;          // [2 halves][S2RING] S tile computed
-  uint64_t* s_free = s_full + 2 * S2RING;     // [2 halves][S2RING] PV of that tile retired
-  uint64_t* p_full = s_free + 2 * S2RING;     // [2 halves][S2RING] P + metadata written (8 warps)
-  uint64_t* o_full = p_full + 2 * S2RING;     // [2 halves]
-  uint64_t* o_empty = o_full + 2;             // [2 halves] (8 warps)
-  uint32_t* tmem_slot = (uint32_t*)(o_empty + 2);
-  float* red_max = (float*)(smem + S2_RED);   // [h][pair][128]
+  uint64_t* q_full = bars;                // [2]
+  uint64_t* q_empty = q_full + 2;         // [2]
+  uint64_t* k_full = q_empty + 2;         // [K2ST]
+  uint64_t* k_empty = k_full + K2ST;      // [K2ST]
+  uint64_t* v_full = k_empty + K2ST;      // [V2ST]
+  uint64_t* v_empty = v_full + V2ST;      // [V2ST]
+  uint64_t* s_full = v_empty + V2ST;      // [S2RING] S of a step computed
+  uint64_t* s_free = s_full + S2RING;     // [S2RING] PV of that step retired (buffer free)
+  // [2 halves][S2RING] P + metadata of a step written (8 warps).  Per half, not per slot only:
+  // each PV issuer may run a step ahead of the other set, and a shared slot barrier would
+  // then satisfy its wait with the other set's previous phase (parity aliasing).
+  uint64_t* p_full = s_free + S2RING;
+  uint64_t* o_full = p_full + 2 * S2RING; // [2 halves]
+  uint64_t* o_empty = o_full + 2;         // [2 halves] (8 warps)
+  uint64_t* pv_done = o_empty + 2;        // [2 halves] every PV of this half so far retired
+  uint32_t* tmem_slot = (uint32_t*)(pv_done + 2);
+  float* red_max = (float*)(smem + S2_RED);  // [h][pair][128]
   float* red_sum = red_max + 2 * 2 * BM;
 
   const uint32_t warp = tc::warp_id();
   const uint32_t lane = threadIdx.x & 31;
+  unsigned long long* trace = blockIdx.x == 0 ? g_flash_trace : nullptr;
   const int iblocks = n / (2 * BM);
   const int items = bh * iblocks;
-  const int ntiles = n / BN2;
+  const int ntiles = n / BN;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == W_QK && lane == 0) {
     tc::prefetch_tmap(&tm_q);
     tc::prefetch_tmap(&tm_k);
     tc::prefetch_tmap(&tm_v);
@@ -544,79 +571,74 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc::mbar_init(&q_empty[i], 1);
       tc::mbar_init(&o_full[i], 1);
       tc::mbar_init(&o_empty[i], 8);
+      tc::mbar_init(&pv_done[i], 1);
     }
-    for (int i = 0; i < 2 * S2RING; ++i) {
+    for (int i = 0; i < S2RING; ++i) {
       tc::mbar_init(&s_full[i], 1);
       tc::mbar_init(&s_free[i], 1);
-      tc::mbar_init(&p_full[i], 8);
     }
+    for (int i = 0; i < 2 * S2RING; ++i) tc::mbar_init(&p_full[i], 8);
     for (int i = 0; i < K2ST; ++i) {
       tc::mbar_init(&k_full[i], 1);
       tc::mbar_init(&k_empty[i], 1);
     }
     for (int i = 0; i < V2ST; ++i) {
       tc::mbar_init(&v_full[i], 1);
-      tc::mbar_init(&v_empty[i], 1);
+      tc::mbar_init(&v_empty[i], 2);  // released by both PV issuers
     }
     tc::fence_barrier_init();
   }
-  if (warp == 2) tc::tmem_alloc<512>(tmem_slot);
+  if (warp == W_PV) tc::tmem_alloc<512>(tmem_slot);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer: Q (both halves) and K (keys permuted)
+  if (warp == W_QK) {
+    // ------------------------------------------------------------ TMA producer: Q (both halves), K (keys permuted), V
     if (lane == 0) {
-      int ks = 0, it = 0;
-      uint32_t kph = 0;
+      int ks = 0, vs = 0, it = 0;
+      uint32_t kph = 0, vph = 0;
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
         const int b = item / iblocks, ib = item % iblocks;
         const int qs = it & 1;
-        tc::mbar_wait_sleep(&q_empty[qs], ((it >> 1) & 1) ^ 1);
+        wait_role(variant, &q_empty[qs], ((it >> 1) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&q_full[qs], 2 * Q_BYTES);
         tc::tma_load_3d(smem + S2_Q + (2 * qs) * Q_BYTES, &tm_q, &q_full[qs], 0, ib * 2 * BM, b);
         tc::tma_load_3d(smem + S2_Q + (2 * qs + 1) * Q_BYTES, &tm_q, &q_full[qs], 0, ib * 2 * BM + BM, b);
         for (int t = 0; t < ntiles; ++t) {
-          tc::mbar_wait_sleep(&k_empty[ks], kph ^ 1);
-          tc::mbar_arrive_expect_tx(&k_full[ks], K2_BYTES);
-          tc::tma_load_5d(smem + S2_K + ks * K2_BYTES, &tm_k, &k_full[ks], 0, 0, 0, t * (BN2 / 4), b);
+          wait_role(variant, &k_empty[ks], kph ^ 1);
+          tc::mbar_arrive_expect_tx(&k_full[ks], K_BYTES);
+          tc::tma_load_5d(smem + S2_K + ks * K_BYTES, &tm_k, &k_full[ks], 0, 0, 0, t * (BN / 4), b);
+          FTRACE(8, it, t, 0);
           if (++ks == K2ST) { ks = 0; kph ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 3) {
-    // ------------------------------------------------------------ TMA producer: V
-    if (lane == 0) {
-      int vs = 0;
-      uint32_t vph = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x) {
-        const int b = item / iblocks;
-        for (int t = 0; t < ntiles; ++t) {
-          tc::mbar_wait_sleep(&v_empty[vs], vph ^ 1);
-          tc::mbar_arrive_expect_tx(&v_full[vs], V2_BYTES);
-          tc::tma_load_3d(smem + S2_V + vs * V2_BYTES, &tm_v, &v_full[vs], 0, t * BN2, b);
+          wait_role(variant, &v_empty[vs], vph ^ 1);
+          tc::mbar_arrive_expect_tx(&v_full[vs], V_BYTES);
+          tc::tma_load_3d(smem + S2_V + vs * V_BYTES, &tm_v, &v_full[vs], 0, t * BN, b);
+          FTRACE(9, it, t, 0);
           if (++vs == V2ST) { vs = 0; vph ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ S issuer: S = Q_h K_t^T into ring slot t % 3 of half h
-    if (lane == 0) {
+  } else if (warp == W_S) {
+    // ------------------------------------------------------------ S issuer: step g = 2t + h -> buffer g % 3
+    {  // whole warp, converged; elected lanes issue
       constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
-      constexpr uint32_t idesc_s = tc::instr_desc(fmt, BM, BN2, false, false, false);
+      constexpr uint32_t idesc_s = tc::instr_desc(fmt, BM, BN, false, false, false);
       int ks = 0, it = 0, sb = 0;
       uint32_t kph = 0, sph = 0;
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
         const int qs = it & 1;
-        tc::mbar_wait_sleep(&q_full[qs], (it >> 1) & 1);
+        wait_role(variant, &q_full[qs], (it >> 1) & 1);
         for (int t = 0; t < ntiles; ++t) {
-          tc::mbar_wait_sleep(&k_full[ks], kph);
-          const uint32_t k_addr = tc::smem_u32(smem + S2_K + ks * K2_BYTES);
+          wait_role(variant, &k_full[ks], kph);
+          if (lane == 0) FTRACE(10, it, t, 0);
+          const uint32_t k_addr = tc::smem_u32(smem + S2_K + ks * K_BYTES);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            tc::mbar_wait_sleep(&s_free[h * S2RING + sb], sph ^ 1);  // tile t - 3 of half h retired
+            if (lane == 0) FTRACE(3, it, t, h);
+            wait_role(variant, &s_free[sb], sph ^ 1);  // PV of step g - 3 retired
+            if (lane == 0) FTRACE(4, it, t, h);
             tc::tc_fence_after();
             const uint32_t q_addr = tc::smem_u32(smem + S2_Q + (2 * qs + h) * Q_BYTES);
             if (!(variant & 32)) {
@@ -624,73 +646,78 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int kk = 0; kk < HD / 16; ++kk) {
                 const uint64_t ad = tc::smem_desc(q_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
                 const uint64_t bd = tc::smem_desc(k_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
-                tc::mma_f16_ss(tmem_base + (h * S2RING + sb) * BN2, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+                tc::mma_f16_ss_w(tmem_base + sb * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
               }
             }
-            tc::mma_commit(&s_full[h * S2RING + sb]);
+            tc::mma_commit_w(&s_full[sb]);
+            if (lane == 0) FTRACE(5, it, t, h);
+            if (++sb == S2RING) { sb = 0; sph ^= 1; }
           }
-          tc::mma_commit(&k_empty[ks]);
+          tc::mma_commit_w(&k_empty[ks]);
           if (++ks == K2ST) { ks = 0; kph ^= 1; }
-          if (++sb == S2RING) { sb = 0; sph ^= 1; }
         }
-        tc::mma_commit(&q_empty[qs]);
+        tc::mma_commit_w(&q_empty[qs]);
       }
     }
-  } else if (warp == 2) {
-    // ------------------------------------------------------------ PV issuer: O_h += P V_t (2 sparse K=32 MMAs per half)
-    if (lane == 0) {
+  } else if (warp == W_PV || warp == W_PV1) {
+    // ------------------------------------------------------------ PV issuer of half h: O_h += P V_t (4 sparse K=32
+    // MMAs, A in TMEM); one issuer per half, so a lagging set never blocks the other's PV
+    {  // whole warp, converged; elected lanes issue
+      const int h = warp == W_PV ? 0 : 1;
       constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
       constexpr uint32_t idesc_pv = tc::instr_desc(fmt, BM, HD, false, true, true);
-      int vs = 0, it = 0, sb = 0;
-      uint32_t vph = 0, sph = 0;
+      int vs = 0, it = 0;
+      uint32_t vph = 0, gt = 0;
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-        for (int t = 0; t < ntiles; ++t) {
-          tc::mbar_wait_sleep(&v_full[vs], vph);
-          const uint32_t v_addr = tc::smem_u32(smem + S2_V + vs * V2_BYTES);
+        wait_role(variant, &o_empty[h], (it & 1) ^ 1);
+        for (int t = 0; t < ntiles; ++t, ++gt) {
+          const uint32_t g = 2 * gt + h, slot = g % S2RING;
+          wait_role(variant, &v_full[vs], vph);
+          wait_role(variant, &p_full[h * S2RING + slot], (gt / S2RING) & 1);  // k-th use by this half = gt / 3
+          if (lane == 0) FTRACE(6, it, t, h);
+          tc::tc_fence_after();
+          const uint32_t v_addr = tc::smem_u32(smem + S2_V + vs * V_BYTES);
+          const uint32_t s_col = tmem_base + slot * BN;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            if (t == 0) tc::mbar_wait_sleep(&o_empty[h], (it & 1) ^ 1);
-            tc::mbar_wait_sleep(&p_full[h * S2RING + sb], sph);
-            tc::tc_fence_after();
-            const uint32_t s_col = tmem_base + (h * S2RING + sb) * BN2;
-#pragma unroll
-            for (int q = 0; q < ((variant & 16) ? 0 : 2); ++q) {
-              const uint64_t bd = tc::smem_desc(v_addr + q * 32 * 128, V2_BYTES, 1024, tc::kSwizzle128B);
-              tc::mma_sp_f16_ts(tmem_base + T2_O + h * HD, s_col + 32 * q + 16, bd, s_col + 32 * q, idesc_pv,
+          for (int q = 0; q < ((variant & 16) ? 0 : 4); ++q) {
+            const uint64_t bd = tc::smem_desc(v_addr + q * 32 * 128, V_BYTES, 1024, tc::kSwizzle128B);
+            tc::mma_sp_f16_ts_w(tmem_base + T2_O + h * HD, s_col + 32 * q + 16, bd, s_col + 32 * q, idesc_pv,
                                 (t > 0 || q > 0) ? 1u : 0u);
-            }
-            tc::mma_commit(&s_free[h * S2RING + sb]);
-            if (t == ntiles - 1) tc::mma_commit(&o_full[h]);
           }
-          tc::mma_commit(&v_empty[vs]);
+          tc::mma_commit_w(&s_free[slot]);
+          tc::mma_commit_w(&v_empty[vs]);
+          tc::mma_commit_w(&pv_done[h]);
+          if (lane == 0) FTRACE(7, it, t, h);
           if (++vs == V2ST) { vs = 0; vph ^= 1; }
-          if (++sb == S2RING) { sb = 0; sph ^= 1; }
         }
+        tc::mma_commit_w(&o_full[h]);
       }
     }
-  } else {
+  } else if (warp < SM_WARPS) {
     // ------------------------------------------------------------ softmax / prune / epilogue sets
-    const int sw = warp - 4;
-    const int h = sw >> 3;               // half owned by this set
-    const int pr = (sw >> 2) & 1;        // quarter of the 64-key tile = sparse MMA index
+    const int h = warp >> 3;              // half owned by this set
+    const int pr = (warp >> 2) & 1;       // column pair: quarters 2pr, 2pr + 1
     const int quad = warp & 3;
-    const int r = quad * 32 + lane;      // row within the half == TMEM lane
+    const int r = quad * 32 + lane;       // row within the half == TMEM lane
     const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16);
-    const uint32_t s_col0 = lane_base + h * S2RING * BN2 + 32 * pr;  // + slot * BN2
     const uint32_t pbar = 1 + h * 4 + quad;  // named barrier of the two warps sharing these rows
     const float c = scale * kLog2e;
     float* rmax = red_max + h * 2 * BM;
     float* rsum = red_sum + h * 2 * BM;
-    uint64_t* my_s_full = s_full + h * S2RING;
-    uint64_t* my_s_free = s_free + h * S2RING;
-    uint64_t* my_p_full = p_full + h * S2RING;
-    int sb = 0, it = 0;
-    uint32_t sph = 0;
-    // maximum of this row over the set's 64 columns of the current S
-    auto row_max = [&](const uint32_t (&s)[32]) {
+    const bool tw = quad == 0 && pr == 0 && lane == 0;
+    uint32_t gt = 0, scol = 0;  // scol: this warp's first S column of the current step's buffer
+    int it = 0;
+    // maximum of this row over the set's 128 columns of the current S (both warps of the pair)
+    auto row_max = [&]() {
       float mt = -INFINITY;
+#pragma unroll 1
+      for (int ch = 0; ch < 2; ++ch) {
+        uint32_t s[32];
+        tc::tmem_ld_32x32b_x32(scol + 32 * ch, s);
+        tc::tmem_ld_wait(s);
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) mt = fmaxf(mt, fmaxf(__uint_as_float(s[j]), __uint_as_float(s[j + 1])));
+        for (int j = 0; j < 32; j += 2) mt = fmaxf(mt, fmaxf(__uint_as_float(s[j]), __uint_as_float(s[j + 1])));
+      }
       rmax[pr * BM + r] = mt;
       tc::named_bar_sync(pbar, 64);
       const float m = fmaxf(rmax[r], rmax[BM + r]);
@@ -700,63 +727,79 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
       const int b = item / iblocks, ib = item % iblocks;
       float mlog = 0.f, l0 = 0.f, l1 = 0.f;
-      for (int t = 0; t < ntiles; ++t) {
-        tc::mbar_wait(&my_s_full[sb], sph);
+      for (int t = 0; t < ntiles; ++t, ++gt) {
+        const uint32_t g = 2 * gt + h;  // global step
+        const uint32_t slot = g % S2RING;
+        scol = lane_base + slot * BN + 64 * pr;
+        tc::mbar_wait(&s_full[slot], (g / S2RING) & 1);
+        if (tw) FTRACE(0, it, t, h);
         tc::tc_fence_after();
-        uint32_t s[32];
-        tc::tmem_ld_32x32b_x32(s_col0 + sb * BN2, s);
-        tc::tmem_ld_wait(s);
-        uint32_t pk[8], W;
-        float lt0, lt1;
-        if (t == 0) {
-          mlog = row_max(s);  // the shift starts at the row maximum of the item's first tile
-          prune_exp_tile<T>(s, c, mlog, two, pk, W, lt0, lt1);
-        } else {
-          if (variant & 8) {  // timing experiment: no prune / exp arithmetic
+        if (t == 0) mlog = row_max();  // the shift starts at the row maximum of the item's first tile
+        uint32_t pk[2][8], W[2];
+        float lt0 = 0.f, lt1 = 0.f;
+        auto compute = [&]() {
+          lt0 = lt1 = 0.f;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) pk[j] = s[j] ^ s[j + 8];
-            W = 0x44444444u;
-            lt0 = lt1 = 0.f;
-          } else {
-            prune_exp_tile<T>(s, c, mlog, two, pk, W, lt0, lt1);
-          }
-          if (bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit))) {
-            // ---- slow path (both warps of the pair): raise the shift to the row maximum,
-            // rescale O_h and the sums once every PV into O_h so far (tile t-1) retired
-            const int sprev = sb == 0 ? S2RING - 1 : sb - 1;
-            tc::mbar_wait(&my_s_free[sprev], sb == 0 ? sph ^ 1 : sph);
-            tc::tc_fence_after();
-            const float mnew = fmaxf(mlog, row_max(s));
-            const float f = fex2(mlog - mnew);
-            l0 *= f;
-            l1 *= f;
-#pragma unroll 1
-            for (int hh = 0; hh < 2; ++hh) {
-              uint32_t o[16];
-              const uint32_t oaddr = lane_base + T2_O + h * HD + 32 * pr + 16 * hh;
-              tc::tmem_ld_32x32b_x16(oaddr, o);
-              tc::tmem_ld_wait(o);
+          for (int ch = 0; ch < 2; ++ch) {
+            uint32_t s[32];
+            tc::tmem_ld_32x32b_x32(scol + 32 * ch, s);
+            tc::tmem_ld_wait(s);
+            float a0, a1;
+            if (variant & 8) {  // timing experiment: no prune / exp arithmetic
 #pragma unroll
-              for (int j = 0; j < 16; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * f);
-              tc::tmem_st_32x32b_x16(oaddr, o);
+              for (int j = 0; j < 8; ++j) pk[ch][j] = s[j] ^ s[j + 8];
+              W[ch] = 0x44444444u;
+              a0 = a1 = 0.f;
+            } else {
+              prune_exp_tile<T>(s, c, mlog, two, pk[ch], W[ch], a0, a1);
             }
-            tc::tmem_st_wait();
-            mlog = mnew;
-            prune_exp_tile<T>(s, c, mlog, two, pk, W, lt0, lt1);
+            add2(lt0, lt1, a0, a1, lt0, lt1);
           }
+        };
+        compute();
+        if (t > 0 && bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit))) {
+          // ---- slow path (both warps of the pair): raise the shift to the row maximum,
+          // rescale O_h and the sums once every PV into O_h so far (this half's tile t-1) retired.
+          // (pv_done[h] completes once per tile of this half and cannot run ahead of this set,
+          // unlike the ring barriers, which the other set may advance twice meanwhile.)
+          tc::mbar_wait(&pv_done[h], (gt - 1) & 1);
+          tc::tc_fence_after();
+          const float mnew = fmaxf(mlog, row_max());
+          const float f = fex2(mlog - mnew);
+          l0 *= f;
+          l1 *= f;
+#pragma unroll 1
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t o[16];
+            const uint32_t oaddr = lane_base + T2_O + h * HD + 32 * pr + 16 * hh;
+            tc::tmem_ld_32x32b_x16(oaddr, o);
+            tc::tmem_ld_wait(o);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * f);
+            tc::tmem_st_32x32b_x16(oaddr, o);
+          }
+          tc::tmem_st_wait();
+          mlog = mnew;
+          compute();
         }
         add2(l0, l1, lt0, lt1, l0, l1);
-        // P (8 columns of 16-bit pairs) and the metadata word of TMEM lane r into the tile's own,
-        // already read S columns; rows r and r^8 trade metadata halves (include/dfss.h)
-        const uint32_t partner = __shfl_xor_sync(0xffffffffu, W, 8);
-        const uint32_t word = (lane & 8) ? ((partner >> 16) | (W & 0xFFFF0000u)) : ((W & 0xFFFFu) | (partner << 16));
-        tc::tmem_st_32x32b_x8(s_col0 + sb * BN2 + 16, pk);
-        tc::tmem_st_32x32b_x1(s_col0 + sb * BN2, word);
+        if (tw) FTRACE(1, it, t, h);
+        // P (8 columns of 16-bit pairs at 32q + 16) and the metadata word (column 32q) of each
+        // chunk into this warp's own, already read S columns; rows r and r^8 trade metadata
+        // halves (include/dfss.h)
+#pragma unroll
+        for (int ch = 0; ch < 2; ++ch) {
+          const uint32_t partner = __shfl_xor_sync(0xffffffffu, W[ch], 8);
+          const uint32_t word =
+              (lane & 8) ? ((partner >> 16) | (W[ch] & 0xFFFF0000u)) : ((W[ch] & 0xFFFFu) | (partner << 16));
+          tc::tmem_st_32x32b_x8(scol + 32 * ch + 16, pk[ch]);
+          tc::tmem_st_32x32b_x1(scol + 32 * ch, word);
+        }
         tc::tmem_st_wait();
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&my_p_full[sb]);
-        if (++sb == S2RING) { sb = 0; sph ^= 1; }
+        if (lane == 0) tc::mbar_arrive(&p_full[h * S2RING + slot]);
+        if (tw) FTRACE(2, it, t, h);
       }
       // ---- epilogue: O_h / row sum; this warp writes columns [32 pr, +32) of its rows
       rsum[pr * BM + r] = l0 + l1;
@@ -783,7 +826,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == W_PV) {
     tc::tc_fence_after();
     tc::tmem_dealloc<512>(tmem_base);
   }
@@ -810,7 +853,7 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
   // half.  DFSS_FLASH_KERNEL=1 forces the one-set kernel (experiments).
   static const int force1 = getenv("DFSS_FLASH_KERNEL") ? atoi(getenv("DFSS_FLASH_KERNEL")) == 1 : 0;
   const bool two_set = n % (2 * BM) == 0 && !force1;
-  const uint32_t kvbox = two_set ? BN2 : BN;
+  const uint32_t kvbox = BN;
   kbox[3] = kvbox / 4;
   if (!encode_tmap_3d(&tq, dt, 2, (void*)q, HD, n, bh, HD, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !encode_tmap(&tk, dt, 5, (void*)k, kdims, kstr, kbox, CU_TENSOR_MAP_SWIZZLE_128B) ||
@@ -829,7 +872,29 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
   // DFSS_FLASH_VARIANT (timing experiments only; results invalid when set):
   // bit3 skip prune/exp arithmetic, bit4 skip PV MMAs, bit5 skip S MMAs
   static const int variant = getenv("DFSS_FLASH_VARIANT") ? atoi(getenv("DFSS_FLASH_VARIANT")) : 0;
+  static const char* trace_file = getenv("DFSS_FLASH_TRACE");
+  unsigned long long* trace = nullptr;
+  const size_t trace_n = 16 * 2 * 64 * 2;
+  if (trace_file && two_set) {
+    cudaMalloc(&trace, trace_n * 8);
+    cudaMemset(trace, 0, trace_n * 8);
+    cudaMemcpyToSymbol(g_flash_trace, &trace, sizeof(trace));
+  }
   kern<<<grid, NUM_THREADS, smem_total, s>>>(tq, tk, tv, (T*)out, scale, (int)bh, n, 2u, variant);
+  if (trace) {
+    cudaStreamSynchronize(s);
+    unsigned long long* host = (unsigned long long*)malloc(trace_n * 8);
+    cudaMemcpy(host, trace, trace_n * 8, cudaMemcpyDeviceToHost);
+    FILE* f = fopen(trace_file, "wb");
+    if (f) {
+      fwrite(host, 8, trace_n, f);
+      fclose(f);
+    }
+    free(host);
+    unsigned long long* null = nullptr;
+    cudaMemcpyToSymbol(g_flash_trace, &null, sizeof(null));
+    cudaFree(trace);
+  }
   return cudaGetLastError();
 }
 

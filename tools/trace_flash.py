@@ -1,0 +1,16 @@
+"""Run one c4-shaped dfss_attention with DFSS_FLASH_TRACE and print the CTA-0 pipeline timeline (bring-up)."""
+import os, sys
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+out_file = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/flash_trace.bin"
+if os.environ.get("DFSS_FLASH_TRACE") is None:
+    import subprocess
+    env = dict(os.environ, DFSS_FLASH_TRACE=out_file)
+    subprocess.run([sys.executable, __file__, out_file], env=env, check=True)
+    sys.exit(0)
+import torch
+import paper_2203_00091_b200 as dfss
+q, k, v = (torch.randn(8, 12, 4096, 64, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+for _ in range(3):
+    dfss.dfss_attention(q, k, v, "2:4")
+torch.cuda.synchronize()

@@ -239,13 +239,25 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True):
             kt_info[name] = float(np.mean(time_steps(fn, max(3, args.steps), 2, flush)))
         flops = 3.0 * n * n * d  # QK^T (2n^2d) + kept-half PV (n^2d), SURVEY §8(d)
         achieved = flops * bh / (ms_per_step * 1e-3) / 1e12
-        roof = {"kernel": "dfss_flash_kernel", "bound": "tensor", "achieved": round(achieved, 1), "peak": tf_peak,
-                "unit": "TFLOP/s", "frac": round(achieved / tf_peak, 4), "traffic": None,
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(prof):
+            try:
+                t = json.load(open(prof)).get(cfg_name, {}).get("flash")
+                traffic = None if t is None else int(t)
+            except Exception:
+                traffic = None
+        roof = {"kernel": "dfss_flash2_kernel" if n % 256 == 0 else "dfss_flash_kernel", "bound": "tensor",
+                "achieved": round(achieved, 1), "peak": tf_peak,
+                "unit": "TFLOP/s", "frac": round(achieved / tf_peak, 4), "traffic": traffic,
                 "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_src})",
                 "algorithmic_flops_per_launch": flops * bh,
-                "note": "no n^2 HBM traffic; executed tensor work 5n^2d (S twice + sparse PV); "
-                        "bound in practice by the 2:4 selection on the ALU pipe"}
-        ab = {"flash": 10 * n * d * 2}
+                "algorithmic_hbm_bytes_per_launch": 4 * n * d * 2 * bh,
+                "note": "fused kernel, no n^2 HBM traffic (traffic = ncu dram bytes per launch, Q/K/V/O only); "
+                        "tensor work 2n^2d (S) + sparse PV at the 2:4 rate; the bound in practice is the 2:4 "
+                        "prune + exp epilogue on the ALU/FMA pipes (~35 issue-cycles per 4-score group, "
+                        "tools/prune_probe.cu), see profiles/"}
+        ab = {"flash": 4 * n * d * 2}
         dom = "flash"
     else:
         stages = (("sddmm", k_sddmm), ("softmax", k_softmax), ("spmm", k_spmm))

@@ -744,6 +744,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint32_t s[32];
             tc::tmem_ld_32x32b_x32(scol + 32 * ch, s);
             tc::tmem_ld_wait(s);
+            if (tw) FTRACE(11 + 2 * ch, it, t, h);
             float a0, a1;
             if (variant & 8) {  // timing experiment: no prune / exp arithmetic
 #pragma unroll
@@ -754,6 +755,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               prune_exp_tile<T>(s, c, mlog, two, pk[ch], W[ch], a0, a1);
             }
             add2(lt0, lt1, a0, a1, lt0, lt1);
+            if (tw) FTRACE(12 + 2 * ch, it, t, h);
           }
         };
         compute();

@@ -159,11 +159,12 @@ __device__ __forceinline__ void prune_exp_tile(const uint32_t (&s)[32], float c,
     const float v2 = __uint_as_float(s[4 * g + 1]);
     const float v1 = __uint_as_float(s[4 * g + 2]);
     const float v3 = __uint_as_float(s[4 * g + 3]);
-    // winner index of each pair from the sign of the difference; +0 added so that a
-    // (-0) - (+0) tie reads as +0 (ties keep the lower index)
+    // winner index of each pair from the sign of the difference (ties -> +0 -> lower index).
+    // tcgen05.mma writes every zero score as +0 (tools/negzero_probe.cu; covered by
+    // test_flash_tie_lattice_and_zero_queries), so (-0) - (+0) cannot occur and the
+    // differences need no canonicalisation.
     float d01, d23;
     sub2(v0, v2, v1, v3, d01, d23);
-    add2(d01, d23, 0.f, 0.f, d01, d23);
     const uint32_t a = sign_bit(d01, two), b = sign_bit(d23, two);
     const float w01 = fmaxf(v0, v1), l01 = fminf(v0, v1);
     const float w23 = fmaxf(v2, v3), l23 = fminf(v2, v3);

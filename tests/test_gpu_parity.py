@@ -369,6 +369,14 @@ def test_flash_tie_lattice_and_zero_queries():
     kept = vv.reshape(2, n // 4, 4, 64)[:, :, :2].reshape(2, n // 2, 64).mean(1)
     assert np.abs(want[0] - kept[:, None, :]).max() < 1e-12
     assert np.abs(out[0] - kept[:, None, :]).max() < 2e-2
+    # -0 queries against keys whose sign alternates per key: every dot product is a sum of
+    # -0 (or +0) terms only, so in IEEE arithmetic the scores alternate -0 / +0.  The fused
+    # kernel relies on tcgen05 writing zero sums as +0 (tools/negzero_probe.cu) to skip
+    # canonicalising the pair differences; the reference treats -0 == +0 (lower index wins).
+    sign = torch.where(torch.arange(n) % 2 == 0, 1.0, -1.0).view(1, 1, n, 1)
+    kpos = (torch.rand((1, 2, n, 64), generator=g) + 0.5) * sign
+    out, want = _flash_vs_oracle(-torch.zeros_like(q), kpos.to(torch.bfloat16).cuda(), v, "signed-zero scores")
+    assert np.abs(out[0] - kept[:, None, :]).max() < 2e-2
 
 
 @pytest.mark.parametrize("n", [128, 256, 4096])

@@ -1,4 +1,4 @@
-// flash_tc.cu -- fully fused DFSS attention on tcgen05 (2:4, bf16/fp16, head dim 64).
+// flash_tc.cu -- fully fused DFSS attention on tcgen05 (2:4 and 1:2, bf16/fp16, head dim 64).
 //
 // pipeline.nm_attention (pipeline.py:15-32) in one kernel with no n x n tensor of any
 // kind in HBM.  Per 128-query half-block h and 128-key tile t:
@@ -147,7 +147,11 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
 // One quarter-tile of one row: 8 groups of 4 scores s[] in (v0, v2, v1, v3) register order.
 // Prunes 2:4 (reference rule), exponentiates the kept half against the shift `mlog`
 // (= m * c), packs P, builds the metadata word W (group g at bits 4g) and the partial sum.
-template <typename T>
+//
+// PAIRS (mode 1:2 on 16-bit data): keep the larger of each pair, element 1 iff v1 > v0
+// (codec.py:114-117) -- on the tensor core this is the 2:4 pattern with one survivor per
+// pair, nibble 8 + a + 4b, so the same sparse MMA consumes it.
+template <typename T, bool PAIRS>
 __device__ __forceinline__ void prune_exp_tile(const uint32_t (&s)[32], float c, float mlog, uint32_t two,
                                                uint32_t (&pk)[8], uint32_t& W, float& lt0, float& lt1) {
   W = 0x88888888u;
@@ -166,15 +170,19 @@ __device__ __forceinline__ void prune_exp_tile(const uint32_t (&s)[32], float c,
     float d01, d23;
     sub2(v0, v2, v1, v3, d01, d23);
     const uint32_t a = sign_bit(d01, two), b = sign_bit(d23, two);
-    const float w01 = fmaxf(v0, v1), l01 = fminf(v0, v1);
-    const float w23 = fmaxf(v2, v3), l23 = fminf(v2, v3);
-    const bool keep01 = l01 >= w23;  // lower-index loser vs higher-index winner
-    const bool keep23 = l23 > w01;   // higher-index loser must strictly beat the winner
-    const float lo = keep01 ? v0 : (keep23 ? v2 : w01);
-    const float hi = keep01 ? v1 : (keep23 ? v3 : w23);
+    const float w01 = fmaxf(v0, v1), w23 = fmaxf(v2, v3);
+    float lo = w01, hi = w23;
     // nibble - 8: 0x4 -> -4, 0xE -> 6, mixed 8 + a + 4b -> a + 4b
-    int nib = keep23 ? 6 : (int)(a + 4u * b);
-    nib = keep01 ? -4 : nib;
+    int nib = (int)(a + 4u * b);
+    if (!PAIRS) {
+      const float l01 = fminf(v0, v1), l23 = fminf(v2, v3);
+      const bool keep01 = l01 >= w23;  // lower-index loser vs higher-index winner
+      const bool keep23 = l23 > w01;   // higher-index loser must strictly beat the winner
+      lo = keep01 ? v0 : (keep23 ? v2 : w01);
+      hi = keep01 ? v1 : (keep23 ? v3 : w23);
+      nib = keep23 ? 6 : nib;
+      nib = keep01 ? -4 : nib;
+    }
     W += (uint32_t)nib * (1u << (4 * g));
     float x0, x1;
     fma2s(lo, hi, c, -mlog, x0, x1);
@@ -184,7 +192,7 @@ __device__ __forceinline__ void prune_exp_tile(const uint32_t (&s)[32], float c,
   }
 }
 
-template <typename T, int HALVES>
+template <typename T, int HALVES, bool PAIRS>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     dfss_flash_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, T* __restrict__ out, float scale, int bh, int n,
@@ -402,7 +410,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // first tile of the item: the shift starts at the row maximum of this tile
             mlog[h] = row_max(s);
             l0[h] = l1[h] = 0.f;
-            prune_exp_tile<T>(s, c, mlog[h], two, pk, W, lt0, lt1);
+            prune_exp_tile<T, PAIRS>(s, c, mlog[h], two, pk, W, lt0, lt1);
           } else {
             if (variant & 8) {  // timing experiment: no prune / exp arithmetic
 #pragma unroll
@@ -410,7 +418,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               W = 0x44444444u;
               lt0 = lt1 = 0.f;
             } else {
-              prune_exp_tile<T>(s, c, mlog[h], two, pk, W, lt0, lt1);
+              prune_exp_tile<T, PAIRS>(s, c, mlog[h], two, pk, W, lt0, lt1);
             }
             if (bar_any(qbar, 128, !(lt0 + lt1 <= kSumLimit))) {
               // ---- slow path (whole quad): raise the shift to the row maximum, rescale O_h and the sums.
@@ -431,7 +439,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               tc::tmem_st_32x32b_x16(oaddr, o);
               tc::tmem_st_wait();
               mlog[h] = mnew;
-              prune_exp_tile<T>(s, c, mlog[h], two, pk, W, lt0, lt1);
+              prune_exp_tile<T, PAIRS>(s, c, mlog[h], two, pk, W, lt0, lt1);
             }
           }
           add2(l0[h], l1[h], lt0, lt1, l0[h], l1[h]);
@@ -529,7 +537,7 @@ __device__ unsigned long long* g_flash_trace = nullptr;
       trace[((((slot) * 2 + (it_)) * 64 + (t_)) * 2 + (h_))] = clock64();                          \
   } while (0)
 
-template <typename T>
+template <typename T, bool PAIRS>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     dfss_flash2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, T* __restrict__ out, float scale, int bh, int n,
@@ -753,7 +761,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               W[ch] = 0x44444444u;
               a0 = a1 = 0.f;
             } else {
-              prune_exp_tile<T>(s, c, mlog, two, pk[ch], W[ch], a0, a1);
+              prune_exp_tile<T, PAIRS>(s, c, mlog, two, pk[ch], W[ch], a0, a1);
             }
             add2(lt0, lt1, a0, a1, lt0, lt1);
             if (tw) FTRACE(12 + 2 * ch, it, t, h);
@@ -836,10 +844,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 bool tc_flash_supported(int gs, int dtype, int n, int d) {
-  return gs == 4 && (dtype == DFSS_BF16 || dtype == DFSS_F16) && d == HD && n % BM == 0 && n > 0;
+  return (gs == 4 || gs == 2) && (dtype == DFSS_BF16 || dtype == DFSS_F16) && d == HD && n % BM == 0 && n > 0;
 }
 
-template <typename T>
+template <typename T, bool PAIRS>
 static cudaError_t flash_launch_typed(const void* q, const void* k, const void* v, void* out, float scale, int64_t bh,
                                       int n, cudaStream_t s) {
   const CUtensorMapDataType dt =
@@ -863,7 +871,7 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
       !encode_tmap_3d(&tv, dt, 2, (void*)v, HD, n, bh, HD, kvbox, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   const int halves = two_set ? 2 : 1;
-  auto kern = two_set ? dfss_flash2_kernel<T> : dfss_flash_kernel<T, 1>;
+  auto kern = two_set ? dfss_flash2_kernel<T, PAIRS> : dfss_flash_kernel<T, 1, PAIRS>;
   const int smem_total = two_set ? S2_TOTAL : SMEM_TOTAL;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_total);
   if (e != cudaSuccess) return e;
@@ -905,8 +913,12 @@ cudaError_t launch_flash_tc(const void* q, const void* k, const void* v, void* o
                             int64_t bh, int n, int d, cudaStream_t s) {
   if (!tc_flash_supported(gs, dtype, n, d)) return cudaErrorNotSupported;
   if (bh == 0) return cudaSuccess;
-  if (dtype == DFSS_BF16) return flash_launch_typed<__nv_bfloat16>(q, k, v, out, scale, bh, n, s);
-  return flash_launch_typed<__half>(q, k, v, out, scale, bh, n, s);
+  if (gs == 2) {
+    if (dtype == DFSS_BF16) return flash_launch_typed<__nv_bfloat16, true>(q, k, v, out, scale, bh, n, s);
+    return flash_launch_typed<__half, true>(q, k, v, out, scale, bh, n, s);
+  }
+  if (dtype == DFSS_BF16) return flash_launch_typed<__nv_bfloat16, false>(q, k, v, out, scale, bh, n, s);
+  return flash_launch_typed<__half, false>(q, k, v, out, scale, bh, n, s);
 }
 
 }  // namespace dfss

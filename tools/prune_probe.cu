@@ -61,25 +61,37 @@ __global__ void __launch_bounds__(640, 1) k(int iters, uint32_t* out, long long*
       }
       const float w01 = MODE == 10 ? v0 : fmaxf(v0, v1), l01 = MODE == 10 ? v1 : fminf(v0, v1);
       const float w23 = MODE == 10 ? v2 : fmaxf(v2, v3), l23 = MODE == 10 ? v3 : fminf(v2, v3);
-      const bool keep01 = MODE >= 8 ? false : l01 >= w23;
-      const bool keep23 = MODE >= 8 ? false : l23 > w01;
+      const bool keep01 = (MODE >= 8 && MODE < 12) ? false : l01 >= w23;
+      const bool keep23 = (MODE >= 8 && MODE < 12) ? false : l23 > w01;
       float lo = MODE == 6 ? w01 : (keep01 ? v0 : (keep23 ? v2 : w01));
       float hi = MODE == 6 ? w23 : (keep01 ? v1 : (keep23 ? v3 : w23));
       int nib = (int)(MODE == 2 ? (a | b) : (a + 4u * b));
-      if (MODE != 7 && MODE < 8) {
+      if (MODE != 7 && (MODE < 8 || MODE >= 12)) {
         nib = keep23 ? 6 : nib;
         nib = keep01 ? -4 : nib;
       }
-      if (MODE == 12) {
+      if (MODE == 12 || MODE == 13) {
+        // keep predicates once, then predicated moves (nibble only for 13, nibble + lo/hi for 12)
         float lo2 = w01, hi2 = w23;
         int nib2 = (int)(a + 4u * b);
-        asm("{\n\t.reg .pred p01, p23;\n\t"
-            "setp.ge.f32 p01, %5, %6;\n\t"
-            "setp.gt.f32 p23, %7, %8;\n\t"
-            "@p23 mov.b32 %0, %9;\n\t@p23 mov.b32 %1, %10;\n\t@p23 mov.b32 %2, 6;\n\t"
-            "@p01 mov.b32 %0, %11;\n\t@p01 mov.b32 %1, %12;\n\t@p01 mov.b32 %2, -4;\n\t}"
-            : "+f"(lo2), "+f"(hi2), "+r"(nib2), "+f"(lo2), "+f"(hi2)
-            : "f"(l01), "f"(w23), "f"(l23), "f"(w01), "f"(v2), "f"(v3), "f"(v0), "f"(v1));
+        if (MODE == 12)
+          asm volatile("{\n\t.reg .pred p01, p23;\n\t"
+              "setp.ge.f32 p01, %3, %4;\n\t"
+              "setp.gt.f32 p23, %5, %6;\n\t"
+              "@p23 mov.b32 %0, %7;\n\t@p23 mov.b32 %1, %8;\n\t@p23 mov.b32 %2, 6;\n\t"
+              "@p01 mov.b32 %0, %9;\n\t@p01 mov.b32 %1, %10;\n\t@p01 mov.b32 %2, -4;\n\t}"
+              : "+f"(lo2), "+f"(hi2), "+r"(nib2)
+              : "f"(l01), "f"(w23), "f"(l23), "f"(w01), "f"(v2), "f"(v3), "f"(v0), "f"(v1));
+        else {
+          lo2 = keep01 ? v0 : (keep23 ? v2 : w01);
+          hi2 = keep01 ? v1 : (keep23 ? v3 : w23);
+          asm volatile("{\n\t.reg .pred p01, p23;\n\t"
+              "setp.ge.f32 p01, %1, %2;\n\t"
+              "setp.gt.f32 p23, %3, %4;\n\t"
+              "@p23 mov.b32 %0, 6;\n\t@p01 mov.b32 %0, -4;\n\t}"
+              : "+r"(nib2)
+              : "f"(l01), "f"(w23), "f"(l23), "f"(w01));
+        }
         lo = lo2; hi = hi2; nib = nib2;
       }
       W += (uint32_t)nib * (1u << (4 * g));
@@ -118,8 +130,9 @@ int main() {
   cudaMalloc(&out, 148 * 640 * 4); cudaMalloc(&cyc, 148 * 8);
   const char* names[] = {"IMAD.HI sign bits", "SHF sign bits", "SHF + mask nibble", "SHF, no canon FADD2",
                          "no MUFU", "no F2FP (PRMT)", "no FSEL", "no nibble SEL", "no keep FSETP",
-                         "8 + no sign bits", "8 + no FMNMX", "8 + no d FADD2s/sign", "predicated movs"};
-  for (int mode = 0; mode < 13; ++mode) {
+                         "8 + no sign bits", "8 + no FMNMX", "8 + no d FADD2s/sign", "predicated movs",
+                         "predicated nibble movs"};
+  for (int mode = 0; mode < 14; ++mode) {
     const int warps = 16;
     switch (mode) {
       case 0: k<0><<<148, warps * 32>>>(4096, out, cyc, 0.18f, 0.5f, 2u); break;
@@ -135,6 +148,7 @@ int main() {
       case 10: k<10><<<148, warps * 32>>>(4096, out, cyc, 0.18f, 0.5f, 2u); break;
       case 11: k<11><<<148, warps * 32>>>(4096, out, cyc, 0.18f, 0.5f, 2u); break;
       case 12: k<12><<<148, warps * 32>>>(4096, out, cyc, 0.18f, 0.5f, 2u); break;
+      case 13: k<13><<<148, warps * 32>>>(4096, out, cyc, 0.18f, 0.5f, 2u); break;
     }
     cudaDeviceSynchronize();
     cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);

@@ -13,11 +13,13 @@ def t_ms(fn, it=20):
     e.record(); torch.cuda.synchronize()
     return s.elapsed_time(e) / it
 
+import os as _os
+MODE = _os.environ.get("DFSS_MODE", "2:4")
 for name, (b, h, n, dt) in {"c2": (32, 12, 512, torch.bfloat16), "c3": (16, 16, 1024, torch.float16),
                              "c4": (8, 12, 4096, torch.bfloat16)}.items():
     q, k, v = (torch.randn(b, h, n, 64, device="cuda", dtype=dt) for _ in range(3))
     out = torch.empty_like(q)
-    ws = torch.empty(dfss.workspace_bytes("2:4", dt, b * h, n, 64), dtype=torch.uint8, device="cuda")
-    a = t_ms(lambda: dfss.dfss_attention(q, k, v, "2:4", out=out, workspace=ws))
+    ws = torch.empty(dfss.workspace_bytes(MODE, dt, b * h, n, 64), dtype=torch.uint8, device="cuda")
+    a = t_ms(lambda: dfss.dfss_attention(q, k, v, MODE, out=out, workspace=ws))
     s = t_ms(lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v))
-    print(f"{name}: dfss {a:.4f} ms  sdpa {s:.4f} ms  speedup {s / a:.3f}x", flush=True)
+    print(f"{name} {MODE}: dfss {a:.4f} ms  sdpa {s:.4f} ms  speedup {s / a:.3f}x", flush=True)

@@ -169,7 +169,10 @@ __device__ __forceinline__ void prune_exp_tile(const uint32_t (&s)[32], float c,
     // differences need no canonicalisation.
     float d01, d23;
     sub2(v0, v2, v1, v3, d01, d23);
-    const uint32_t a = sign_bit(d01, two), b = sign_bit(d23, two);
+    // sign bits: IMAD.HI on the FMA pipe for 2:4 (the ALU pipe is the busy one there), SHF on
+    // the otherwise idle ALU pipe for 1:2 (there the FMA pipe and MUFU are the busy ones)
+    const uint32_t a = PAIRS ? __float_as_uint(d01) >> 31 : sign_bit(d01, two);
+    const uint32_t b = PAIRS ? __float_as_uint(d23) >> 31 : sign_bit(d23, two);
     const float w01 = fmaxf(v0, v1), w23 = fmaxf(v2, v3);
     float lo = w01, hi = w23;
     // nibble - 8: 0x4 -> -4, 0xE -> 6, mixed 8 + a + 4b -> a + 4b

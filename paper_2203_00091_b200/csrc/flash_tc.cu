@@ -736,6 +736,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc::named_bar_sync(pbar, 64);
       return m * c;
     };
+    // ---- epilogue of a finished item: O_h / row sum; this warp writes columns [32 pr, +32) of its rows
+    bool pend = false;
+    int pend_b = 0, pend_ib = 0, pend_it = 0;
+    float pend_l = 0.f;
+    auto epilogue = [&]() {
+      rsum[pr * BM + r] = pend_l;
+      tc::named_bar_sync(pbar, 64);
+      const float inv = 1.0f / (rsum[r] + rsum[BM + r]);
+      tc::named_bar_sync(pbar, 64);
+      tc::mbar_wait(&o_full[h], pend_it & 1);
+      tc::tc_fence_after();
+      uint32_t o[32];
+      tc::tmem_ld_32x32b_x32(lane_base + T2_O + h * HD + 32 * pr, o);
+      tc::tmem_ld_wait(o);
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&o_empty[h]);
+      uint32_t pko[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        pko[j] = fpack2<T>(__uint_as_float(o[2 * j]) * inv, __uint_as_float(o[2 * j + 1]) * inv);
+      const int64_t row = (int64_t)pend_b * n + (pend_ib * 2 + h) * BM + r;
+      uint4* orow = reinterpret_cast<uint4*>(out + row * HD + 32 * pr);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) orow[j] = make_uint4(pko[4 * j], pko[4 * j + 1], pko[4 * j + 2], pko[4 * j + 3]);
+      pend = false;
+    };
     for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
       const int b = item / iblocks, ib = item % iblocks;
       float mlog = 0.f, l0 = 0.f, l1 = 0.f;
@@ -814,29 +841,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&p_full[h * S2RING + slot]);
         if (tw) FTRACE(2, it, t, h);
+        if (pend) epilogue();  // previous item's output (t == 0 only)
       }
-      // ---- epilogue: O_h / row sum; this warp writes columns [32 pr, +32) of its rows
-      rsum[pr * BM + r] = l0 + l1;
-      tc::named_bar_sync(pbar, 64);
-      const float inv = 1.0f / (rsum[r] + rsum[BM + r]);
-      tc::named_bar_sync(pbar, 64);
-      tc::mbar_wait(&o_full[h], it & 1);
-      tc::tc_fence_after();
-      uint32_t o[32];
-      tc::tmem_ld_32x32b_x32(lane_base + T2_O + h * HD + 32 * pr, o);
-      tc::tmem_ld_wait(o);
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&o_empty[h]);
-      uint32_t pko[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        pko[j] = fpack2<T>(__uint_as_float(o[2 * j]) * inv, __uint_as_float(o[2 * j + 1]) * inv);
-      const int64_t row = (int64_t)b * n + (ib * 2 + h) * BM + r;
-      uint4* orow = reinterpret_cast<uint4*>(out + row * HD + 32 * pr);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) orow[j] = make_uint4(pko[4 * j], pko[4 * j + 1], pko[4 * j + 2], pko[4 * j + 3]);
+      // the epilogue of this item runs after step 0 of the next one (below), so the wait for
+      // the item's last PV overlaps that step instead of idling the set at every item boundary
+      pend = true;
+      pend_b = b;
+      pend_ib = ib;
+      pend_it = it;
+      pend_l = l0 + l1;
     }
+    if (pend) epilogue();
   }
   tc::tc_fence_before();
   __syncthreads();

@@ -10,7 +10,8 @@ if os.environ.get("DFSS_FLASH_TRACE") is None:
     sys.exit(0)
 import torch
 import paper_2203_00091_b200 as dfss
-q, k, v = (torch.randn(8, 12, 4096, 64, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+shape = [int(x) for x in os.environ.get("TRACE_SHAPE", "8,12,4096,64").split(",")]
+q, k, v = (torch.randn(*shape, device="cuda", dtype=torch.bfloat16) for _ in range(3))
 for _ in range(3):
     dfss.dfss_attention(q, k, v, "2:4")
 torch.cuda.synchronize()

@@ -141,6 +141,19 @@ int dfss_nm_attention(const void* q, const void* k, const void* v, void* out, in
                       int64_t bh, int n, int d, void* workspace, int64_t workspace_bytes, void* stream);
 
 /*
+ * nm_attention with a BlockMask (pipeline.py:15-32 with block_mask; mask threaded as in
+ * fused.py:73-82 and sparse_ops.py:27-30,57-64): tile_keep is the DEVICE uint8 grid
+ * [ceil(n/tile_rows)][ceil(n/tile_cols)] shared by every (batch, head); masked tiles are
+ * structurally absent.  16-bit inputs with tile_rows and tile_cols multiples of 32 run the
+ * fused kernel (masked 32x32 chunks skipped); other shapes run the staged kernels.  Rows whose
+ * tiles are all masked are undefined here -- the host layer rejects them first, as the
+ * reference's softmax_rows does ("empty row N").  tile_keep == NULL is dfss_nm_attention.
+ */
+int dfss_nm_attention_masked(const void* q, const void* k, const void* v, void* out, int mode, int dtype, int math,
+                             int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows, int tile_cols,
+                             void* workspace, int64_t workspace_bytes, void* stream);
+
+/*
  * Parity hook: prune a given fp32 score tensor with the SAME device selection
  * routine the SDDMM epilogue uses (codec._select_rows, codec.py:289-313).
  *   scores [rows, cols] fp32 -> nonzeros [rows, cols/2] (nz_dtype),

@@ -38,6 +38,8 @@ SIGNATURES = {
                          _vp]),
     "dfss_nm_attention_workspace_bytes": (_i64, [_i32, _i32, _i64, _i32, _i32]),
     "dfss_nm_attention": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i64, _i32, _i32, _vp, _i64, _vp]),
+    "dfss_nm_attention_masked": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i64, _i32, _i32, _vp, _i32, _i32, _vp,
+                                        _i64, _vp]),
     "dfss_prune_scores": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i64, _i32, _vp]),
     "dfss_meta_hw_to_logical": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp]),
     "dfss_meta_logical_to_hw": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp]),

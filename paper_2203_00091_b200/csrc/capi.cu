@@ -135,10 +135,18 @@ int64_t dfss_nm_attention_workspace_bytes(int mode, int dtype, int64_t bh, int n
 
 int dfss_nm_attention(const void* q, const void* k, const void* v, void* out, int mode, int dtype, int math,
                       int64_t bh, int n, int d, void* workspace, int64_t workspace_bytes, void* stream) {
+  return dfss_nm_attention_masked(q, k, v, out, mode, dtype, math, bh, n, d, nullptr, 0, 0, workspace,
+                                  workspace_bytes, stream);
+}
+
+int dfss_nm_attention_masked(const void* q, const void* k, const void* v, void* out, int mode, int dtype, int math,
+                             int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows, int tile_cols,
+                             void* workspace, int64_t workspace_bytes, void* stream) {
   if (!valid_mode(mode)) return fail(DFSS_ERR_INVALID, "unknown sparsity mode (expected 2 or 4)");
   if (!valid_dtype(dtype)) return fail(DFSS_ERR_INVALID, "unknown dtype");
   if (bh < 0 || n < 1 || d < 1) return fail(DFSS_ERR_INVALID, "shape dimensions must be positive");
   if (n % mode != 0) return fail(DFSS_ERR_INVALID, "sequence length not group-aligned for the mode");
+  if (int st = check_keep(tile_keep, tile_rows, tile_cols, mode)) return st;
   const int64_t need = dfss_nm_attention_workspace_bytes(mode, dtype, bh, n, d);
   if (!workspace || workspace_bytes < need) return fail(DFSS_ERR_INVALID, "workspace too small");
   if (bh == 0) return DFSS_OK;
@@ -149,9 +157,21 @@ int dfss_nm_attention(const void* q, const void* k, const void* v, void* out, in
   uint32_t* meta = (uint32_t*)(ws + (nz_bytes + 255) / 256 * 256);
   float* row_max = (float*)(ws + (nz_bytes + 255) / 256 * 256 + (meta_bytes + 255) / 256 * 256);
   const float scale = 1.0f / sqrtf((float)d);
-  // fully fused: one kernel, no n x n tensor in HBM (flash_tc.cu)
-  if (math == DFSS_MATH_AUTO && dtype != DFSS_F32 && dfss::tc_flash_supported(mode, dtype, n, d) && dfss_has_tcgen05())
-    return cuda_status(dfss::launch_flash_tc(q, k, v, out, scale, mode, dtype, bh, n, d, (cudaStream_t)stream));
+  // fully fused: one kernel, no n x n tensor in HBM (flash_tc.cu); block masks with 32-aligned tiles
+  if (math == DFSS_MATH_AUTO && dtype != DFSS_F32 && dfss::tc_flash_supported(mode, dtype, n, d) &&
+      (!tile_keep || dfss::tc_flash_mask_supported(tile_rows, tile_cols)) && dfss_has_tcgen05())
+    return cuda_status(dfss::launch_flash_tc(q, k, v, out, scale, mode, dtype, bh, n, d, tile_keep, tile_rows,
+                                             tile_cols, (cudaStream_t)stream));
+  if (tile_keep) {
+    // staged with the mask threaded through every stage (fused.py:73-82, sparse_ops.py:27-30,57-64)
+    int st = dfss_sddmm_prune(q, k, nz, meta, scale, mode, dtype, dtype, math, bh, n, n, d, tile_keep, tile_rows,
+                              tile_cols, nullptr, nullptr, stream);
+    if (st) return st;
+    st = dfss_softmax_rows(nz, nz, dtype, dtype, bh, n, n / 2, tile_keep, tile_rows, tile_cols, nullptr, stream);
+    if (st) return st;
+    return dfss_spmm(nz, meta, v, out, mode, dtype, dtype, dtype, bh, n, n, d, tile_keep, tile_rows, tile_cols,
+                     nullptr, stream);
+  }
   // fused path: SDDMM+prune (+row max) -> SpMM with the softmax applied to the staged P tiles
   const bool fused = math == DFSS_MATH_AUTO && dtype != DFSS_F32 &&
                      dfss::tc_sddmm_supported(mode, dtype, dtype, n, n, d) &&

@@ -194,7 +194,11 @@ cudaError_t launch_spmm_tc(const void* p, const uint32_t* meta, const void* v, v
 bool tc_sddmm_supported(int gs, int in_dtype, int nz_dtype, int n, int m, int d);
 // fully fused attention (flash_tc.cu): no n x n tensor in HBM
 bool tc_flash_supported(int gs, int dtype, int n, int d);
+// tile_keep (nullable): BlockMask grid [ceil(n/tile_rows)][ceil(n/tile_cols)], uint8, shared by all bh;
+// needs tile_rows % 32 == 0 and tile_cols % 32 == 0 (tc_flash_mask_supported)
+bool tc_flash_mask_supported(int tile_rows, int tile_cols);
 cudaError_t launch_flash_tc(const void* q, const void* k, const void* v, void* out, float scale, int gs, int dtype,
-                            int64_t bh, int n, int d, cudaStream_t s);
+                            int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows, int tile_cols,
+                            cudaStream_t s);
 bool tc_spmm_supported(int gs, int p_dtype, int v_dtype, int out_dtype, int rows, int n_k, int d);
 }  // namespace dfss

@@ -144,6 +144,27 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
+// Optional tile-grid keep mask (BlockMask, codec.py:150-200): keep[i * grid_cols + j] covers
+// rows [i*tile_rows, +tile_rows) and key columns [j*tile_cols, +tile_cols), shared by every
+// (batch, head).  The fused kernels need tile_rows and tile_cols to be multiples of 32, so a
+// warp's 32 rows x 32 columns chunk lies in one tile: masked chunks are skipped warp-uniformly
+// (no prune / exp work, zero P), i.e. masked tiles are structurally absent as in the reference.
+struct TileMask {
+  const uint8_t* keep;
+  int tile_rows, tile_cols, grid_cols;
+  __device__ __forceinline__ bool masked(int row, int col) const {
+    return keep != nullptr && __ldg(keep + (row / tile_rows) * grid_cols + col / tile_cols) == 0;
+  }
+};
+
+// masked chunk: no kept values, P = 0, nibble 0x4 in every group (W = 0x44444444)
+__device__ __forceinline__ void masked_chunk(uint32_t (&pk)[8], uint32_t& W, float& lt0, float& lt1) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) pk[j] = 0u;
+  W = 0x44444444u;
+  lt0 = lt1 = 0.f;
+}
+
 // One quarter-tile of one row: 8 groups of 4 scores s[] in (v0, v2, v1, v3) register order.
 // Prunes 2:4 (reference rule), exponentiates the kept half against the shift `mlog`
 // (= m * c), packs P, builds the metadata word W (group g at bits 4g) and the partial sum.
@@ -195,11 +216,11 @@ __device__ __forceinline__ void prune_exp_tile(const uint32_t (&s)[32], float c,
   }
 }
 
-template <typename T, int HALVES, bool PAIRS>
+template <typename T, int HALVES, bool PAIRS, bool MASKED>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     dfss_flash_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, T* __restrict__ out, float scale, int bh, int n,
-                      uint32_t two, int variant) {
+                      uint32_t two, int variant, TileMask tmask) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + SMEM_BAR);
@@ -378,10 +399,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int pb = 0;
     uint32_t pph = 0, oph = 0, g = 0;
     // row maximum of the current step over the quad's four quarters (scaled to log2 units)
+    bool cmask = false;  // this warp's chunk of the current tile is masked (BlockMask)
     auto row_max = [&](const uint32_t (&s)[32]) {
       float mt = -INFINITY;
+      if (!cmask) {
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) mt = fmaxf(mt, fmaxf(__uint_as_float(s[j]), __uint_as_float(s[j + 1])));
+        for (int j = 0; j < 32; j += 2) mt = fmaxf(mt, fmaxf(__uint_as_float(s[j]), __uint_as_float(s[j + 1])));
+      }
       red_max[quarter * BM + r] = mt;
       tc::named_bar_sync(qbar, 128);
       const float m = fmaxf(fmaxf(red_max[r], red_max[BM + r]), fmaxf(red_max[2 * BM + r], red_max[3 * BM + r]));
@@ -406,6 +430,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
           uint32_t pk[8], W;
           float lt0, lt1;
+          cmask = MASKED && tmask.masked((ib * HALVES + h) * BM + quad * 32, t * BN + quarter * 32);
           // P stage pb: PV of step g - PST (for PST = 2 and two halves: this half's previous tile) retired
           tc::mbar_wait(&p_empty[pb], pph ^ 1);
           tc::tc_fence_after();
@@ -413,7 +438,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // first tile of the item: the shift starts at the row maximum of this tile
             mlog[h] = row_max(s);
             l0[h] = l1[h] = 0.f;
-            prune_exp_tile<T, PAIRS>(s, c, mlog[h], two, pk, W, lt0, lt1);
+            if (cmask) masked_chunk(pk, W, lt0, lt1); else prune_exp_tile<T, PAIRS>(s, c, mlog[h], two, pk, W, lt0, lt1);
           } else {
             if (variant & 8) {  // timing experiment: no prune / exp arithmetic
 #pragma unroll
@@ -421,7 +446,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               W = 0x44444444u;
               lt0 = lt1 = 0.f;
             } else {
-              prune_exp_tile<T, PAIRS>(s, c, mlog[h], two, pk, W, lt0, lt1);
+              if (cmask) masked_chunk(pk, W, lt0, lt1); else prune_exp_tile<T, PAIRS>(s, c, mlog[h], two, pk, W, lt0, lt1);
             }
             if (bar_any(qbar, 128, !(lt0 + lt1 <= kSumLimit))) {
               // ---- slow path (whole quad): raise the shift to the row maximum, rescale O_h and the sums.
@@ -442,7 +467,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               tc::tmem_st_32x32b_x16(oaddr, o);
               tc::tmem_st_wait();
               mlog[h] = mnew;
-              prune_exp_tile<T, PAIRS>(s, c, mlog[h], two, pk, W, lt0, lt1);
+              if (cmask) masked_chunk(pk, W, lt0, lt1); else prune_exp_tile<T, PAIRS>(s, c, mlog[h], two, pk, W, lt0, lt1);
             }
           }
           add2(l0[h], l1[h], lt0, lt1, l0[h], l1[h]);
@@ -540,11 +565,11 @@ __device__ unsigned long long* g_flash_trace = nullptr;
       trace[((((slot) * 2 + (it_)) * 64 + (t_)) * 2 + (h_))] = clock64();                          \
   } while (0)
 
-template <typename T, bool PAIRS>
+template <typename T, bool PAIRS, bool MASKED>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     dfss_flash2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, T* __restrict__ out, float scale, int bh, int n,
-                       uint32_t two, int variant) {
+                       uint32_t two, int variant, TileMask tmask) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + S2_BAR);
@@ -720,10 +745,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t gt = 0, scol = 0;  // scol: this warp's first S column of the current step's buffer
     int it = 0;
     // maximum of this row over the set's 128 columns of the current S (both warps of the pair)
+    bool cm[2] = {false, false};  // this warp's two chunks of the current tile masked (BlockMask)
     auto row_max = [&]() {
       float mt = -INFINITY;
-#pragma unroll 1
+#pragma unroll
       for (int ch = 0; ch < 2; ++ch) {
+        if (cm[ch]) continue;
         uint32_t s[32];
         tc::tmem_ld_32x32b_x32(scol + 32 * ch, s);
         tc::tmem_ld_wait(s);
@@ -773,6 +800,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc::mbar_wait(&s_full[slot], (g / S2RING) & 1);
         if (tw) FTRACE(0, it, t, h);
         tc::tc_fence_after();
+        const int row0 = (ib * 2 + h) * BM + quad * 32, col0 = t * BN + 64 * pr;
+        cm[0] = MASKED && tmask.masked(row0, col0);
+        cm[1] = MASKED && tmask.masked(row0, col0 + 32);
         if (t == 0) mlog = row_max();  // the shift starts at the row maximum of the item's first tile
         uint32_t pk[2][8], W[2];
         float lt0 = 0.f, lt1 = 0.f;
@@ -780,11 +810,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           lt0 = lt1 = 0.f;
 #pragma unroll
           for (int ch = 0; ch < 2; ++ch) {
+            float a0, a1;
+            if (cm[ch]) {  // masked tile: structurally absent
+              masked_chunk(pk[ch], W[ch], a0, a1);
+              continue;
+            }
             uint32_t s[32];
             tc::tmem_ld_32x32b_x32(scol + 32 * ch, s);
             tc::tmem_ld_wait(s);
             if (tw) FTRACE(11 + 2 * ch, it, t, h);
-            float a0, a1;
             if (variant & 8) {  // timing experiment: no prune / exp arithmetic
 #pragma unroll
               for (int j = 0; j < 8; ++j) pk[ch][j] = s[j] ^ s[j + 8];
@@ -865,9 +899,9 @@ bool tc_flash_supported(int gs, int dtype, int n, int d) {
   return (gs == 4 || gs == 2) && (dtype == DFSS_BF16 || dtype == DFSS_F16) && d == HD && n % BM == 0 && n > 0;
 }
 
-template <typename T, bool PAIRS>
+template <typename T, bool PAIRS, bool MASKED>
 static cudaError_t flash_launch_typed(const void* q, const void* k, const void* v, void* out, float scale, int64_t bh,
-                                      int n, cudaStream_t s) {
+                                      int n, TileMask tmask, cudaStream_t s) {
   const CUtensorMapDataType dt =
       std::is_same<T, __nv_bfloat16>::value ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv;
@@ -889,7 +923,7 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
       !encode_tmap_3d(&tv, dt, 2, (void*)v, HD, n, bh, HD, kvbox, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   const int halves = two_set ? 2 : 1;
-  auto kern = two_set ? dfss_flash2_kernel<T, PAIRS> : dfss_flash_kernel<T, 1, PAIRS>;
+  auto kern = two_set ? dfss_flash2_kernel<T, PAIRS, MASKED> : dfss_flash_kernel<T, 1, PAIRS, MASKED>;
   const int smem_total = two_set ? S2_TOTAL : SMEM_TOTAL;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_total);
   if (e != cudaSuccess) return e;
@@ -909,7 +943,7 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
     cudaMemset(trace, 0, trace_n * 8);
     cudaMemcpyToSymbol(g_flash_trace, &trace, sizeof(trace));
   }
-  kern<<<grid, NUM_THREADS, smem_total, s>>>(tq, tk, tv, (T*)out, scale, (int)bh, n, 2u, variant);
+  kern<<<grid, NUM_THREADS, smem_total, s>>>(tq, tk, tv, (T*)out, scale, (int)bh, n, 2u, variant, tmask);
   if (trace) {
     cudaStreamSynchronize(s);
     unsigned long long* host = (unsigned long long*)malloc(trace_n * 8);
@@ -927,16 +961,31 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
   return cudaGetLastError();
 }
 
+bool tc_flash_mask_supported(int tile_rows, int tile_cols) {
+  return tile_rows > 0 && tile_cols > 0 && tile_rows % 32 == 0 && tile_cols % 32 == 0;
+}
+
 cudaError_t launch_flash_tc(const void* q, const void* k, const void* v, void* out, float scale, int gs, int dtype,
-                            int64_t bh, int n, int d, cudaStream_t s) {
+                            int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows, int tile_cols,
+                            cudaStream_t s) {
   if (!tc_flash_supported(gs, dtype, n, d)) return cudaErrorNotSupported;
+  if (tile_keep && !tc_flash_mask_supported(tile_rows, tile_cols)) return cudaErrorNotSupported;
   if (bh == 0) return cudaSuccess;
+  TileMask m{tile_keep, tile_keep ? tile_rows : 1, tile_keep ? tile_cols : 1,
+             tile_keep ? (n + tile_cols - 1) / tile_cols : 1};
+  const bool bf = dtype == DFSS_BF16, masked = tile_keep != nullptr;
   if (gs == 2) {
-    if (dtype == DFSS_BF16) return flash_launch_typed<__nv_bfloat16, true>(q, k, v, out, scale, bh, n, s);
-    return flash_launch_typed<__half, true>(q, k, v, out, scale, bh, n, s);
+    if (masked)
+      return bf ? flash_launch_typed<__nv_bfloat16, true, true>(q, k, v, out, scale, bh, n, m, s)
+                : flash_launch_typed<__half, true, true>(q, k, v, out, scale, bh, n, m, s);
+    return bf ? flash_launch_typed<__nv_bfloat16, true, false>(q, k, v, out, scale, bh, n, m, s)
+              : flash_launch_typed<__half, true, false>(q, k, v, out, scale, bh, n, m, s);
   }
-  if (dtype == DFSS_BF16) return flash_launch_typed<__nv_bfloat16, false>(q, k, v, out, scale, bh, n, s);
-  return flash_launch_typed<__half, false>(q, k, v, out, scale, bh, n, s);
+  if (masked)
+    return bf ? flash_launch_typed<__nv_bfloat16, false, true>(q, k, v, out, scale, bh, n, m, s)
+              : flash_launch_typed<__half, false, true>(q, k, v, out, scale, bh, n, m, s);
+  return bf ? flash_launch_typed<__nv_bfloat16, false, false>(q, k, v, out, scale, bh, n, m, s)
+            : flash_launch_typed<__half, false, false>(q, k, v, out, scale, bh, n, m, s);
 }
 
 }  // namespace dfss

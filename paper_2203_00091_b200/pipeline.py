@@ -26,11 +26,29 @@ def workspace_bytes(mode, dtype: torch.dtype, bh: int, n: int, d: int) -> int:
     return int(_lib.load().dfss_nm_attention_workspace_bytes(mode.group_size, _lib.dtype_id(dtype), bh, n, d))
 
 
+def _check_block_mask(block_mask: BlockMask, n: int, mode: SparsityMode) -> None:
+    """Reference validation of a BlockMask for an n x n score matrix (fused.py:58-82,
+    sparse_ops.py:25-30): tile columns group-aligned, grid covering, no empty row."""
+    if block_mask.tile_cols % mode.group_size != 0:
+        raise ValueError(
+            f"tile {block_mask.tile_rows}x{block_mask.tile_cols} must have columns divisible by the "
+            f"group size {mode.group_size}"
+        )
+    block_mask.check_covers(n, n)
+    empty = ~block_mask.keep.any(axis=1)
+    if empty.any():
+        row = int(np.flatnonzero(empty)[0]) * block_mask.tile_rows
+        raise ValueError(f"empty row {row}: all tiles masked, softmax undefined")
+
+
 def dfss_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode="2:4", *, math_mode: str = "auto",
-                   out: torch.Tensor | None = None, workspace: torch.Tensor | None = None) -> torch.Tensor:
+                   block_mask: BlockMask | None = None, out: torch.Tensor | None = None,
+                   workspace: torch.Tensor | None = None) -> torch.Tensor:
     """softmax_N:M(Q K^T / sqrt d) V for [..., n, d] q/k/v on one CUDA device.
 
-    One C-ABI call (dfss_nm_attention); no dense n x n tensor is allocated.
+    One C-ABI call (dfss_nm_attention / dfss_nm_attention_masked); no dense n x n tensor is
+    allocated.  ``block_mask`` (shared by every batch / head) makes masked tiles structurally
+    absent, as in the reference's fused path (fused.py:73-82).
     """
     mode = as_mode(mode)
     if q.shape != k.shape or q.shape != v.shape:
@@ -53,9 +71,17 @@ def dfss_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode="2:4"
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
     lib = _lib.load()
-    _lib.check(lib.dfss_nm_attention(_lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(out), mode.group_size,
-                                     _lib.dtype_id(q.dtype), _MATH[math_mode], bh, n, d, _lib.ptr(workspace), need,
-                                     _lib.stream_of(q)), "nm_attention")
+    if block_mask is None:
+        _lib.check(lib.dfss_nm_attention(_lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(out), mode.group_size,
+                                         _lib.dtype_id(q.dtype), _MATH[math_mode], bh, n, d, _lib.ptr(workspace),
+                                         need, _lib.stream_of(q)), "nm_attention")
+        return out
+    _check_block_mask(block_mask, n, mode)
+    keep = block_mask.device_keep(q.device)
+    _lib.check(lib.dfss_nm_attention_masked(_lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(out), mode.group_size,
+                                            _lib.dtype_id(q.dtype), _MATH[math_mode], bh, n, d, _lib.ptr(keep),
+                                            block_mask.tile_rows, block_mask.tile_cols, _lib.ptr(workspace), need,
+                                            _lib.stream_of(q)), "nm_attention")
     return out
 
 
@@ -63,10 +89,13 @@ def nm_attention(inputs: AttentionInputs, mode: SparsityMode, block_mask: BlockM
                  tile_rows: int = 32, tile_cols: int = 64) -> DenseMatrix:
     """Drop-in sparse attention: fused prune -> sparse softmax -> SpMM (pipeline.py:15-32)."""
     mode = as_mode(mode)
-    if block_mask is None:
-        return DenseMatrix(dfss_attention(inputs.q.data, inputs.k.data, inputs.v.data, mode), check_finite=False)
-    compressed, _ = attention_sddmm(inputs.q, inputs.k, mode, block_mask, tile_rows=tile_rows, tile_cols=tile_cols)
-    return spmm(softmax_rows(compressed, check=False), inputs.v)
+    if block_mask is not None and (block_mask.tile_rows, block_mask.tile_cols) != (tile_rows, tile_cols):
+        raise ValueError(
+            f"block mask tiles {block_mask.tile_rows}x{block_mask.tile_cols} "
+            f"do not match the fused tiling {tile_rows}x{tile_cols}"
+        )
+    out = dfss_attention(inputs.q.data, inputs.k.data, inputs.v.data, mode, block_mask=block_mask)
+    return DenseMatrix(out, check_finite=False)
 
 
 @dataclass(frozen=True)

@@ -451,6 +451,56 @@ def test_block_masked_pipeline_matches_staged_oracle():
     assert_close(out, want, 1e-5, 1e-5, "masked pipeline")
 
 
+def _masked_oracle(q64, k64, v64, mask, mode):
+    """Reference nm_attention with a block mask (fused.py:73-82, sparse_ops.py:18-68) on one head."""
+    n, d = q64.shape
+    scores = ref.gemm_scaled(q64, k64, 1.0 / math.sqrt(d))
+    nz, meta = ref.compress_logical(scores, mode)
+    present = mask.nonzero_keep(n, n)
+    p = oracle_c.softmax_nonzeros(nz, present)
+    cols = ref.nonzero_columns(meta, n, n, mode)
+    return oracle_c.spmm_gather(p, cols, v64, present)
+
+
+@pytest.mark.parametrize("n,tiles,mode,dtype", [
+    (512, (32, 64), "2:4", torch.bfloat16),   # two-set fused kernel, reference default tiling
+    (512, (64, 128), "1:2", torch.float16),   # two-set, coarser tiles, 1:2
+    (384, (32, 32), "2:4", torch.float16),    # one-set fused kernel (n % 256 != 0)
+    (256, (16, 64), "2:4", torch.bfloat16),   # tile rows not 32-aligned: staged kernels
+])
+def test_block_masked_attention_matches_reference(n, tiles, mode, dtype):
+    """BlockMask on the fast path: masked tiles structurally absent, softmax over the present
+    kept entries, per head; includes row blocks whose first key tiles are masked."""
+    rng = np.random.default_rng(n)
+    tr, tc_ = tiles
+    keep = rng.random((-(-n // tr), -(-n // tc_))) < 0.55
+    keep[:, 0] = False          # first key tile masked everywhere: the shift starts at -inf
+    keep[np.arange(keep.shape[0]), rng.integers(1, keep.shape[1], keep.shape[0])] = True  # no empty row
+    mask = dfss.BlockMask(keep, tile_rows=tr, tile_cols=tc_)
+    (q, k, v), (q64, k64, v64) = seeded_qkv((1, 2, n, 64), dtype, seed=7)
+    out = _np(dfss.dfss_attention(q, k, v, mode, block_mask=mask))
+    for h in range(2):
+        want = _masked_oracle(q64[0, h], k64[0, h], v64[0, h], mask, mode)
+        assert_close(out[0, h], want, 2e-2, 2e-2, f"masked {mode} n={n} tiles={tiles} head {h}")
+    # nm_attention with the reference signature routes to the same path
+    got = _np(dfss.nm_attention(dfss.AttentionInputs(q[0, 0], k[0, 0], v[0, 0]), mode, mask, tile_rows=tr,
+                                tile_cols=tc_).data)
+    assert_close(got, out[0, 0], 1e-6, 1e-6, "nm_attention(block_mask) == dfss_attention(block_mask)")
+
+
+def test_block_mask_empty_row_and_tiling_errors():
+    (q, k, v), _ = seeded_qkv((1, 1, 256, 64), torch.bfloat16, seed=2)
+    keep = np.ones((8, 4), dtype=bool)
+    keep[3] = False
+    with pytest.raises(ValueError, match="empty row 96"):
+        dfss.dfss_attention(q, k, v, "2:4", block_mask=dfss.BlockMask(keep, 32, 64))
+    with pytest.raises(ValueError, match="does not match"):
+        dfss.dfss_attention(q, k, v, "2:4", block_mask=dfss.BlockMask(np.ones((4, 4), dtype=bool), 32, 64))
+    with pytest.raises(ValueError, match="fused tiling"):
+        dfss.nm_attention(dfss.AttentionInputs(q[0, 0], k[0, 0], v[0, 0]), "2:4",
+                          dfss.BlockMask(np.ones((8, 4), dtype=bool), 32, 64), tile_rows=32, tile_cols=32)
+
+
 def test_module_and_value_envelope():
     mod = dfss.DFSSAttention("2:4")
     q, k, v = (torch.randn(2, 4, 256, 64, device="cuda", dtype=torch.bfloat16) for _ in range(3))

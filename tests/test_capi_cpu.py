@@ -111,3 +111,37 @@ def test_product_never_imports_the_oracle():
         for f in files:
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 assert not pat.search(open(os.path.join(dirpath, f)).read()), f
+
+
+def test_container_header_validation_and_nibble_packing():
+    """NMCS parsing rejects malformed headers before touching the GPU (container.py:74-92);
+    nibble packing is the reference's (low nibble first, zero pad)."""
+    import struct
+
+    import numpy as np
+
+    from conftest import golden
+    from paper_2203_00091_b200 import container
+
+    g = golden("container.npz")
+    raw = g["nmcs_24"].tobytes()
+    with pytest.raises(ValueError, match="truncated"):
+        container.from_bytes(raw[:10])
+    with pytest.raises(ValueError, match="bad magic"):
+        container.from_bytes(b"XXXX" + raw[4:])
+    with pytest.raises(ValueError, match="unsupported container version"):
+        container.from_bytes(raw[:4] + bytes([2]) + raw[5:])
+    with pytest.raises(ValueError, match="unknown mode code"):
+        container.from_bytes(raw[:5] + bytes([7]) + raw[6:])
+    with pytest.raises(ValueError, match="container size"):
+        container.from_bytes(raw + b"\0")
+    magic, version, mode, layout, rows, cols = struct.unpack_from("<4sBBBII", raw)
+    assert (magic, version, mode, layout, rows, cols) == (b"NMCS", 1, 2, 0, 33, 64)
+    nib = np.array([4, 8, 9, 0xC, 0xD], dtype=np.uint8)
+    packed = container.pack_nibbles(nib)
+    assert packed == bytes([0x84, 0xC9, 0x0D])
+    assert (container.unpack_nibbles(packed, 5) == nib).all()
+    # the golden file's nibble section is exactly the reference packing of its own stream
+    nz_end = 15 + 8 * rows * cols // 2
+    stream = container.unpack_nibbles(raw[nz_end:], rows * cols // 4)
+    assert container.pack_nibbles(stream) == raw[nz_end:]

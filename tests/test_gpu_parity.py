@@ -501,6 +501,28 @@ def test_block_mask_empty_row_and_tiling_errors():
                           dfss.BlockMask(np.ones((8, 4), dtype=bool), 32, 64), tile_rows=32, tile_cols=32)
 
 
+@pytest.mark.parametrize("name,mode", [("12", "1:2"), ("24", "2:4")])
+def test_container_export_import_bytewise_vs_reference(name, mode, tmp_path):
+    """GPU CompressedSparse -> NMCS bytes identical to the reference's to_bytes on the same
+    scores (tests/golden/make_container_golden.py); import of the reference file round-trips."""
+    g = golden("container.npz")
+    scores = torch.from_numpy(g[f"scores_{name}"].astype(np.float32)).cuda()
+    want = g[f"nmcs_{name}"].tobytes()
+    c = dfss.compress_logical(scores, mode)
+    assert dfss.to_bytes(c) == want
+    path = tmp_path / "m.nmcs"
+    assert dfss.write_container(c, path) == len(want)
+    back = dfss.read_container(path)
+    assert torch.equal(back.metadata, c.metadata)
+    assert torch.equal(back.nonzeros, c.nonzeros)
+    assert dfss.to_bytes(back) == want
+    # batched export: one slice per container
+    cb = dfss.compress_logical(torch.stack([scores, scores]), mode)
+    assert dfss.to_bytes(cb, index=1) == want
+    with pytest.raises(ValueError, match="index"):
+        dfss.to_bytes(cb)
+
+
 def test_module_and_value_envelope():
     mod = dfss.DFSSAttention("2:4")
     q, k, v = (torch.randn(2, 4, 256, 64, device="cuda", dtype=torch.bfloat16) for _ in range(3))

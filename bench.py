@@ -42,6 +42,17 @@ CONFIGS = {
     "c4": dict(batch=8, heads=12, seq=4096, d=64, mode="2:4", dtype="bfloat16",
                desc="Long-sequence DFSS 2:4 bf16 attention, batch 8, 12 heads, seq 4096, head_dim 64"),
 }
+# configs[4]: the sequence sweep, batch 8 x 12 heads (SURVEY §8(d) proposal), reported in the
+# default line's "sweep" object (the fp32 1:2 arm runs the exact-FP32 staged kernels: there
+# is no tf32 tensor-core path yet)
+for _n in (384, 512, 768, 1024, 2048, 4096):
+    CONFIGS[f"c5_24_{_n}"] = dict(batch=8, heads=12, seq=_n, d=64, mode="2:4", dtype="bfloat16",
+                                  desc=f"sweep 2:4 bf16, batch 8, 12 heads, seq {_n}")
+    CONFIGS[f"c5_12_{_n}"] = dict(batch=8, heads=12, seq=_n, d=64, mode="1:2", dtype="bfloat16",
+                                  desc=f"sweep 1:2 bf16, batch 8, 12 heads, seq {_n}")
+    if _n <= 1024:
+        CONFIGS[f"c5_12f32_{_n}"] = dict(batch=8, heads=12, seq=_n, d=64, mode="1:2", dtype="float32",
+                                         desc=f"sweep 1:2 fp32 (exact FFMA), batch 8, 12 heads, seq {_n}")
 DT = {"float32": torch.float32, "bfloat16": torch.bfloat16, "float16": torch.float16}
 METRIC = "DFSS attention ms & speedup vs dense attention (seq 512–4096) on B200; TFLOPS"
 UNIT = "TFLOP/s (dense-equivalent 4*n^2*d per head)"
@@ -160,7 +171,7 @@ def algorithmic_bytes(cfg, fused=False):
     }
 
 
-def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True):
+def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True, info=True):
     import paper_2203_00091_b200 as dfss
 
     cfg = CONFIGS[cfg_name]
@@ -213,10 +224,12 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True):
     # ---- per-kernel breakdown on the same stream (the kernels dfss_attention launches)
     scale = 1.0 / math.sqrt(d)
     holder = {}
-    tc16 = cfg["mode"] == "2:4" and cfg["dtype"] != "float32" and d == 64 and n % 128 == 0
+    tc16 = cfg["dtype"] != "float32" and d == 64 and n % 128 == 0  # the fused kernel (2:4 and 1:2)
+
+    staged_tc = tc16 and cfg["mode"] == "2:4"  # the staged tcgen05 kernels are 2:4-only
 
     def k_sddmm():
-        holder["c"], _ = dfss.sddmm_prune(q, k, mode, scale, with_row_max=tc16)
+        holder["c"], _ = dfss.sddmm_prune(q, k, mode, scale, with_row_max=staged_tc)
 
     def k_softmax():
         holder["p"] = dfss.softmax_rows(holder["c"], check=False)
@@ -227,7 +240,8 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True):
     def k_spmm_softmax():
         dfss.spmm_softmax(holder["c"], v)
 
-    k_sddmm(); k_softmax(); k_spmm()
+    if info or not tc16:
+        k_sddmm(); k_softmax(); k_spmm()
     torch.cuda.synchronize()
     hbm_peak, tf_peak, peak_src = peaks()
     kt_info = {}
@@ -236,6 +250,8 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True):
         kt = {"flash": ms_per_step}
         for name, fn in (("sddmm_rowmax", k_sddmm), ("spmm_softmax", k_spmm_softmax), ("softmax_rows", k_softmax),
                          ("spmm", k_spmm)):
+            if not (info and staged_tc):
+                break
             kt_info[name] = float(np.mean(time_steps(fn, max(3, args.steps), 2, flush)))
         flops = 3.0 * n * n * d  # QK^T (2n^2d) + kept-half PV (n^2d), SURVEY §8(d)
         achieved = flops * bh / (ms_per_step * 1e-3) / 1e12
@@ -382,6 +398,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["dfss", "reference"], default="dfss")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the configs[4] sequence sweep")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for the CPU baseline")
     ap.add_argument("--no-extra", action="store_true", help="skip sweep / e2e / cpu baseline (profiling runs)")
     args = ap.parse_args()
@@ -463,6 +480,16 @@ def main():
                 except Exception as ex:
                     sweep[name] = {"error": str(ex)[:200]}
             extra["other_configs"] = sweep
+            if not args.no_sweep:
+                sw = {}
+                for name in sorted((c for c in CONFIGS if c.startswith("c5_")), key=lambda c: (c.split("_")[1], int(c.split("_")[2]))):
+                    try:
+                        r2, _ = run_dfss(argparse.Namespace(steps=5, warmup=3), name, 1, 0, 0, device, info=False)
+                        sw[name] = {"ms": round(r2["ms_per_step"], 4), "tflops": round(r2["value"], 1),
+                                    "speedup_vs_dense": r2["speedup_vs_dense"], "path": r2["path"].split(":")[0]}
+                    except Exception as ex:
+                        sw[name] = {"error": str(ex)[:200]}
+                extra["sweep"] = sw
 
     if rank == 0:
         line = {

@@ -201,4 +201,10 @@ cudaError_t launch_flash_tc(const void* q, const void* k, const void* v, void* o
                             int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows, int tile_cols,
                             cudaStream_t s);
 bool tc_spmm_supported(int gs, int p_dtype, int v_dtype, int out_dtype, int rows, int n_k, int d);
+// fused 1:2 attention on fp32 inputs with tf32 tensor cores (flash_tf32.cu), n % 256 == 0, d = 64
+bool tc_flash_tf32_supported(int gs, int n, int d);
+// vt_scratch: bh * n * 64 floats of device scratch (V^T; the kind::tf32 B operand must be K-major)
+cudaError_t launch_flash_tf32(const void* q, const void* k, const void* v, void* out, float scale, int64_t bh, int n,
+                              int d, const uint8_t* tile_keep, int tile_rows, int tile_cols, void* vt_scratch,
+                              cudaStream_t s);
 }  // namespace dfss

@@ -47,8 +47,7 @@
 
 #include <type_traits>
 
-#include "dfss_common.cuh"
-#include "tc_common.cuh"
+#include "flash_common.cuh"
 
 namespace dfss {
 
@@ -82,88 +81,6 @@ constexpr int TM_E = TM_O + 2 * HD;  // PST x 4 metadata columns
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kSumLimit = 256.0f;  // a quarter-tile partial sum above 2^8 triggers a shift update
 }  // namespace
-
-// ---------------------------------------------------------------- packed fp32 helpers (sm_100 FADD2/FFMA2)
-__device__ __forceinline__ void sub2(float a0, float a1, float b0, float b1, float& d0, float& d1) {
-  asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
-      "sub.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
-      : "=f"(d0), "=f"(d1)
-      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
-}
-__device__ __forceinline__ void add2(float a0, float a1, float b0, float b1, float& d0, float& d1) {
-  asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
-      "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
-      : "=f"(d0), "=f"(d1)
-      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
-}
-// (a0, a1) * c + (b, b)
-__device__ __forceinline__ void fma2s(float a0, float a1, float c, float b, float& d0, float& d1) {
-  asm("{\n\t.reg .b64 a, cc, bb, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 cc, {%4, %4};\n\tmov.b64 bb, {%5, %5};\n\t"
-      "fma.rn.f32x2 d, a, cc, bb;\n\tmov.b64 {%0, %1}, d;\n\t}"
-      : "=f"(d0), "=f"(d1)
-      : "f"(a0), "f"(a1), "f"(c), "f"(b));
-}
-
-__device__ __forceinline__ float fex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-template <typename T>
-__device__ __forceinline__ uint32_t fpack2(float lo, float hi) {
-  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-    __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
-    return *reinterpret_cast<uint32_t*>(&p);
-  } else {
-    __half2 p = __floats2half2_rn(lo, hi);
-    return *reinterpret_cast<uint32_t*>(&p);
-  }
-}
-
-// bar.red.or over `count` threads of named barrier `id`: true iff any thread passed true
-__device__ __forceinline__ bool bar_any(uint32_t id, uint32_t count, bool pred) {
-  uint32_t r;
-  asm volatile(
-      "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\tbar.red.or.pred q, %2, %3, p;\n\tselp.u32 %0, 1, 0, q;\n\t}"
-      : "=r"(r)
-      : "r"((uint32_t)pred), "r"(id), "r"(count)
-      : "memory");
-  return r != 0;
-}
-
-// role-warp wait: sleeping try_wait, or spinning with variant bit 10 (experiment)
-__device__ __forceinline__ void wait_role(int variant, uint64_t* bar, uint32_t parity) {
-  if (variant & 1024)
-    tc::mbar_wait(bar, parity);
-  else
-    tc::mbar_wait_sleep(bar, parity);
-}
-
-__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-}
-
-// Optional tile-grid keep mask (BlockMask, codec.py:150-200): keep[i * grid_cols + j] covers
-// rows [i*tile_rows, +tile_rows) and key columns [j*tile_cols, +tile_cols), shared by every
-// (batch, head).  The fused kernels need tile_rows and tile_cols to be multiples of 32, so a
-// warp's 32 rows x 32 columns chunk lies in one tile: masked chunks are skipped warp-uniformly
-// (no prune / exp work, zero P), i.e. masked tiles are structurally absent as in the reference.
-struct TileMask {
-  const uint8_t* keep;
-  int tile_rows, tile_cols, grid_cols;
-  __device__ __forceinline__ bool masked(int row, int col) const {
-    return keep != nullptr && __ldg(keep + (row / tile_rows) * grid_cols + col / tile_cols) == 0;
-  }
-};
-
-// masked chunk: no kept values, P = 0, nibble 0x4 in every group (W = 0x44444444)
-__device__ __forceinline__ void masked_chunk(uint32_t (&pk)[8], uint32_t& W, float& lt0, float& lt1) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j) pk[j] = 0u;
-  W = 0x44444444u;
-  lt0 = lt1 = 0.f;
-}
 
 // One quarter-tile of one row: 8 groups of 4 scores s[] in (v0, v2, v1, v3) register order.
 // Prunes 2:4 (reference rule), exponentiates the kept half against the shift `mlog`

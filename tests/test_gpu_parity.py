@@ -523,6 +523,48 @@ def test_container_export_import_bytewise_vs_reference(name, mode, tmp_path):
         dfss.to_bytes(cb)
 
 
+def _tf32(x: np.ndarray) -> np.ndarray:
+    """The operand the tf32 tensor core multiplies: fp32 with the low 13 mantissa bits dropped."""
+    return (x.astype(np.float32).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("n", [256, 512, 1024])
+def test_tf32_12_fused_attention(n):
+    """configs[4] "1:2 tf32": fp32 inputs, tf32 tensor cores, fused 1:2 kernel.  Checked like the
+    16-bit paths: the reference nm_attention in float64 on the operands the hardware multiplies
+    (tf32-truncated Q, K, V), at the 16-bit bar 2e-2; and within 5e-2 of the exact-FP32 pipeline
+    (pairs whose scores differ by less than the tf32 rounding may keep the other element)."""
+    (q, k, v), (q64, k64, v64) = seeded_qkv((1, 3, n, 64), torch.float32, seed=n + 1)
+    out = _np(dfss.dfss_attention(q, k, v, "1:2", math_mode="tf32"))
+    want = oracle_attention(_tf32(q64), _tf32(k64), _tf32(v64), "1:2")
+    assert_close(out, want, 2e-2, 2e-2, f"tf32 1:2 n={n}")
+    exact = _np(dfss.dfss_attention(q, k, v, "1:2", math_mode="ffma"))
+    assert np.abs(out - exact).max() < 5e-2
+
+
+def test_tf32_12_masked_and_shift_path():
+    g = torch.Generator().manual_seed(31)
+    n = 512
+    q = torch.randn((1, 2, n, 64), generator=g)
+    k = torch.randn((1, 2, n, 64), generator=g) * torch.linspace(0.2, 3.0, n).view(1, 1, n, 1)
+    v = torch.randn((1, 2, n, 64), generator=g)
+    q, k, v = (x.cuda() for x in (q, k, v))
+    out = _np(dfss.dfss_attention(q, k, v, "1:2", math_mode="tf32"))
+    want = oracle_attention(*(_tf32(x.cpu().numpy()) for x in (q, k, v)), "1:2")
+    assert_close(out, want, 2e-2, 2e-2, "tf32 growing scores")
+    rng = np.random.default_rng(4)
+    keep = rng.random((n // 32, n // 64)) < 0.6
+    keep[:, 0] = False
+    keep[np.arange(keep.shape[0]), rng.integers(1, keep.shape[1], keep.shape[0])] = True
+    mask = dfss.BlockMask(keep, 32, 64)
+    out = _np(dfss.dfss_attention(q, k, v, "1:2", math_mode="tf32", block_mask=mask))
+    qq, kk, vv = (_tf32(x.cpu().numpy()) for x in (q, k, v))
+    for h in range(2):
+        assert_close(out[0, h], _masked_oracle(qq[0, h], kk[0, h], vv[0, h], mask, "1:2"), 2e-2, 2e-2, "tf32 masked")
+    with pytest.raises(RuntimeError, match="tf32 attention needs"):
+        dfss.dfss_attention(q, k, v, "2:4", math_mode="tf32")
+
+
 def test_module_and_value_envelope():
     mod = dfss.DFSSAttention("2:4")
     q, k, v = (torch.randn(2, 4, 256, 64, device="cuda", dtype=torch.bfloat16) for _ in range(3))

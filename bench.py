@@ -43,13 +43,16 @@ CONFIGS = {
                desc="Long-sequence DFSS 2:4 bf16 attention, batch 8, 12 heads, seq 4096, head_dim 64"),
 }
 # configs[4]: the sequence sweep, batch 8 x 12 heads (SURVEY §8(d) proposal), reported in the
-# default line's "sweep" object (the fp32 1:2 arm runs the exact-FP32 staged kernels: there
-# is no tf32 tensor-core path yet)
+# default line's "sweep" object: 2:4 bf16 and 1:2 bf16 (fused kernel), 1:2 tf32 (fused tf32
+# kernel, n % 256 == 0) and, for reference, 1:2 exact FP32 (staged FFMA kernels)
 for _n in (384, 512, 768, 1024, 2048, 4096):
     CONFIGS[f"c5_24_{_n}"] = dict(batch=8, heads=12, seq=_n, d=64, mode="2:4", dtype="bfloat16",
                                   desc=f"sweep 2:4 bf16, batch 8, 12 heads, seq {_n}")
     CONFIGS[f"c5_12_{_n}"] = dict(batch=8, heads=12, seq=_n, d=64, mode="1:2", dtype="bfloat16",
                                   desc=f"sweep 1:2 bf16, batch 8, 12 heads, seq {_n}")
+    if _n % 256 == 0:
+        CONFIGS[f"c5_12tf32_{_n}"] = dict(batch=8, heads=12, seq=_n, d=64, mode="1:2", dtype="float32", math="tf32",
+                                          desc=f"sweep 1:2 tf32 (fp32 inputs), batch 8, 12 heads, seq {_n}")
     if _n <= 1024:
         CONFIGS[f"c5_12f32_{_n}"] = dict(batch=8, heads=12, seq=_n, d=64, mode="1:2", dtype="float32",
                                          desc=f"sweep 1:2 fp32 (exact FFMA), batch 8, 12 heads, seq {_n}")
@@ -183,14 +186,15 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True, info=Tr
     q, k, v = qkv[0], qkv[1], qkv[2]
     bh = hi - lo
     mode = dfss.SparsityMode.parse(cfg["mode"])
-    ws_bytes = dfss.workspace_bytes(mode, q.dtype, bh, n, d)
+    math_mode = cfg.get("math", "auto")
+    ws_bytes = dfss.workspace_bytes(mode, q.dtype, bh, n, d, math_mode)
     workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
     out = torch.empty_like(q)
     flush_buf = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
     flush = lambda: flush_buf.fill_(1)
 
     def step():
-        dfss.dfss_attention(q, k, v, mode, out=out, workspace=workspace)
+        dfss.dfss_attention(q, k, v, mode, math_mode=math_mode, out=out, workspace=workspace)
 
     # ---- timed region: barrier + synchronize on both sides, max over ranks
     if ws > 1:
@@ -224,7 +228,8 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True, info=Tr
     # ---- per-kernel breakdown on the same stream (the kernels dfss_attention launches)
     scale = 1.0 / math.sqrt(d)
     holder = {}
-    tc16 = cfg["dtype"] != "float32" and d == 64 and n % 128 == 0  # the fused kernel (2:4 and 1:2)
+    tc16 = ((cfg["dtype"] != "float32" and n % 128 == 0) or (cfg.get("math") == "tf32" and n % 256 == 0)) and d == 64
+    # ^ a fused kernel runs (16-bit 2:4 / 1:2, or tf32 1:2)
 
     staged_tc = tc16 and cfg["mode"] == "2:4"  # the staged tcgen05 kernels are 2:4-only
 

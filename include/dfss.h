@@ -137,6 +137,11 @@ int dfss_spmm(const void* p, const uint32_t* meta_hw, const void* v, void* out, 
  *   max, softmax-fused SpMM); everything else runs SDDMM -> softmax -> SpMM.
  */
 int64_t dfss_nm_attention_workspace_bytes(int mode, int dtype, int64_t bh, int n, int d);
+/* Exact workspace for the path dfss_nm_attention(_masked) will take with these arguments:
+ * 0 for the fused 16-bit kernel, bh*n*d*4 (V^T) for the fused tf32 kernel, the staged
+ * bytes above otherwise.  masked != 0 when a tile_keep grid will be passed. */
+int64_t dfss_nm_attention_workspace_bytes_for(int mode, int dtype, int math, int64_t bh, int n, int d,
+                                              int tile_rows, int tile_cols, int masked);
 int dfss_nm_attention(const void* q, const void* k, const void* v, void* out, int mode, int dtype, int math,
                       int64_t bh, int n, int d, void* workspace, int64_t workspace_bytes, void* stream);
 

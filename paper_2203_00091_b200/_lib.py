@@ -37,6 +37,7 @@ SIGNATURES = {
     "dfss_spmm": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i64, _i32, _i32, _i32, _vp, _i32, _i32, _vp,
                          _vp]),
     "dfss_nm_attention_workspace_bytes": (_i64, [_i32, _i32, _i64, _i32, _i32]),
+    "dfss_nm_attention_workspace_bytes_for": (_i64, [_i32, _i32, _i32, _i64, _i32, _i32, _i32, _i32, _i32]),
     "dfss_nm_attention": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i64, _i32, _i32, _vp, _i64, _vp]),
     "dfss_nm_attention_masked": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i64, _i32, _i32, _vp, _i32, _i32, _vp,
                                         _i64, _vp]),

@@ -125,6 +125,19 @@ int dfss_spmm(const void* p, const uint32_t* meta_hw, const void* v, void* out, 
                                             tile_keep, tile_rows, tile_cols, s));
 }
 
+int64_t dfss_nm_attention_workspace_bytes_for(int mode, int dtype, int math, int64_t bh, int n, int d,
+                                              int tile_rows, int tile_cols, int masked) {
+  if (!valid_mode(mode) || !valid_dtype(dtype) || bh < 0 || n < 1 || d < 1) return -1;
+  const bool mask_ok = !masked || dfss::tc_flash_mask_supported(tile_rows, tile_cols);
+  if (math == DFSS_MATH_AUTO && dtype != DFSS_F32 && dfss::tc_flash_supported(mode, dtype, n, d) && mask_ok &&
+      dfss_has_tcgen05())
+    return 0;  // fused kernel: no intermediate in HBM
+  if (math == DFSS_MATH_TF32 && dtype == DFSS_F32 && dfss::tc_flash_tf32_supported(mode, n, d) && mask_ok &&
+      dfss_has_tcgen05())
+    return (bh * (int64_t)n * d * 4 + 255) / 256 * 256;  // V^T for the K-major tf32 B operand
+  return dfss_nm_attention_workspace_bytes(mode, dtype, bh, n, d);
+}
+
 int64_t dfss_nm_attention_workspace_bytes(int mode, int dtype, int64_t bh, int n, int d) {
   (void)d;
   if (!valid_mode(mode) || !valid_dtype(dtype) || bh < 0 || n < 1) return -1;
@@ -147,8 +160,9 @@ int dfss_nm_attention_masked(const void* q, const void* k, const void* v, void* 
   if (bh < 0 || n < 1 || d < 1) return fail(DFSS_ERR_INVALID, "shape dimensions must be positive");
   if (n % mode != 0) return fail(DFSS_ERR_INVALID, "sequence length not group-aligned for the mode");
   if (int st = check_keep(tile_keep, tile_rows, tile_cols, mode)) return st;
-  const int64_t need = dfss_nm_attention_workspace_bytes(mode, dtype, bh, n, d);
-  if (!workspace || workspace_bytes < need) return fail(DFSS_ERR_INVALID, "workspace too small");
+  const int64_t need =
+      dfss_nm_attention_workspace_bytes_for(mode, dtype, math, bh, n, d, tile_rows, tile_cols, tile_keep != nullptr);
+  if (need > 0 && (!workspace || workspace_bytes < need)) return fail(DFSS_ERR_INVALID, "workspace too small");
   if (bh == 0) return DFSS_OK;
   const int64_t nz_bytes = bh * (int64_t)n * (n / 2) * dfss::dtype_bytes(dtype);
   const int64_t meta_bytes = dfss_meta_hw_words(mode, bh, n, n) * 4;

@@ -20,10 +20,15 @@ from .fused import _MATH, attention_sddmm
 from .sparse_ops import softmax_rows, spmm
 
 
-def workspace_bytes(mode, dtype: torch.dtype, bh: int, n: int, d: int) -> int:
-    """Device scratch for the compressed P and metadata of one dfss_attention call."""
+def workspace_bytes(mode, dtype: torch.dtype, bh: int, n: int, d: int, math_mode: str = "auto",
+                    block_mask: BlockMask | None = None) -> int:
+    """Device scratch one dfss_attention call needs on the path it will take: 0 for the fused
+    16-bit kernel, V^T for the fused tf32 kernel, the compressed P + metadata when staged."""
     mode = as_mode(mode)
-    return int(_lib.load().dfss_nm_attention_workspace_bytes(mode.group_size, _lib.dtype_id(dtype), bh, n, d))
+    tr, tc_ = (block_mask.tile_rows, block_mask.tile_cols) if block_mask is not None else (0, 0)
+    return int(_lib.load().dfss_nm_attention_workspace_bytes_for(mode.group_size, _lib.dtype_id(dtype),
+                                                                 _MATH[math_mode], bh, n, d, tr, tc_,
+                                                                 int(block_mask is not None)))
 
 
 def _check_block_mask(block_mask: BlockMask, n: int, mode: SparsityMode) -> None:
@@ -67,8 +72,8 @@ def dfss_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode="2:4"
     bh = int(np.prod(q.shape[:-2], dtype=np.int64)) if q.dim() > 2 else 1
     if out is None:
         out = torch.empty_like(q)
-    need = workspace_bytes(mode, q.dtype, bh, n, d)
-    if workspace is None or workspace.numel() < need:
+    need = workspace_bytes(mode, q.dtype, bh, n, d, math_mode, block_mask)
+    if need and (workspace is None or workspace.numel() < need):
         workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
     lib = _lib.load()
     if block_mask is None:

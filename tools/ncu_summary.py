@@ -102,8 +102,9 @@ def main(tag: str) -> None:
             continue
         kname = re.sub(r"\(.*", "", m["kernel"]).replace("void ", "")
         dram = m.get("dram_read", 0) + m.get("dram_write", 0)
-        key = ("flash" if "flash" in kname else "sddmm" if "sddmm" in kname else "softmax" if "softmax" in kname
-               else "spmm")
+        suffix = base.split("_")[-1]
+        key = (suffix if suffix.startswith("flash") and suffix != "flash" else "flash" if "flash" in kname
+               else "sddmm" if "sddmm" in kname else "softmax" if "softmax" in kname else "spmm")
         traffic.setdefault(cfg, {})[key] = int(dram)
         lines += [f"## `{kname}` — {cfg} (`{base}.ncu-rep`)", "",
                   f"- duration {m.get('duration', 0) * 1e6:.1f} µs at SM clock {m.get('sm_clock', 0) / 1e9:.2f} GHz",

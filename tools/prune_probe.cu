@@ -44,9 +44,9 @@ __global__ void __launch_bounds__(640, 1) k(int iters, uint32_t* out, long long*
       const float v3 = __uint_as_float(s[4 * g + 3]);
       float d01, d23;
       sub2(v0, v2, v1, v3, d01, d23);
-      if (MODE != 3 && MODE != 11) add2(d01, d23, 0.f, 0.f, d01, d23);
+      if (MODE != 3 && MODE != 11 && MODE != 14) add2(d01, d23, 0.f, 0.f, d01, d23);
       uint32_t a, b;
-      if (MODE == 9 || MODE == 11) {
+      if (MODE == 9 || MODE == 11 || MODE == 14) {
         a = 0u;
         b = 0u;
       } else if (MODE == 1 || MODE == 3) {  // sign bits on the ALU pipe (SHF)
@@ -68,6 +68,13 @@ __global__ void __launch_bounds__(640, 1) k(int iters, uint32_t* out, long long*
       int nib = (int)(MODE == 2 ? (a | b) : (a + 4u * b));
       if (MODE != 7 && (MODE < 8 || MODE >= 12)) {
         nib = keep23 ? 6 : nib;
+        nib = keep01 ? -4 : nib;
+      }
+      if (MODE == 14) {
+        const bool pa = v1 > v0, pb = v3 > v2;
+        int m4 = pa ? 1 : 0;
+        m4 = pb ? m4 + 4 : m4;
+        nib = keep23 ? 6 : m4;
         nib = keep01 ? -4 : nib;
       }
       if (MODE == 12 || MODE == 13) {
@@ -131,8 +138,8 @@ int main() {
   const char* names[] = {"IMAD.HI sign bits", "SHF sign bits", "SHF + mask nibble", "SHF, no canon FADD2",
                          "no MUFU", "no F2FP (PRMT)", "no FSEL", "no nibble SEL", "no keep FSETP",
                          "8 + no sign bits", "8 + no FMNMX", "8 + no d FADD2s/sign", "predicated movs",
-                         "predicated nibble movs"};
-  for (int mode = 0; mode < 14; ++mode) {
+                         "predicated nibble movs", "FSETP sign bits"};
+  for (int mode = 0; mode < 15; ++mode) {
     const int warps = 16;
     switch (mode) {
       case 0: k<0><<<148, warps * 32>>>(4096, out, cyc, 0.18f, 0.5f, 2u); break;
@@ -149,6 +156,7 @@ int main() {
       case 11: k<11><<<148, warps * 32>>>(4096, out, cyc, 0.18f, 0.5f, 2u); break;
       case 12: k<12><<<148, warps * 32>>>(4096, out, cyc, 0.18f, 0.5f, 2u); break;
       case 13: k<13><<<148, warps * 32>>>(4096, out, cyc, 0.18f, 0.5f, 2u); break;
+      case 14: k<14><<<148, warps * 32>>>(4096, out, cyc, 0.18f, 0.5f, 2u); break;
     }
     cudaDeviceSynchronize();
     cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);

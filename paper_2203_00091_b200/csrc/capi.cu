@@ -131,7 +131,7 @@ int64_t dfss_nm_attention_workspace_bytes_for(int mode, int dtype, int math, int
   const bool mask_ok = !masked || dfss::tc_flash_mask_supported(tile_rows, tile_cols);
   if (math == DFSS_MATH_AUTO && dtype != DFSS_F32 && dfss::tc_flash_supported(mode, dtype, n, d) && mask_ok &&
       dfss_has_tcgen05())
-    return 0;  // fused kernel: no intermediate in HBM
+    return masked ? dfss::flash_mask_workspace_bytes(n) : 0;  // fused: no intermediate in HBM (mask bitmaps only)
   if (math == DFSS_MATH_TF32 && dtype == DFSS_F32 && dfss::tc_flash_tf32_supported(mode, n, d) && mask_ok &&
       dfss_has_tcgen05())
     return (bh * (int64_t)n * d * 4 + 255) / 256 * 256;  // V^T for the K-major tf32 B operand
@@ -175,7 +175,7 @@ int dfss_nm_attention_masked(const void* q, const void* k, const void* v, void* 
   if (math == DFSS_MATH_AUTO && dtype != DFSS_F32 && dfss::tc_flash_supported(mode, dtype, n, d) &&
       (!tile_keep || dfss::tc_flash_mask_supported(tile_rows, tile_cols)) && dfss_has_tcgen05())
     return cuda_status(dfss::launch_flash_tc(q, k, v, out, scale, mode, dtype, bh, n, d, tile_keep, tile_rows,
-                                             tile_cols, (cudaStream_t)stream));
+                                             tile_cols, workspace, (cudaStream_t)stream));
   // tf32 1:2 on fp32 inputs: the fused tf32 kernel (configs[4] "1:2 tf32")
   if (math == DFSS_MATH_TF32 && dtype == DFSS_F32 && dfss::tc_flash_tf32_supported(mode, n, d) &&
       (!tile_keep || dfss::tc_flash_mask_supported(tile_rows, tile_cols)) && dfss_has_tcgen05())

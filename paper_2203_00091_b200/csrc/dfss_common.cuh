@@ -199,7 +199,9 @@ bool tc_flash_supported(int gs, int dtype, int n, int d);
 bool tc_flash_mask_supported(int tile_rows, int tile_cols);
 cudaError_t launch_flash_tc(const void* q, const void* k, const void* v, void* out, float scale, int gs, int dtype,
                             int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows, int tile_cols,
-                            cudaStream_t s);
+                            void* workspace, cudaStream_t s);
+// workspace of launch_flash_tc with a tile mask (liveness bitmaps); unmasked needs none
+int64_t flash_mask_workspace_bytes(int n);
 bool tc_spmm_supported(int gs, int p_dtype, int v_dtype, int out_dtype, int rows, int n_k, int d);
 // fused 1:2 attention on fp32 inputs with tf32 tensor cores (flash_tf32.cu), n % 256 == 0, d = 64
 bool tc_flash_tf32_supported(int gs, int n, int d);

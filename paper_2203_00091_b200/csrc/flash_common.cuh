@@ -79,8 +79,23 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
 struct TileMask {
   const uint8_t* keep;
   int tile_rows, tile_cols, grid_cols;
+  // bitmaps derived from keep by mask_bits_kernel (flash_tc.cu), in the fused kernels' workspace:
+  // sbits [n/128 row blocks][sbw words], bit t = any kept tile in the 128 x 128 step (rows, t);
+  // cbits [n/32 row strips][cbw words], bit c = 32 x 32 chunk (strip, c) kept
+  const uint32_t* sbits = nullptr;
+  const uint32_t* cbits = nullptr;
+  const int* order = nullptr;  // [n/256] row blocks by live steps, heaviest first (two-set schedule)
+  int sbw = 0, cbw = 0;
   __device__ __forceinline__ bool masked(int row, int col) const {
     return keep != nullptr && __ldg(keep + (row / tile_rows) * grid_cols + col / tile_cols) == 0;
+  }
+  // any kept tile in rows [row0, row0 + rows) x columns [col0, col0 + cols)?
+  __device__ __forceinline__ bool region_live(int row0, int rows, int col0, int cols) const {
+    if (keep == nullptr) return true;
+    for (int i = row0 / tile_rows; i <= (row0 + rows - 1) / tile_rows; ++i)
+      for (int j = col0 / tile_cols; j <= (col0 + cols - 1) / tile_cols; ++j)
+        if (__ldg(keep + i * grid_cols + j)) return true;
+    return false;
   }
 };
 

@@ -467,7 +467,8 @@ constexpr int S2_K = S2_Q + 4 * Q_BYTES;
 constexpr int S2_V = S2_K + K2ST * K_BYTES;
 constexpr int S2_RED = S2_V + V2ST * V_BYTES;  // red_max / red_sum: [2 halves][2 pairs][128] floats each
 constexpr int S2_BAR = S2_RED + 2 * 2 * 2 * BM * 4;
-constexpr int S2_TOTAL = S2_BAR + 512 + 1024;
+constexpr int S2_LIVE = S2_BAR + 512;             // BlockMask step bitmap (masked kernels; sized at launch)
+constexpr int S2_TOTAL = S2_LIVE + 1024;
 constexpr int S2RING = 3;                      // S buffers (TMEM), 128 columns each
 constexpr int T2_O = S2RING * BN;              // O_h at T2_O + 64 h
 static_assert(T2_O + 2 * HD <= 512, "TMEM budget");
@@ -515,6 +516,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int iblocks = n / (2 * BM);
   const int items = bh * iblocks;
   const int ntiles = n / BN;
+  // BlockMask tile skipping: a 128 x 128 step whose mask tiles are all
+  // masked is not computed at all -- no K / V load when both halves are dead, no S MMA, no
+  // softmax work, no PV.  Every role evaluates the same predicate and counts only live steps,
+  // so the S ring / barrier phases stay in lock-step (identical to the dense sequence when
+  // nothing is masked).
+  // Liveness comes from the step bitmap (copied to shared memory below) and, for the softmax
+  // warps, from per-strip chunk words held one per lane: no mask load on any critical path.
+  uint32_t* s_live = (uint32_t*)(smem + S2_LIVE);
+  auto live = [&](int ib, int t, int hh) {
+    return !MASKED || (variant & 8192) || ((s_live[(ib * 2 + hh) * tmask.sbw + (t >> 5)] >> (t & 31)) & 1u);
+  };
+  int* s_order = (int*)(s_live + (n / BM) * tmask.sbw);
+  if (MASKED) {
+    for (int i = threadIdx.x; i < (n / BM) * tmask.sbw; i += blockDim.x) s_live[i] = __ldg(tmask.sbits + i);
+    for (int i = threadIdx.x; i < iblocks; i += blockDim.x) s_order[i] = __ldg(tmask.order + i);
+  }
+  // k-th item of this CTA.  Dense: round robin (item = b * iblocks + ib).  Masked: items cost
+  // their live steps, which depend on the row block only; row blocks are ranked by cost
+  // (mask_order_kernel) and the ranked items dealt out in snake order -- heaviest first,
+  // alternating direction per round -- so CTAs finish together (an all-kept mask reproduces the
+  // dense order).  Every role walks the same sequence.
+  auto item_at = [&](int k) -> int {
+    const int g = gridDim.x;
+    if (!MASKED) {
+      const int i = blockIdx.x + k * g;
+      return i < items ? i : -1;
+    }
+    const int p = k * g + ((k & 1) ? g - 1 - (int)blockIdx.x : (int)blockIdx.x);
+    if (p >= items) return -1;
+    // within a group of equal-cost row blocks keep the dense head-major order (K / V reuse in L2)
+    const int info = s_order[p / bh], r0 = (info >> 8) & 255, m = info >> 16, o = p - r0 * bh;
+    return (o / m) * iblocks + (s_order[r0 + o % m] & 255);
+  };
 
   if (warp == W_QK && lane == 0) {
     tc::prefetch_tmap(&tm_q);
@@ -553,7 +587,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int ks = 0, vs = 0, it = 0;
       uint32_t kph = 0, vph = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      for (int kk_ = 0, item = item_at(0); item >= 0; item = item_at(++kk_), ++it) {
         const int b = item / iblocks, ib = item % iblocks;
         const int qs = it & 1;
         wait_role(variant, &q_empty[qs], ((it >> 1) & 1) ^ 1);
@@ -561,6 +595,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc::tma_load_3d(smem + S2_Q + (2 * qs) * Q_BYTES, &tm_q, &q_full[qs], 0, ib * 2 * BM, b);
         tc::tma_load_3d(smem + S2_Q + (2 * qs + 1) * Q_BYTES, &tm_q, &q_full[qs], 0, ib * 2 * BM + BM, b);
         for (int t = 0; t < ntiles; ++t) {
+          if (MASKED && !live(ib, t, 0) && !live(ib, t, 1)) continue;
           wait_role(variant, &k_empty[ks], kph ^ 1);
           tc::mbar_arrive_expect_tx(&k_full[ks], K_BYTES);
           tc::tma_load_5d(smem + S2_K + ks * K_BYTES, &tm_k, &k_full[ks], 0, 0, 0, t * (BN / 4), b);
@@ -581,15 +616,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       constexpr uint32_t idesc_s = tc::instr_desc(fmt, BM, BN, false, false, false);
       int ks = 0, it = 0, sb = 0;
       uint32_t kph = 0, sph = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      for (int kk_ = 0, item = item_at(0); item >= 0; item = item_at(++kk_), ++it) {
         const int qs = it & 1;
+        const int ib = item % iblocks;
         wait_role(variant, &q_full[qs], (it >> 1) & 1);
         for (int t = 0; t < ntiles; ++t) {
+          const bool lv[2] = {live(ib, t, 0), live(ib, t, 1)};
+          if (MASKED && !lv[0] && !lv[1]) continue;
           wait_role(variant, &k_full[ks], kph);
           if (lane == 0) FTRACE(10, it, t, 0);
           const uint32_t k_addr = tc::smem_u32(smem + S2_K + ks * K_BYTES);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
+            if (MASKED && !lv[h]) continue;
             if (lane == 0) FTRACE(3, it, t, h);
             wait_role(variant, &s_free[sb], sph ^ 1);  // PV of step g - 3 retired
             if (lane == 0) FTRACE(4, it, t, h);
@@ -621,13 +660,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
       constexpr uint32_t idesc_pv = tc::instr_desc(fmt, BM, HD, false, true, true);
       int vs = 0, it = 0;
-      uint32_t vph = 0, gt = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      uint32_t vph = 0, gcount = 0, pbits = 0;  // live steps so far (both halves); p_full phase per slot
+      for (int kk_ = 0, item = item_at(0); item >= 0; item = item_at(++kk_), ++it) {
+        const int ib = item % iblocks;
         wait_role(variant, &o_empty[h], (it & 1) ^ 1);
-        for (int t = 0; t < ntiles; ++t, ++gt) {
-          const uint32_t g = 2 * gt + h, slot = g % S2RING;
+        bool first = true;  // first live step of this half-item initialises O_h
+        for (int t = 0; t < ntiles; ++t) {
+          const bool l0 = live(ib, t, 0), l1 = live(ib, t, 1);
+          if (MASKED && !l0 && !l1) continue;  // tile not loaded
+          const uint32_t g = gcount + (h ? (uint32_t)l0 : 0u), slot = g % S2RING;
+          gcount += (uint32_t)l0 + (uint32_t)l1;
+          if (MASKED && !(h ? l1 : l0)) {  // this half is masked here: release the V stage unused
+            // wait for the load first: arriving early could complete the stage's PREVIOUS phase
+            // while the other half's PV still reads it
+            wait_role(variant, &v_full[vs], vph);
+            if (lane == 0) tc::mbar_arrive(&v_empty[vs]);
+            if (++vs == V2ST) { vs = 0; vph ^= 1; }
+            continue;
+          }
           wait_role(variant, &v_full[vs], vph);
-          wait_role(variant, &p_full[h * S2RING + slot], (gt / S2RING) & 1);  // k-th use by this half = gt / 3
+          wait_role(variant, &p_full[h * S2RING + slot], (pbits >> slot) & 1);
+          pbits ^= 1u << slot;
           if (lane == 0) FTRACE(6, it, t, h);
           tc::tc_fence_after();
           const uint32_t v_addr = tc::smem_u32(smem + S2_V + vs * V_BYTES);
@@ -636,8 +689,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int q = 0; q < ((variant & 16) ? 0 : 4); ++q) {
             const uint64_t bd = tc::smem_desc(v_addr + q * 32 * 128, V_BYTES, 1024, tc::kSwizzle128B);
             tc::mma_sp_f16_ts_w(tmem_base + T2_O + h * HD, s_col + 32 * q + 16, bd, s_col + 32 * q, idesc_pv,
-                                (t > 0 || q > 0) ? 1u : 0u);
+                                (!first || q > 0) ? 1u : 0u);
           }
+          first = false;
           tc::mma_commit_w(&s_free[slot]);
           tc::mma_commit_w(&v_empty[vs]);
           tc::mma_commit_w(&pv_done[h]);
@@ -659,7 +713,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     float* rmax = red_max + h * 2 * BM;
     float* rsum = red_sum + h * 2 * BM;
     const bool tw = quad == 0 && pr == 0 && lane == 0;
-    uint32_t gt = 0, scol = 0;  // scol: this warp's first S column of the current step's buffer
+    uint32_t gcount = 0, hcount = 0, scol = 0;  // live steps (both halves / this half); this warp's S column
     int it = 0;
     // maximum of this row over the set's 128 columns of the current S (both warps of the pair)
     bool cm[2] = {false, false};  // this warp's two chunks of the current tile masked (BlockMask)
@@ -667,12 +721,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       float mt = -INFINITY;
 #pragma unroll
       for (int ch = 0; ch < 2; ++ch) {
-        if (cm[ch]) continue;
         uint32_t s[32];
         tc::tmem_ld_32x32b_x32(scol + 32 * ch, s);
         tc::tmem_ld_wait(s);
+        float mc = -INFINITY;
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) mt = fmaxf(mt, fmaxf(__uint_as_float(s[j]), __uint_as_float(s[j + 1])));
+        for (int j = 0; j < 32; j += 2) mc = fmaxf(mc, fmaxf(__uint_as_float(s[j]), __uint_as_float(s[j + 1])));
+        if (!cm[ch]) mt = fmaxf(mt, mc);
       }
       rmax[pr * BM + r] = mt;
       tc::named_bar_sync(pbar, 64);
@@ -707,20 +762,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int j = 0; j < 4; ++j) orow[j] = make_uint4(pko[4 * j], pko[4 * j + 1], pko[4 * j + 2], pko[4 * j + 3]);
       pend = false;
     };
-    for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+    // chunk-keep word `lane` of this warp's 32-row strip (cbits), next item's prefetched
+    auto cword = [&](int item_) -> uint32_t {
+      if (!MASKED || item_ < 0 || (int)lane >= tmask.cbw) return 0u;
+      const int strip = ((item_ % iblocks) * 2 + h) * (BM / 32) + quad;
+      return __ldg(tmask.cbits + (int64_t)strip * tmask.cbw + lane);
+    };
+    uint32_t cw = cword(item_at(0));
+    for (int kk_ = 0, item = item_at(0); item >= 0; item = item_at(++kk_), ++it) {
       const int b = item / iblocks, ib = item % iblocks;
+      const uint32_t cwn = cword(item_at(kk_ + 1));
       float mlog = 0.f, l0 = 0.f, l1 = 0.f;
-      for (int t = 0; t < ntiles; ++t, ++gt) {
-        const uint32_t g = 2 * gt + h;  // global step
+      bool first = true;  // first live step of this half-item: establishes the shift
+      for (int t = 0; t < ntiles; ++t) {
+        const bool lv0 = live(ib, t, 0), lv1 = live(ib, t, 1);
+        const uint32_t g = gcount + (h ? (uint32_t)lv0 : 0u);  // global live step
+        gcount += (uint32_t)lv0 + (uint32_t)lv1;
+        if (MASKED && !(h ? lv1 : lv0)) continue;  // whole 128 x 128 step masked for this half
+        ++hcount;
         const uint32_t slot = g % S2RING;
         scol = lane_base + slot * BN + 64 * pr;
         tc::mbar_wait(&s_full[slot], (g / S2RING) & 1);
         if (tw) FTRACE(0, it, t, h);
         tc::tc_fence_after();
-        const int row0 = (ib * 2 + h) * BM + quad * 32, col0 = t * BN + 64 * pr;
-        cm[0] = MASKED && tmask.masked(row0, col0);
-        cm[1] = MASKED && tmask.masked(row0, col0 + 32);
-        if (t == 0) mlog = row_max();  // the shift starts at the row maximum of the item's first tile
+        if (MASKED && !(variant & 4096)) {
+          const int c32 = 4 * t + 2 * pr;  // this warp's first 32-column chunk
+          const uint32_t w = __shfl_sync(0xffffffffu, cw, c32 >> 5) >> (c32 & 31);
+          cm[0] = !(w & 1u);
+          cm[1] = !(w & 2u);
+        }
+        if (first) mlog = row_max();  // the shift starts at the row maximum of the item's first live tile
         uint32_t pk[2][8], W[2];
         float lt0 = 0.f, lt1 = 0.f;
         auto compute = [&]() {
@@ -728,10 +799,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int ch = 0; ch < 2; ++ch) {
             float a0, a1;
-            if (cm[ch]) {  // masked tile: structurally absent
-              masked_chunk(pk[ch], W[ch], a0, a1);
-              continue;
-            }
             uint32_t s[32];
             tc::tmem_ld_32x32b_x32(scol + 32 * ch, s);
             tc::tmem_ld_wait(s);
@@ -744,17 +811,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             } else {
               prune_exp_tile<T, PAIRS>(s, c, mlog, two, pk[ch], W[ch], a0, a1);
             }
+            // masked chunk (structurally absent): computed like the others -- straight-line code
+            // keeps the two chunks interleaved -- then overwritten (predicated moves)
+            if (MASKED && cm[ch]) masked_chunk(pk[ch], W[ch], a0, a1);
             add2(lt0, lt1, a0, a1, lt0, lt1);
             if (tw) FTRACE(12 + 2 * ch, it, t, h);
           }
         };
         compute();
-        if (t > 0 && bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit))) {
+        if (!first && bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit))) {
           // ---- slow path (both warps of the pair): raise the shift to the row maximum,
           // rescale O_h and the sums once every PV into O_h so far (this half's tile t-1) retired.
           // (pv_done[h] completes once per tile of this half and cannot run ahead of this set,
           // unlike the ring barriers, which the other set may advance twice meanwhile.)
-          tc::mbar_wait(&pv_done[h], (gt - 1) & 1);
+          tc::mbar_wait(&pv_done[h], (hcount - 2) & 1);  // completion of this half's previous live step
           tc::tc_fence_after();
           const float mnew = fmaxf(mlog, row_max());
           const float f = fex2(mlog - mnew);
@@ -792,7 +862,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&p_full[h * S2RING + slot]);
         if (tw) FTRACE(2, it, t, h);
-        if (pend) epilogue();  // previous item's output (t == 0 only)
+        first = false;
+        if (pend) epilogue();  // previous item's output (first live step only)
       }
       // the epilogue of this item runs after step 0 of the next one (below), so the wait for
       // the item's last PV overlaps that step instead of idling the set at every item boundary
@@ -801,6 +872,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       pend_ib = ib;
       pend_it = it;
       pend_l = l0 + l1;
+      cw = cwn;
     }
     if (pend) epilogue();
   }
@@ -810,6 +882,57 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc::tc_fence_after();
     tc::tmem_dealloc<512>(tmem_base);
   }
+}
+
+// BlockMask tile grid -> step / chunk bitmaps (TileMask::sbits / cbits) for the two-set
+// kernel; one thread per bit, a warp writes one word.
+__global__ void mask_bits_kernel(TileMask m, int n, uint32_t* __restrict__ sbits, uint32_t* __restrict__ cbits) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t ns = (int64_t)(n / BM) * m.sbw * 32, nc = (int64_t)(n / 32) * m.cbw * 32;
+  bool bit = false;
+  if (i < ns) {
+    const int row = (int)(i / (m.sbw * 32)), t = (int)(i % (m.sbw * 32));
+    bit = t < n / BN && m.region_live(row * BM, BM, t * BN, BN);
+  } else if (i < ns + nc) {
+    const int64_t j = i - ns;
+    const int strip = (int)(j / (m.cbw * 32)), c = (int)(j % (m.cbw * 32));
+    bit = c < n / 32 && !m.masked(strip * 32, c * 32);
+  }
+  const uint32_t w = __ballot_sync(0xffffffffu, bit);
+  if ((threadIdx.x & 31) == 0) {
+    if (i < ns) sbits[i >> 5] = w;
+    else if (i < ns + nc) cbits[(i - ns) >> 5] = w;
+  }
+}
+
+// row blocks (256 rows, one two-set item) ranked by live steps, heaviest first (ties: lower
+// block first); one thread per row block, n <= 32768
+__global__ void mask_order_kernel(const uint32_t* __restrict__ sbits, int sbw, int iblocks, int* __restrict__ order) {
+  __shared__ int cost[128];
+  const int i = threadIdx.x;
+  if (i < iblocks) {
+    int c = 0;
+    for (int w = 0; w < 2 * sbw; ++w) c += __popc(sbits[2 * i * sbw + w]);
+    cost[i] = c;
+  }
+  __syncthreads();
+  if (i < iblocks) {  // order[rank] = block | first rank of its equal-cost group << 8 | group size << 16
+    int r = 0, r0 = 0, m = 0;
+    for (int j = 0; j < iblocks; ++j) {
+      r += cost[j] > cost[i] || (cost[j] == cost[i] && j < i);
+      r0 += cost[j] > cost[i];
+      m += cost[j] == cost[i];
+    }
+    order[r] = i | r0 << 8 | m << 16;
+  }
+}
+
+static int mask_sbw(int n) { return (n / BN + 31) / 32; }
+static int mask_cbw(int n) { return (n / 32 + 31) / 32; }
+static int64_t mask_words(int n) { return (int64_t)(n / BM) * mask_sbw(n) + (int64_t)(n / 32) * mask_cbw(n); }
+
+int64_t flash_mask_workspace_bytes(int n) {
+  return ((mask_words(n) + n / (2 * BM)) * 4 + 255) / 256 * 256;  // bitmaps + row-block order
 }
 
 bool tc_flash_supported(int gs, int dtype, int n, int d) {
@@ -832,7 +955,8 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
   // per half); otherwise 128-row items and 128-key tiles with all 16 softmax warps on one
   // half.  DFSS_FLASH_KERNEL=1 forces the one-set kernel (experiments).
   static const int force1 = getenv("DFSS_FLASH_KERNEL") ? atoi(getenv("DFSS_FLASH_KERNEL")) == 1 : 0;
-  const bool two_set = n % (2 * BM) == 0 && !force1;
+  // masked two-set kernel: one chunk word per lane (n <= 32768)
+  const bool two_set = n % (2 * BM) == 0 && !force1 && (!MASKED || mask_cbw(n) <= 32);
   const uint32_t kvbox = BN;
   kbox[3] = kvbox / 4;
   if (!encode_tmap_3d(&tq, dt, 2, (void*)q, HD, n, bh, HD, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
@@ -841,7 +965,15 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
     return cudaErrorInvalidValue;
   const int halves = two_set ? 2 : 1;
   auto kern = two_set ? dfss_flash2_kernel<T, PAIRS, MASKED> : dfss_flash_kernel<T, 1, PAIRS, MASKED>;
-  const int smem_total = two_set ? S2_TOTAL : SMEM_TOTAL;
+  const int smem_total =
+      two_set ? S2_TOTAL + (MASKED ? ((n / BM) * tmask.sbw + n / (2 * BM)) * 4 : 0) : SMEM_TOTAL;
+  if (smem_total > 227 * 1024) return cudaErrorNotSupported;
+  if (MASKED && two_set) {
+    const int64_t bits = ((int64_t)(n / BM) * tmask.sbw + (int64_t)(n / 32) * tmask.cbw) * 32;
+    mask_bits_kernel<<<(unsigned)((bits + 255) / 256), 256, 0, s>>>(tmask, n, (uint32_t*)tmask.sbits,
+                                                                    (uint32_t*)tmask.cbits);
+    mask_order_kernel<<<1, 128, 0, s>>>(tmask.sbits, tmask.sbw, n / (2 * BM), (int*)tmask.order);
+  }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_total);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -884,12 +1016,20 @@ bool tc_flash_mask_supported(int tile_rows, int tile_cols) {
 
 cudaError_t launch_flash_tc(const void* q, const void* k, const void* v, void* out, float scale, int gs, int dtype,
                             int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows, int tile_cols,
-                            cudaStream_t s) {
+                            void* workspace, cudaStream_t s) {
   if (!tc_flash_supported(gs, dtype, n, d)) return cudaErrorNotSupported;
   if (tile_keep && !tc_flash_mask_supported(tile_rows, tile_cols)) return cudaErrorNotSupported;
+  if (tile_keep && !workspace) return cudaErrorInvalidValue;  // flash_mask_workspace_bytes(n)
   if (bh == 0) return cudaSuccess;
   TileMask m{tile_keep, tile_keep ? tile_rows : 1, tile_keep ? tile_cols : 1,
              tile_keep ? (n + tile_cols - 1) / tile_cols : 1};
+  if (tile_keep) {
+    m.sbw = mask_sbw(n);
+    m.cbw = mask_cbw(n);
+    m.sbits = (const uint32_t*)workspace;
+    m.cbits = m.sbits + (int64_t)(n / BM) * m.sbw;
+    m.order = (const int*)(m.sbits + mask_words(n));
+  }
   const bool bf = dtype == DFSS_BF16, masked = tile_keep != nullptr;
   if (gs == 2) {
     if (masked)

@@ -23,7 +23,8 @@ from .sparse_ops import softmax_rows, spmm
 def workspace_bytes(mode, dtype: torch.dtype, bh: int, n: int, d: int, math_mode: str = "auto",
                     block_mask: BlockMask | None = None) -> int:
     """Device scratch one dfss_attention call needs on the path it will take: 0 for the fused
-    16-bit kernel, V^T for the fused tf32 kernel, the compressed P + metadata when staged."""
+    16-bit kernel (its liveness bitmaps with a block mask), V^T for the fused tf32 kernel, the
+    compressed P + metadata when staged."""
     mode = as_mode(mode)
     tr, tc_ = (block_mask.tile_rows, block_mask.tile_cols) if block_mask is not None else (0, 0)
     return int(_lib.load().dfss_nm_attention_workspace_bytes_for(mode.group_size, _lib.dtype_id(dtype),

@@ -488,6 +488,54 @@ def test_block_masked_attention_matches_reference(n, tiles, mode, dtype):
     assert_close(got, out[0, 0], 1e-6, 1e-6, "nm_attention(block_mask) == dfss_attention(block_mask)")
 
 
+def _block_causal_keep(n, tr, tc_, blk=128):
+    """Keep-mask on (tr, tc_) tiles that is block-causal at blk x blk granularity."""
+    rows = np.arange(-(-n // tr)) * tr // blk
+    cols = np.arange(-(-n // tc_)) * tc_ // blk
+    return cols[None, :] <= rows[:, None]
+
+
+@pytest.mark.parametrize("mode,dtype", [("2:4", torch.bfloat16), ("1:2", torch.float16)])
+def test_block_mask_whole_steps_skipped(mode, dtype):
+    """Whole 128 x 128 steps masked (block-causal + random dead blocks): the two-set kernel skips
+    them entirely, including steps dead for one 128-row half of a 256-row item only; several
+    items per CTA so the barrier phases must survive variable step counts."""
+    n, tr, tc_ = 1024, 32, 64
+    rng = np.random.default_rng(11)
+    keep = _block_causal_keep(n, tr, tc_)
+    blocks = rng.random((n // 128, n // 128)) < 0.3          # extra dead 128 x 128 blocks below the diagonal
+    np.fill_diagonal(blocks, False)
+    keep &= ~np.kron(blocks, np.ones((128 // tr, 128 // tc_), dtype=bool))
+    mask = dfss.BlockMask(keep, tile_rows=tr, tile_cols=tc_)
+    (q, k, v), (q64, k64, v64) = seeded_qkv((4, 40, n, 64), dtype, seed=5)   # 640 items > 148 CTAs
+    out = _np(dfss.dfss_attention(q, k, v, mode, block_mask=mask))
+    for b, h in [(0, 0), (1, 17), (3, 39)]:
+        want = _masked_oracle(q64[b, h], k64[b, h], v64[b, h], mask, mode)
+        assert_close(out[b, h], want, 2e-2, 2e-2, f"block-causal {mode} ({b},{h})")
+
+
+def test_block_mask_skipping_saves_time():
+    """Block-causal masks (~56% of the 128 x 128 steps live at n = 4096) cut the fused kernel time."""
+    n = 4096
+    (q, k, v), _ = seeded_qkv((1, 64, n, 64), torch.bfloat16, seed=3)
+    mask = dfss.BlockMask(_block_causal_keep(n, 32, 64), 32, 64)
+    out = torch.empty_like(q)
+
+    def timed(bm):
+        for _ in range(3):
+            dfss.dfss_attention(q, k, v, "2:4", block_mask=bm, out=out)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            dfss.dfss_attention(q, k, v, "2:4", block_mask=bm, out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / 10
+
+    dense, causal = timed(None), timed(mask)
+    assert causal < 0.75 * dense, (causal, dense)
+
+
 def test_block_mask_empty_row_and_tiling_errors():
     (q, k, v), _ = seeded_qkv((1, 1, 256, 64), torch.bfloat16, seed=2)
     keep = np.ones((8, 4), dtype=bool)

@@ -12,6 +12,9 @@ import torch
 import paper_2203_00091_b200 as dfss
 shape = [int(x) for x in os.environ.get("TRACE_SHAPE", "8,12,4096,64").split(",")]
 q, k, v = (torch.randn(*shape, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+bm = None
+if os.environ.get("TRACE_MASK") == "all":  # all-kept block mask: the masked kernel on a dense pattern
+    bm = dfss.BlockMask(np.ones((shape[2] // 32, shape[2] // 64), dtype=bool), 32, 64)
 for _ in range(3):
-    dfss.dfss_attention(q, k, v, "2:4")
+    dfss.dfss_attention(q, k, v, "2:4", block_mask=bm)
 torch.cuda.synchronize()

@@ -15,7 +15,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libdfss_sm100a.so")
+# DFSS_LIB: an alternative build of the same library (kernel experiments in tools/)
+LIB_PATH = os.environ.get("DFSS_LIB") or os.path.join(_HERE, "lib", "libdfss_sm100a.so")
 
 DFSS_OK, DFSS_ERR_INVALID, DFSS_ERR_UNSUPPORTED, DFSS_ERR_CUDA, DFSS_ERR_NO_DEVICE = 0, -1, -2, -3, -4
 F32, BF16, F16 = 0, 1, 2

@@ -49,6 +49,10 @@
 
 #include "flash_common.cuh"
 
+#ifndef DFSS_MASK_EXP
+#define DFSS_MASK_EXP 0  // compile-time experiment switches (tools/mask_exp.sh); 0 in the product
+#endif
+
 namespace dfss {
 
 namespace {
@@ -525,6 +529,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // warps, from per-strip chunk words held one per lane: no mask load on any critical path.
   uint32_t* s_live = (uint32_t*)(smem + S2_LIVE);
   auto live = [&](int ib, int t, int hh) {
+#if DFSS_MASK_EXP & 1
+    return true;
+#endif
     return !MASKED || (variant & 8192) || ((s_live[(ib * 2 + hh) * tmask.sbw + (t >> 5)] >> (t & 31)) & 1u);
   };
   int* s_order = (int*)(s_live + (n / BM) * tmask.sbw);
@@ -537,17 +544,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // (mask_order_kernel) and the ranked items dealt out in snake order -- heaviest first,
   // alternating direction per round -- so CTAs finish together (an all-kept mask reproduces the
   // dense order).  Every role walks the same sequence.
-  auto item_at = [&](int k) -> int {
+  // The position sequence is a pure function of (k, blockIdx) so loop control stays warp-uniform
+  // for the MMA issuers (a trip count read from shared memory would make every loop divergent
+  // in the compiler's eyes: no uniform datapath, R2UR / ELECT around each MMA).
+  auto pos_at = [&](int k) -> int {
     const int g = gridDim.x;
-    if (!MASKED) {
-      const int i = blockIdx.x + k * g;
-      return i < items ? i : -1;
-    }
-    const int p = k * g + ((k & 1) ? g - 1 - (int)blockIdx.x : (int)blockIdx.x);
-    if (p >= items) return -1;
+    return k * g + (MASKED && (k & 1) && !(DFSS_MASK_EXP & 16) ? g - 1 - (int)blockIdx.x : (int)blockIdx.x);
+  };
+  auto item_of = [&](int p) -> int {
+    if (!MASKED || (DFSS_MASK_EXP & 8)) return p;
     // within a group of equal-cost row blocks keep the dense head-major order (K / V reuse in L2)
     const int info = s_order[p / bh], r0 = (info >> 8) & 255, m = info >> 16, o = p - r0 * bh;
     return (o / m) * iblocks + (s_order[r0 + o % m] & 255);
+  };
+  // step-liveness words of an item's two halves for tiles [32 (t / 32), +32), refreshed every
+  // 32 tiles; bit_u reads one as a warp vote so branches on it stay uniform in the converged
+  // role warps
+  auto live_words = [&](int ib, int t, uint32_t& w0, uint32_t& w1) {
+    if (MASKED && (t & 31) == 0) {
+      w0 = s_live[(ib * 2) * tmask.sbw + (t >> 5)];
+      w1 = s_live[(ib * 2 + 1) * tmask.sbw + (t >> 5)];
+    }
+  };
+  auto bit_u = [&](uint32_t w, int t) {
+    return !MASKED || (DFSS_MASK_EXP & 1) || __any_sync(0xffffffffu, (w >> (t & 31)) & 1u);
   };
 
   if (warp == W_QK && lane == 0) {
@@ -587,7 +607,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int ks = 0, vs = 0, it = 0;
       uint32_t kph = 0, vph = 0;
-      for (int kk_ = 0, item = item_at(0); item >= 0; item = item_at(++kk_), ++it) {
+      for (int kk_ = 0, pos = pos_at(0); pos < items; pos = pos_at(++kk_), ++it) {
+        const int item = item_of(pos);
+        uint32_t lw0 = 0, lw1 = 0;
         const int b = item / iblocks, ib = item % iblocks;
         const int qs = it & 1;
         wait_role(variant, &q_empty[qs], ((it >> 1) & 1) ^ 1);
@@ -595,7 +617,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc::tma_load_3d(smem + S2_Q + (2 * qs) * Q_BYTES, &tm_q, &q_full[qs], 0, ib * 2 * BM, b);
         tc::tma_load_3d(smem + S2_Q + (2 * qs + 1) * Q_BYTES, &tm_q, &q_full[qs], 0, ib * 2 * BM + BM, b);
         for (int t = 0; t < ntiles; ++t) {
-          if (MASKED && !live(ib, t, 0) && !live(ib, t, 1)) continue;
+          live_words(ib, t, lw0, lw1);
+          if (MASKED && !(DFSS_MASK_EXP & 1) && !(((lw0 | lw1) >> (t & 31)) & 1u)) continue;
           wait_role(variant, &k_empty[ks], kph ^ 1);
           tc::mbar_arrive_expect_tx(&k_full[ks], K_BYTES);
           tc::tma_load_5d(smem + S2_K + ks * K_BYTES, &tm_k, &k_full[ks], 0, 0, 0, t * (BN / 4), b);
@@ -616,12 +639,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       constexpr uint32_t idesc_s = tc::instr_desc(fmt, BM, BN, false, false, false);
       int ks = 0, it = 0, sb = 0;
       uint32_t kph = 0, sph = 0;
-      for (int kk_ = 0, item = item_at(0); item >= 0; item = item_at(++kk_), ++it) {
+      for (int kk_ = 0, pos = pos_at(0); pos < items; pos = pos_at(++kk_), ++it) {
+        const int item = item_of(pos);
+        uint32_t lw0 = 0, lw1 = 0;
         const int qs = it & 1;
         const int ib = item % iblocks;
         wait_role(variant, &q_full[qs], (it >> 1) & 1);
         for (int t = 0; t < ntiles; ++t) {
-          const bool lv[2] = {live(ib, t, 0), live(ib, t, 1)};
+          live_words(ib, t, lw0, lw1);
+          const bool lv[2] = {bit_u(lw0, t), bit_u(lw1, t)};
           if (MASKED && !lv[0] && !lv[1]) continue;
           wait_role(variant, &k_full[ks], kph);
           if (lane == 0) FTRACE(10, it, t, 0);
@@ -661,12 +687,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       constexpr uint32_t idesc_pv = tc::instr_desc(fmt, BM, HD, false, true, true);
       int vs = 0, it = 0;
       uint32_t vph = 0, gcount = 0, pbits = 0;  // live steps so far (both halves); p_full phase per slot
-      for (int kk_ = 0, item = item_at(0); item >= 0; item = item_at(++kk_), ++it) {
+      for (int kk_ = 0, pos = pos_at(0); pos < items; pos = pos_at(++kk_), ++it) {
+        const int item = item_of(pos);
+        uint32_t lw0 = 0, lw1 = 0;
         const int ib = item % iblocks;
         wait_role(variant, &o_empty[h], (it & 1) ^ 1);
         bool first = true;  // first live step of this half-item initialises O_h
         for (int t = 0; t < ntiles; ++t) {
-          const bool l0 = live(ib, t, 0), l1 = live(ib, t, 1);
+          live_words(ib, t, lw0, lw1);
+          const bool l0 = bit_u(lw0, t), l1 = bit_u(lw1, t);
           if (MASKED && !l0 && !l1) continue;  // tile not loaded
           const uint32_t g = gcount + (h ? (uint32_t)l0 : 0u), slot = g % S2RING;
           gcount += (uint32_t)l0 + (uint32_t)l1;
@@ -763,19 +792,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       pend = false;
     };
     // chunk-keep word `lane` of this warp's 32-row strip (cbits), next item's prefetched
-    auto cword = [&](int item_) -> uint32_t {
-      if (!MASKED || item_ < 0 || (int)lane >= tmask.cbw) return 0u;
-      const int strip = ((item_ % iblocks) * 2 + h) * (BM / 32) + quad;
+    auto cword = [&](int pos_) -> uint32_t {
+      if (!MASKED || pos_ >= items || (int)lane >= tmask.cbw || (DFSS_MASK_EXP & 4)) return 0u;
+      const int strip = ((item_of(pos_) % iblocks) * 2 + h) * (BM / 32) + quad;
       return __ldg(tmask.cbits + (int64_t)strip * tmask.cbw + lane);
     };
-    uint32_t cw = cword(item_at(0));
-    for (int kk_ = 0, item = item_at(0); item >= 0; item = item_at(++kk_), ++it) {
+    uint32_t cw = cword(pos_at(0));
+    for (int kk_ = 0, pos = pos_at(0); pos < items; pos = pos_at(++kk_), ++it) {
+        const int item = item_of(pos);
+        uint32_t lw0 = 0, lw1 = 0;
       const int b = item / iblocks, ib = item % iblocks;
-      const uint32_t cwn = cword(item_at(kk_ + 1));
+      const uint32_t cwn = cword(pos_at(kk_ + 1));
       float mlog = 0.f, l0 = 0.f, l1 = 0.f;
       bool first = true;  // first live step of this half-item: establishes the shift
       for (int t = 0; t < ntiles; ++t) {
-        const bool lv0 = live(ib, t, 0), lv1 = live(ib, t, 1);
+        live_words(ib, t, lw0, lw1);
+        const bool lv0 = bit_u(lw0, t), lv1 = bit_u(lw1, t);
         const uint32_t g = gcount + (h ? (uint32_t)lv0 : 0u);  // global live step
         gcount += (uint32_t)lv0 + (uint32_t)lv1;
         if (MASKED && !(h ? lv1 : lv0)) continue;  // whole 128 x 128 step masked for this half
@@ -785,16 +817,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc::mbar_wait(&s_full[slot], (g / S2RING) & 1);
         if (tw) FTRACE(0, it, t, h);
         tc::tc_fence_after();
-        if (MASKED && !(variant & 4096)) {
+        bool anym = false;  // a chunk of this warp masked (uniform): the masked compute variant
+        if (MASKED && !(variant & 4096) && !(DFSS_MASK_EXP & 2)) {
           const int c32 = 4 * t + 2 * pr;  // this warp's first 32-column chunk
           const uint32_t w = __shfl_sync(0xffffffffu, cw, c32 >> 5) >> (c32 & 31);
           cm[0] = !(w & 1u);
           cm[1] = !(w & 2u);
+          anym = __any_sync(0xffffffffu, (~w & 3u) != 0);
         }
         if (first) mlog = row_max();  // the shift starts at the row maximum of the item's first live tile
         uint32_t pk[2][8], W[2];
         float lt0 = 0.f, lt1 = 0.f;
-        auto compute = [&]() {
+        auto compute = [&](auto masked_variant) {
+          constexpr bool MV = decltype(masked_variant)::value;
           lt0 = lt1 = 0.f;
 #pragma unroll
           for (int ch = 0; ch < 2; ++ch) {
@@ -813,13 +848,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             // masked chunk (structurally absent): computed like the others -- straight-line code
             // keeps the two chunks interleaved -- then overwritten (predicated moves)
-            if (MASKED && cm[ch]) masked_chunk(pk[ch], W[ch], a0, a1);
+            if (MV && cm[ch]) masked_chunk(pk[ch], W[ch], a0, a1);
             add2(lt0, lt1, a0, a1, lt0, lt1);
             if (tw) FTRACE(12 + 2 * ch, it, t, h);
           }
         };
-        compute();
-        if (!first && bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit))) {
+        // one copy of the compute code (instruction-cache footprint): the slow path loops back
+#pragma unroll 1
+        for (int pass = 0;; ++pass) {
+          if (MASKED && anym) compute(std::true_type{});
+          else compute(std::false_type{});
+          if (pass > 0 || first || !bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit))) break;
           // ---- slow path (both warps of the pair): raise the shift to the row maximum,
           // rescale O_h and the sums once every PV into O_h so far (this half's tile t-1) retired.
           // (pv_done[h] completes once per tile of this half and cannot run ahead of this set,
@@ -842,7 +881,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           tc::tmem_st_wait();
           mlog = mnew;
-          compute();
         }
         add2(l0, l1, lt0, lt1, l0, l1);
         if (tw) FTRACE(1, it, t, h);

@@ -337,6 +337,38 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True, info=Tr
     return res, (q, k, v, out, lo, hi)
 
 
+def block_mask_measure(device, steps=5):
+    """BlockMask tile skipping on the c4 shape (batch 8, 12 heads, seq 4096,
+    2:4 bf16).  Block-causal mask at 128 x 128 granularity on (32, 64) tiles: fully masked steps
+    are skipped (no K / V load, MMA or softmax work).  Dense SDPA with is_causal=True is listed as
+    the closest dense counterpart (token-causal, not block-causal)."""
+    import paper_2203_00091_b200 as dfss
+
+    b, h, n, d = 8, 12, 4096, 64
+    g = torch.Generator(device="cpu").manual_seed(5)
+    q, k, v = (torch.randn((b, h, n, d), generator=g).to(torch.bfloat16).to(device) for _ in range(3))
+    out = torch.empty_like(q)
+    rows, cols = np.arange(n // 32) * 32 // 128, np.arange(n // 64) * 64 // 128
+    keep = cols[None, :] <= rows[:, None]
+    mask = dfss.BlockMask(keep, 32, 64)
+    ws = torch.empty(dfss.workspace_bytes("2:4", q.dtype, b * h, n, d, block_mask=mask), dtype=torch.uint8,
+                     device=device)
+    flush_buf = torch.empty(256 * 2**20, dtype=torch.uint8, device=device)
+    flush = lambda: flush_buf.fill_(1)  # noqa: E731
+    t = lambda fn: float(np.mean(time_steps(fn, steps, 3, flush)))  # noqa: E731
+    res = {"workload": "c4 shape, 2:4 bf16, block-causal 128x128 BlockMask on 32x64 tiles",
+           "live_step_fraction": round(float(keep[::4, ::2].mean()), 4),
+           "dfss_unmasked_ms": round(t(lambda: dfss.dfss_attention(q, k, v, "2:4", out=out)), 4),
+           "dfss_block_causal_ms": round(t(lambda: dfss.dfss_attention(q, k, v, "2:4", block_mask=mask, out=out,
+                                                                        workspace=ws)), 4)}
+    sdpa = torch.nn.functional.scaled_dot_product_attention
+    res["sdpa_dense_ms"] = round(t(lambda: sdpa(q, k, v)), 4)
+    res["sdpa_causal_ms"] = round(t(lambda: sdpa(q, k, v, is_causal=True)), 4)
+    res["speedup_vs_unmasked"] = round(res["dfss_unmasked_ms"] / res["dfss_block_causal_ms"], 3)
+    res["speedup_vs_sdpa_causal"] = round(res["sdpa_causal_ms"] / res["dfss_block_causal_ms"], 3)
+    return res
+
+
 def e2e_measure(args, cfg, q, k, v, device):
     """Same metric through the public API with pinned host buffers: H2D inputs + compute + D2H output, every step."""
     import paper_2203_00091_b200 as dfss
@@ -495,6 +527,10 @@ def main():
                     except Exception as ex:
                         sw[name] = {"error": str(ex)[:200]}
                 extra["sweep"] = sw
+                try:
+                    extra["block_mask"] = block_mask_measure(device)
+                except Exception as ex:
+                    extra["block_mask"] = {"error": str(ex)[:200]}
 
     if rank == 0:
         line = {

@@ -132,9 +132,9 @@ int64_t dfss_nm_attention_workspace_bytes_for(int mode, int dtype, int math, int
   if (math == DFSS_MATH_AUTO && dtype != DFSS_F32 && dfss::tc_flash_supported(mode, dtype, n, d) && mask_ok &&
       dfss_has_tcgen05())
     return masked ? dfss::flash_mask_workspace_bytes(n) : 0;  // fused: no intermediate in HBM (mask bitmaps only)
-  if (math == DFSS_MATH_TF32 && dtype == DFSS_F32 && dfss::tc_flash_tf32_supported(mode, n, d) && mask_ok &&
-      dfss_has_tcgen05())
-    return (bh * (int64_t)n * d * 4 + 255) / 256 * 256;  // V^T for the K-major tf32 B operand
+  if (math == DFSS_MATH_TF32 && dtype == DFSS_F32 && dfss::tc_flash_tf32_supported(mode, n, d) &&
+      (!masked || (mask_ok && dfss::flash_mask_two_set_ok(n))) && dfss_has_tcgen05())
+    return dfss::flash_tf32_workspace_bytes(bh, n, masked);  // V^T (K-major tf32 B) + mask bitmaps
   return dfss_nm_attention_workspace_bytes(mode, dtype, bh, n, d);
 }
 
@@ -178,7 +178,8 @@ int dfss_nm_attention_masked(const void* q, const void* k, const void* v, void* 
                                              tile_cols, workspace, (cudaStream_t)stream));
   // tf32 1:2 on fp32 inputs: the fused tf32 kernel (configs[4] "1:2 tf32")
   if (math == DFSS_MATH_TF32 && dtype == DFSS_F32 && dfss::tc_flash_tf32_supported(mode, n, d) &&
-      (!tile_keep || dfss::tc_flash_mask_supported(tile_rows, tile_cols)) && dfss_has_tcgen05())
+      (!tile_keep || (dfss::tc_flash_mask_supported(tile_rows, tile_cols) && dfss::flash_mask_two_set_ok(n))) &&
+      dfss_has_tcgen05())
     return cuda_status(dfss::launch_flash_tf32(q, k, v, out, scale, bh, n, d, tile_keep, tile_rows, tile_cols,
                                                workspace, (cudaStream_t)stream));  // V^T in the workspace
   if (math == DFSS_MATH_TF32)

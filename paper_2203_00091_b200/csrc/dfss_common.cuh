@@ -202,10 +202,19 @@ cudaError_t launch_flash_tc(const void* q, const void* k, const void* v, void* o
                             void* workspace, cudaStream_t s);
 // workspace of launch_flash_tc with a tile mask (liveness bitmaps); unmasked needs none
 int64_t flash_mask_workspace_bytes(int n);
+// block-mask step skipping in the two-set fused kernels (flash_tc.cu): n % 256 == 0, n <= 32768
+bool flash_mask_two_set_ok(int n);
+int flash_mask_smem_bytes(int n);
+struct TileMask;
+// fills m's bitmap pointers (workspace of flash_mask_workspace_bytes(n)) and launches the
+// two pre-kernels that build them on stream s
+void prepare_mask_bits(TileMask& m, int n, void* workspace, cudaStream_t s);
 bool tc_spmm_supported(int gs, int p_dtype, int v_dtype, int out_dtype, int rows, int n_k, int d);
 // fused 1:2 attention on fp32 inputs with tf32 tensor cores (flash_tf32.cu), n % 256 == 0, d = 64
 bool tc_flash_tf32_supported(int gs, int n, int d);
-// vt_scratch: bh * n * 64 floats of device scratch (V^T; the kind::tf32 B operand must be K-major)
+// vt_scratch: flash_tf32_workspace_bytes of device scratch -- V^T (the kind::tf32 B operand
+// must be K-major), then the block-mask bitmaps when tile_keep is given (n <= 32768)
+int64_t flash_tf32_workspace_bytes(int64_t bh, int n, bool masked);
 cudaError_t launch_flash_tf32(const void* q, const void* k, const void* v, void* out, float scale, int64_t bh, int n,
                               int d, const uint8_t* tile_keep, int tile_rows, int tile_cols, void* vt_scratch,
                               cudaStream_t s);

@@ -49,9 +49,6 @@
 
 #include "flash_common.cuh"
 
-#ifndef DFSS_MASK_EXP
-#define DFSS_MASK_EXP 0  // compile-time experiment switches (tools/mask_exp.sh); 0 in the product
-#endif
 
 namespace dfss {
 
@@ -528,12 +525,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // Liveness comes from the step bitmap (copied to shared memory below) and, for the softmax
   // warps, from per-strip chunk words held one per lane: no mask load on any critical path.
   uint32_t* s_live = (uint32_t*)(smem + S2_LIVE);
-  auto live = [&](int ib, int t, int hh) {
-#if DFSS_MASK_EXP & 1
-    return true;
-#endif
-    return !MASKED || (variant & 8192) || ((s_live[(ib * 2 + hh) * tmask.sbw + (t >> 5)] >> (t & 31)) & 1u);
-  };
   int* s_order = (int*)(s_live + (n / BM) * tmask.sbw);
   if (MASKED) {
     for (int i = threadIdx.x; i < (n / BM) * tmask.sbw; i += blockDim.x) s_live[i] = __ldg(tmask.sbits + i);
@@ -549,10 +540,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // in the compiler's eyes: no uniform datapath, R2UR / ELECT around each MMA).
   auto pos_at = [&](int k) -> int {
     const int g = gridDim.x;
-    return k * g + (MASKED && (k & 1) && !(DFSS_MASK_EXP & 16) ? g - 1 - (int)blockIdx.x : (int)blockIdx.x);
+    return k * g + (MASKED && (k & 1) ? g - 1 - (int)blockIdx.x : (int)blockIdx.x);
   };
   auto item_of = [&](int p) -> int {
-    if (!MASKED || (DFSS_MASK_EXP & 8)) return p;
+    if (!MASKED) return p;
     // within a group of equal-cost row blocks keep the dense head-major order (K / V reuse in L2)
     const int info = s_order[p / bh], r0 = (info >> 8) & 255, m = info >> 16, o = p - r0 * bh;
     return (o / m) * iblocks + (s_order[r0 + o % m] & 255);
@@ -567,7 +558,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   };
   auto bit_u = [&](uint32_t w, int t) {
-    return !MASKED || (DFSS_MASK_EXP & 1) || __any_sync(0xffffffffu, (w >> (t & 31)) & 1u);
+    return !MASKED || __any_sync(0xffffffffu, (w >> (t & 31)) & 1u);
   };
 
   if (warp == W_QK && lane == 0) {
@@ -618,7 +609,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc::tma_load_3d(smem + S2_Q + (2 * qs + 1) * Q_BYTES, &tm_q, &q_full[qs], 0, ib * 2 * BM + BM, b);
         for (int t = 0; t < ntiles; ++t) {
           live_words(ib, t, lw0, lw1);
-          if (MASKED && !(DFSS_MASK_EXP & 1) && !(((lw0 | lw1) >> (t & 31)) & 1u)) continue;
+          if (MASKED && !(((lw0 | lw1) >> (t & 31)) & 1u)) continue;
           wait_role(variant, &k_empty[ks], kph ^ 1);
           tc::mbar_arrive_expect_tx(&k_full[ks], K_BYTES);
           tc::tma_load_5d(smem + S2_K + ks * K_BYTES, &tm_k, &k_full[ks], 0, 0, 0, t * (BN / 4), b);
@@ -793,7 +784,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     };
     // chunk-keep word `lane` of this warp's 32-row strip (cbits), next item's prefetched
     auto cword = [&](int pos_) -> uint32_t {
-      if (!MASKED || pos_ >= items || (int)lane >= tmask.cbw || (DFSS_MASK_EXP & 4)) return 0u;
+      if (!MASKED || pos_ >= items || (int)lane >= tmask.cbw) return 0u;
       const int strip = ((item_of(pos_) % iblocks) * 2 + h) * (BM / 32) + quad;
       return __ldg(tmask.cbits + (int64_t)strip * tmask.cbw + lane);
     };
@@ -818,7 +809,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (tw) FTRACE(0, it, t, h);
         tc::tc_fence_after();
         bool anym = false;  // a chunk of this warp masked (uniform): the masked compute variant
-        if (MASKED && !(variant & 4096) && !(DFSS_MASK_EXP & 2)) {
+        if (MASKED) {
           const int c32 = 4 * t + 2 * pr;  // this warp's first 32-column chunk
           const uint32_t w = __shfl_sync(0xffffffffu, cw, c32 >> 5) >> (c32 & 31);
           cm[0] = !(w & 1u);
@@ -973,13 +964,28 @@ int64_t flash_mask_workspace_bytes(int n) {
   return ((mask_words(n) + n / (2 * BM)) * 4 + 255) / 256 * 256;  // bitmaps + row-block order
 }
 
+bool flash_mask_two_set_ok(int n) { return n % (2 * BM) == 0 && mask_cbw(n) <= 32; }
+
+int flash_mask_smem_bytes(int n) { return ((n / BM) * mask_sbw(n) + n / (2 * BM)) * 4; }
+
+void prepare_mask_bits(TileMask& m, int n, void* workspace, cudaStream_t s) {
+  m.sbw = mask_sbw(n);
+  m.cbw = mask_cbw(n);
+  m.sbits = (const uint32_t*)workspace;
+  m.cbits = m.sbits + (int64_t)(n / BM) * m.sbw;
+  m.order = (const int*)(m.sbits + mask_words(n));
+  const int64_t bits = mask_words(n) * 32;
+  mask_bits_kernel<<<(unsigned)((bits + 255) / 256), 256, 0, s>>>(m, n, (uint32_t*)m.sbits, (uint32_t*)m.cbits);
+  mask_order_kernel<<<1, 128, 0, s>>>(m.sbits, m.sbw, n / (2 * BM), (int*)m.order);
+}
+
 bool tc_flash_supported(int gs, int dtype, int n, int d) {
   return (gs == 4 || gs == 2) && (dtype == DFSS_BF16 || dtype == DFSS_F16) && d == HD && n % BM == 0 && n > 0;
 }
 
 template <typename T, bool PAIRS, bool MASKED>
 static cudaError_t flash_launch_typed(const void* q, const void* k, const void* v, void* out, float scale, int64_t bh,
-                                      int n, TileMask tmask, cudaStream_t s) {
+                                      int n, TileMask tmask, void* workspace, cudaStream_t s) {
   const CUtensorMapDataType dt =
       std::is_same<T, __nv_bfloat16>::value ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv;
@@ -994,7 +1000,7 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
   // half.  DFSS_FLASH_KERNEL=1 forces the one-set kernel (experiments).
   static const int force1 = getenv("DFSS_FLASH_KERNEL") ? atoi(getenv("DFSS_FLASH_KERNEL")) == 1 : 0;
   // masked two-set kernel: one chunk word per lane (n <= 32768)
-  const bool two_set = n % (2 * BM) == 0 && !force1 && (!MASKED || mask_cbw(n) <= 32);
+  const bool two_set = n % (2 * BM) == 0 && !force1 && (!MASKED || flash_mask_two_set_ok(n));
   const uint32_t kvbox = BN;
   kbox[3] = kvbox / 4;
   if (!encode_tmap_3d(&tq, dt, 2, (void*)q, HD, n, bh, HD, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
@@ -1003,15 +1009,9 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
     return cudaErrorInvalidValue;
   const int halves = two_set ? 2 : 1;
   auto kern = two_set ? dfss_flash2_kernel<T, PAIRS, MASKED> : dfss_flash_kernel<T, 1, PAIRS, MASKED>;
-  const int smem_total =
-      two_set ? S2_TOTAL + (MASKED ? ((n / BM) * tmask.sbw + n / (2 * BM)) * 4 : 0) : SMEM_TOTAL;
+  const int smem_total = two_set ? S2_TOTAL + (MASKED ? flash_mask_smem_bytes(n) : 0) : SMEM_TOTAL;
   if (smem_total > 227 * 1024) return cudaErrorNotSupported;
-  if (MASKED && two_set) {
-    const int64_t bits = ((int64_t)(n / BM) * tmask.sbw + (int64_t)(n / 32) * tmask.cbw) * 32;
-    mask_bits_kernel<<<(unsigned)((bits + 255) / 256), 256, 0, s>>>(tmask, n, (uint32_t*)tmask.sbits,
-                                                                    (uint32_t*)tmask.cbits);
-    mask_order_kernel<<<1, 128, 0, s>>>(tmask.sbits, tmask.sbw, n / (2 * BM), (int*)tmask.order);
-  }
+  if (MASKED && two_set) prepare_mask_bits(tmask, n, workspace, s);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_total);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -1061,26 +1061,19 @@ cudaError_t launch_flash_tc(const void* q, const void* k, const void* v, void* o
   if (bh == 0) return cudaSuccess;
   TileMask m{tile_keep, tile_keep ? tile_rows : 1, tile_keep ? tile_cols : 1,
              tile_keep ? (n + tile_cols - 1) / tile_cols : 1};
-  if (tile_keep) {
-    m.sbw = mask_sbw(n);
-    m.cbw = mask_cbw(n);
-    m.sbits = (const uint32_t*)workspace;
-    m.cbits = m.sbits + (int64_t)(n / BM) * m.sbw;
-    m.order = (const int*)(m.sbits + mask_words(n));
-  }
   const bool bf = dtype == DFSS_BF16, masked = tile_keep != nullptr;
   if (gs == 2) {
     if (masked)
-      return bf ? flash_launch_typed<__nv_bfloat16, true, true>(q, k, v, out, scale, bh, n, m, s)
-                : flash_launch_typed<__half, true, true>(q, k, v, out, scale, bh, n, m, s);
-    return bf ? flash_launch_typed<__nv_bfloat16, true, false>(q, k, v, out, scale, bh, n, m, s)
-              : flash_launch_typed<__half, true, false>(q, k, v, out, scale, bh, n, m, s);
+      return bf ? flash_launch_typed<__nv_bfloat16, true, true>(q, k, v, out, scale, bh, n, m, workspace, s)
+                : flash_launch_typed<__half, true, true>(q, k, v, out, scale, bh, n, m, workspace, s);
+    return bf ? flash_launch_typed<__nv_bfloat16, true, false>(q, k, v, out, scale, bh, n, m, workspace, s)
+              : flash_launch_typed<__half, true, false>(q, k, v, out, scale, bh, n, m, workspace, s);
   }
   if (masked)
-    return bf ? flash_launch_typed<__nv_bfloat16, false, true>(q, k, v, out, scale, bh, n, m, s)
-              : flash_launch_typed<__half, false, true>(q, k, v, out, scale, bh, n, m, s);
-  return bf ? flash_launch_typed<__nv_bfloat16, false, false>(q, k, v, out, scale, bh, n, m, s)
-            : flash_launch_typed<__half, false, false>(q, k, v, out, scale, bh, n, m, s);
+    return bf ? flash_launch_typed<__nv_bfloat16, false, true>(q, k, v, out, scale, bh, n, m, workspace, s)
+              : flash_launch_typed<__half, false, true>(q, k, v, out, scale, bh, n, m, workspace, s);
+  return bf ? flash_launch_typed<__nv_bfloat16, false, false>(q, k, v, out, scale, bh, n, m, workspace, s)
+            : flash_launch_typed<__half, false, false>(q, k, v, out, scale, bh, n, m, workspace, s);
 }
 
 }  // namespace dfss

@@ -21,6 +21,8 @@
 // tmem_e_frg TF32 atom, mma_traits_sm100.hpp:612-621): lane 16 m2 + 8 k1 + m0 holds pairs
 // 4 k1 .. 4 k1 + 3 of rows 16 m2 + m0 (bits 0-15) and 16 m2 + 8 + m0 (bits 16-31).
 // Q is single-buffered (2 x 32 KB) to fit two-stage K and V rings in shared memory.
+#include <type_traits>
+
 #include "flash_common.cuh"
 
 namespace dfss {
@@ -40,7 +42,8 @@ constexpr int F_K = F_Q + 2 * Q_BYTES;
 constexpr int F_V = F_K + KST * KV_BYTES;
 constexpr int F_RED = F_V + VST * KV_BYTES;   // red_max / red_sum [2 halves][2 pairs][128]
 constexpr int F_BAR = F_RED + 2 * 2 * 2 * BM * 4;
-constexpr int F_TOTAL = F_BAR + 512 + 1024;
+constexpr int F_LIVE = F_BAR + 512;           // BlockMask step bitmap + row-block order (sized at launch)
+constexpr int F_TOTAL = F_LIVE + 1024;
 constexpr int RING = 3;
 constexpr int T_O = RING * BN;
 constexpr float kLog2e = 1.4426950408889634f;
@@ -135,6 +138,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int iblocks = n / (2 * BM);
   const int items = bh * iblocks;
   const int ntiles = n / BN;
+  // BlockMask step skipping and the cost-ranked snake schedule: exactly as dfss_flash2_kernel
+  // (flash_tc.cu), which documents the scheme
+  uint32_t* s_live = (uint32_t*)(smem + F_LIVE);
+  int* s_order = (int*)(s_live + (n / BM) * tmask.sbw);
+  if (MASKED) {
+    for (int i = threadIdx.x; i < (n / BM) * tmask.sbw; i += blockDim.x) s_live[i] = __ldg(tmask.sbits + i);
+    for (int i = threadIdx.x; i < iblocks; i += blockDim.x) s_order[i] = __ldg(tmask.order + i);
+  }
+  auto pos_at = [&](int k) -> int {
+    const int g = gridDim.x;
+    return k * g + (MASKED && (k & 1) ? g - 1 - (int)blockIdx.x : (int)blockIdx.x);
+  };
+  auto item_of = [&](int p) -> int {
+    if (!MASKED) return p;
+    const int info = s_order[p / bh], r0 = (info >> 8) & 255, m = info >> 16, o = p - r0 * bh;
+    return (o / m) * iblocks + (s_order[r0 + o % m] & 255);
+  };
+  auto live_words = [&](int ib, int t, uint32_t& w0, uint32_t& w1) {
+    if (MASKED && (t & 31) == 0) {
+      w0 = s_live[(ib * 2) * tmask.sbw + (t >> 5)];
+      w1 = s_live[(ib * 2 + 1) * tmask.sbw + (t >> 5)];
+    }
+  };
+  auto bit_u = [&](uint32_t w, int t) { return !MASKED || __any_sync(0xffffffffu, (w >> (t & 31)) & 1u); };
 
   if (warp == W_QK && lane == 0) {
     tc::prefetch_tmap(&tm_q);
@@ -173,7 +200,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int ks = 0, vs = 0, it = 0;
       uint32_t kph = 0, vph = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      for (int kk_ = 0, pos = pos_at(0); pos < items; pos = pos_at(++kk_), ++it) {
+        const int item = item_of(pos);
+        uint32_t lw0 = 0, lw1 = 0;
         const int b = item / iblocks, ib = item % iblocks;
         tc::mbar_wait_sleep(q_empty, (it & 1) ^ 1);
         tc::mbar_arrive_expect_tx(q_full, 2 * Q_BYTES);
@@ -181,6 +210,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int a = 0; a < 2; ++a)
             tc::tma_load_3d(smem + F_Q + h * Q_BYTES + a * ATOM, &tm_q, q_full, 32 * a, (ib * 2 + h) * BM, b);
         for (int t = 0; t < ntiles; ++t) {
+          live_words(ib, t, lw0, lw1);
+          if (MASKED && !(((lw0 | lw1) >> (t & 31)) & 1u)) continue;
           tc::mbar_wait_sleep(&k_empty[ks], kph ^ 1);
           tc::mbar_arrive_expect_tx(&k_full[ks], KV_BYTES);
           for (int a = 0; a < 2; ++a)
@@ -200,13 +231,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       constexpr uint32_t idesc_s = tc::instr_desc(2, BM, BN, false, false, false);
       int ks = 0, it = 0, sb = 0;
       uint32_t kph = 0, sph = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      for (int kk_ = 0, pos = pos_at(0); pos < items; pos = pos_at(++kk_), ++it) {
+        const int item = item_of(pos);
+        uint32_t lw0 = 0, lw1 = 0;
+        const int ib = item % iblocks;
         tc::mbar_wait_sleep(q_full, it & 1);
         for (int t = 0; t < ntiles; ++t) {
+          live_words(ib, t, lw0, lw1);
+          const bool lv[2] = {bit_u(lw0, t), bit_u(lw1, t)};
+          if (MASKED && !lv[0] && !lv[1]) continue;
           tc::mbar_wait_sleep(&k_full[ks], kph);
           const uint32_t k_addr = tc::smem_u32(smem + F_K + ks * KV_BYTES);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
+            if (MASKED && !lv[h]) continue;
             tc::mbar_wait_sleep(&s_free[sb], sph ^ 1);
             tc::tc_fence_after();
             const uint32_t q_addr = tc::smem_u32(smem + F_Q + h * Q_BYTES);
@@ -232,13 +270,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int h = warp == W_PV ? 0 : 1;
       constexpr uint32_t idesc_pv = tc::instr_desc(2, BM, HD, false, false, true);  // B = V^T, K-major
       int vs = 0, it = 0;
-      uint32_t vph = 0, gt = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+      uint32_t vph = 0, gcount = 0, pbits = 0;  // live steps so far (both halves); p_full phase per slot
+      for (int kk_ = 0, pos = pos_at(0); pos < items; pos = pos_at(++kk_), ++it) {
+        const int item = item_of(pos);
+        uint32_t lw0 = 0, lw1 = 0;
+        const int ib = item % iblocks;
         tc::mbar_wait_sleep(&o_empty[h], (it & 1) ^ 1);
-        for (int t = 0; t < ntiles; ++t, ++gt) {
-          const uint32_t g = 2 * gt + h, slot = g % RING;
+        bool first = true;
+        for (int t = 0; t < ntiles; ++t) {
+          live_words(ib, t, lw0, lw1);
+          const bool l0 = bit_u(lw0, t), l1 = bit_u(lw1, t);
+          if (MASKED && !l0 && !l1) continue;  // tile not loaded
+          const uint32_t g = gcount + (h ? (uint32_t)l0 : 0u), slot = g % RING;
+          gcount += (uint32_t)l0 + (uint32_t)l1;
+          if (MASKED && !(h ? l1 : l0)) {  // this half masked here: release the V stage unused (after its load)
+            tc::mbar_wait_sleep(&v_full[vs], vph);
+            if (lane == 0) tc::mbar_arrive(&v_empty[vs]);
+            if (++vs == VST) { vs = 0; vph ^= 1; }
+            continue;
+          }
           tc::mbar_wait_sleep(&v_full[vs], vph);
-          tc::mbar_wait_sleep(&p_full[h * RING + slot], (gt / RING) & 1);
+          tc::mbar_wait_sleep(&p_full[h * RING + slot], (pbits >> slot) & 1);
+          pbits ^= 1u << slot;
           tc::tc_fence_after();
           const uint32_t v_addr = tc::smem_u32(smem + F_V + vs * KV_BYTES);
           const uint32_t s_col = tmem_base + slot * BN;
@@ -249,9 +302,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               // B: keys 32q + 16j .. +16 of V^T (K-major): atom q, 64-byte offset j inside its 128B rows
               const uint64_t bd = tc::smem_desc(v_addr + q * VT_ATOM + 64 * j, 16, 1024, tc::kSwizzle128B);
               mma_sp_tf32_ts_w(tmem_base + T_O + h * HD, s_col + 32 * q + 16 + 8 * j, bd, s_col + 32 * q + 4 * j,
-                               idesc_pv, (t > 0 || q > 0 || j > 0) ? 1u : 0u);
+                               idesc_pv, (!first || q > 0 || j > 0) ? 1u : 0u);
             }
           }
+          first = false;
           tc::mma_commit_w(&s_free[slot]);
           tc::mma_commit_w(&v_empty[vs]);
           tc::mma_commit_w(&pv_done[h]);
@@ -271,19 +325,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const float c = scale * kLog2e;
     float* rmax = red_max + h * 2 * BM;
     float* rsum = red_sum + h * 2 * BM;
-    uint32_t gt = 0, scol = 0;
+    uint32_t gcount = 0, hcount = 0, scol = 0;
     int it = 0;
     bool cm[2] = {false, false};
     auto row_max = [&]() {
       float mt = -INFINITY;
 #pragma unroll
       for (int ch = 0; ch < 2; ++ch) {
-        if (cm[ch]) continue;
         uint32_t s[32];
         tc::tmem_ld_32x32b_x32(scol + 32 * ch, s);
         tc::tmem_ld_wait(s);
+        float mc = -INFINITY;
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) mt = fmaxf(mt, fmaxf(__uint_as_float(s[j]), __uint_as_float(s[j + 1])));
+        for (int j = 0; j < 32; j += 2) mc = fmaxf(mc, fmaxf(__uint_as_float(s[j]), __uint_as_float(s[j + 1])));
+        if (!cm[ch]) mt = fmaxf(mt, mc);
       }
       rmax[pr * BM + r] = mt;
       tc::named_bar_sync(pbar, 64);
@@ -294,6 +349,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     bool pend = false;
     int pend_b = 0, pend_ib = 0, pend_it = 0;
     float pend_l = 0.f;
+    auto cword = [&](int pos_) -> uint32_t {  // chunk-keep word `lane` of this warp's strip
+      if (!MASKED || pos_ >= items || (int)lane >= tmask.cbw) return 0u;
+      const int strip = ((item_of(pos_) % iblocks) * 2 + h) * (BM / 32) + quad;
+      return __ldg(tmask.cbits + (int64_t)strip * tmask.cbw + lane);
+    };
+    uint32_t cw = cword(pos_at(0));
     auto epilogue = [&]() {
       rsum[pr * BM + r] = pend_l;
       tc::named_bar_sync(pbar, 64);
@@ -315,42 +376,60 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                               __uint_as_float(o[4 * j + 2]) * inv, __uint_as_float(o[4 * j + 3]) * inv);
       pend = false;
     };
-    for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+    for (int kk_ = 0, pos = pos_at(0); pos < items; pos = pos_at(++kk_), ++it) {
+        const int item = item_of(pos);
+        uint32_t lw0 = 0, lw1 = 0;
       const int b = item / iblocks, ib = item % iblocks;
+      const uint32_t cwn = cword(pos_at(kk_ + 1));
       float mlog = 0.f, l0 = 0.f, l1 = 0.f;
-      for (int t = 0; t < ntiles; ++t, ++gt) {
-        const uint32_t g = 2 * gt + h;
+      bool first = true;
+      for (int t = 0; t < ntiles; ++t) {
+        live_words(ib, t, lw0, lw1);
+        const bool lv0 = bit_u(lw0, t), lv1 = bit_u(lw1, t);
+        const uint32_t g = gcount + (h ? (uint32_t)lv0 : 0u);  // global live step
+        gcount += (uint32_t)lv0 + (uint32_t)lv1;
+        if (MASKED && !(h ? lv1 : lv0)) continue;
+        ++hcount;
         const uint32_t slot = g % RING;
         scol = lane_base + slot * BN + 64 * pr;
         tc::mbar_wait(&s_full[slot], (g / RING) & 1);
         tc::tc_fence_after();
-        const int row0 = (ib * 2 + h) * BM + quad * 32, col0 = t * BN + 64 * pr;
-        cm[0] = MASKED && tmask.masked(row0, col0);
-        cm[1] = MASKED && tmask.masked(row0, col0 + 32);
-        if (t == 0) mlog = row_max();
+        bool anym = false;
+        if (MASKED) {
+          const int c32 = 4 * t + 2 * pr;
+          const uint32_t w = __shfl_sync(0xffffffffu, cw, c32 >> 5) >> (c32 & 31);
+          cm[0] = !(w & 1u);
+          cm[1] = !(w & 2u);
+          anym = __any_sync(0xffffffffu, (~w & 3u) != 0);
+        }
+        if (first) mlog = row_max();
         uint32_t p[2][16], W[2][2];
         float lt0 = 0.f, lt1 = 0.f;
-        auto compute = [&]() {
+        auto compute = [&](auto masked_variant) {
+          constexpr bool MV = decltype(masked_variant)::value;
           lt0 = lt1 = 0.f;
 #pragma unroll
           for (int ch = 0; ch < 2; ++ch) {
             float a0, a1;
-            if (cm[ch]) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j) p[ch][j] = 0u;
-              W[ch][0] = W[ch][1] = 0x44444444u;
-              continue;
-            }
             uint32_t s[32];
             tc::tmem_ld_32x32b_x32(scol + 32 * ch, s);
             tc::tmem_ld_wait(s);
             prune12_chunk(s, c, mlog, p[ch], W[ch][0], W[ch][1], a0, a1);
+            if (MV && cm[ch]) {  // masked chunk: structurally absent
+#pragma unroll
+              for (int j = 0; j < 16; ++j) p[ch][j] = 0u;
+              W[ch][0] = W[ch][1] = 0x44444444u;
+              a0 = a1 = 0.f;
+            }
             add2(lt0, lt1, a0, a1, lt0, lt1);
           }
         };
-        compute();
-        if (t > 0 && bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit))) {
-          tc::mbar_wait(&pv_done[h], (gt - 1) & 1);
+#pragma unroll 1
+        for (int pass = 0;; ++pass) {
+          if (MASKED && anym) compute(std::true_type{});
+          else compute(std::false_type{});
+          if (pass > 0 || first || !bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit))) break;
+          tc::mbar_wait(&pv_done[h], (hcount - 2) & 1);
           tc::tc_fence_after();
           const float mnew = fmaxf(mlog, row_max());
           const float f = fex2(mlog - mnew);
@@ -368,7 +447,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           tc::tmem_st_wait();
           mlog = mnew;
-          compute();
         }
         add2(l0, l1, lt0, lt1, l0, l1);
 #pragma unroll
@@ -387,6 +465,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&p_full[h * RING + slot]);
+        first = false;
         if (pend) epilogue();
       }
       pend = true;
@@ -394,6 +473,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       pend_ib = ib;
       pend_it = it;
       pend_l = l0 + l1;
+      cw = cwn;
     }
     if (pend) epilogue();
   }
@@ -421,11 +501,18 @@ __global__ void __launch_bounds__(256) transpose_v_kernel(const float* __restric
 
 bool tc_flash_tf32_supported(int gs, int n, int d) { return gs == 2 && d == HD && n > 0 && n % (2 * BM) == 0; }
 
+static int64_t vt_bytes(int64_t bh, int n) { return (bh * (int64_t)n * HD * 4 + 255) / 256 * 256; }
+
+int64_t flash_tf32_workspace_bytes(int64_t bh, int n, bool masked) {
+  return vt_bytes(bh, n) + (masked ? flash_mask_workspace_bytes(n) : 0);
+}
+
 cudaError_t launch_flash_tf32(const void* q, const void* k, const void* v, void* out, float scale, int64_t bh, int n,
                               int d, const uint8_t* tile_keep, int tile_rows, int tile_cols, void* vt_scratch,
                               cudaStream_t s) {
   if (!tc_flash_tf32_supported(2, n, d)) return cudaErrorNotSupported;
-  if (tile_keep && !tc_flash_mask_supported(tile_rows, tile_cols)) return cudaErrorNotSupported;
+  if (tile_keep && (!tc_flash_mask_supported(tile_rows, tile_cols) || !flash_mask_two_set_ok(n)))
+    return cudaErrorNotSupported;
   if (bh == 0) return cudaSuccess;
   const CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   CUtensorMap tq, tk, tv;
@@ -449,15 +536,19 @@ cudaError_t launch_flash_tf32(const void* q, const void* k, const void* v, void*
   transpose_v_kernel<<<dim3(n / 32, (unsigned)bh), 256, 0, s>>>((const float*)v, (float*)vt_scratch, n);
   TileMask m{tile_keep, tile_keep ? tile_rows : 1, tile_keep ? tile_cols : 1,
              tile_keep ? (n + tile_cols - 1) / tile_cols : 1};
+  // workspace: V^T, then the block-mask bitmaps (flash_tf32_workspace_bytes)
+  if (tile_keep) prepare_mask_bits(m, n, (char*)vt_scratch + vt_bytes(bh, n), s);
   auto kern = tile_keep ? dfss_flash_tf32_kernel<true> : dfss_flash_tf32_kernel<false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, F_TOTAL);
+  const int smem_total = F_TOTAL + (tile_keep ? flash_mask_smem_bytes(n) : 0);
+  if (smem_total > 227 * 1024) return cudaErrorNotSupported;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_total);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t items = bh * (n / (2 * BM));
   const int grid = (int)(items < sms ? items : sms);
-  kern<<<grid, NUM_THREADS, F_TOTAL, s>>>(tq, tk, tv, (float*)out, scale, (int)bh, n, m);
+  kern<<<grid, NUM_THREADS, smem_total, s>>>(tq, tk, tv, (float*)out, scale, (int)bh, n, m);
   return cudaGetLastError();
 }
 

@@ -628,3 +628,23 @@ def test_heatmap_kept_entries_dominate_dense():
         pair = dfss.attention_heatmap(dfss.AttentionInputs(q, k, v), mode)
         kept = pair.sparse.data != 0
         assert bool((pair.sparse.data[kept] >= pair.dense.data[kept] - 1e-6).all())
+
+
+def test_tf32_12_block_mask_whole_steps_skipped():
+    """tf32 kernel with whole 128 x 128 steps masked (block-causal + dead blocks), steps dead
+    for one half only, several items per CTA."""
+    n, tr, tc_ = 1024, 32, 64
+    rng = np.random.default_rng(12)
+    keep = _block_causal_keep(n, tr, tc_)
+    blocks = rng.random((n // 128, n // 128)) < 0.3
+    np.fill_diagonal(blocks, False)
+    keep &= ~np.kron(blocks, np.ones((128 // tr, 128 // tc_), dtype=bool))
+    keep[:, :2] &= rng.random((keep.shape[0], 2)) < 0.5   # partially masked live steps too
+    keep[np.arange(keep.shape[0]), np.arange(keep.shape[0]) * tr // tc_] = True  # diagonal tile: no empty row
+    mask = dfss.BlockMask(keep, tile_rows=tr, tile_cols=tc_)
+    g = torch.Generator().manual_seed(13)
+    q, k, v = (torch.randn((2, 80, n, 64), generator=g).cuda() for _ in range(3))   # 320 items > 148 CTAs
+    out = _np(dfss.dfss_attention(q, k, v, "1:2", math_mode="tf32", block_mask=mask))
+    for b, h in [(0, 0), (1, 41), (1, 79)]:
+        qq, kk, vv = (_tf32(x[b, h].cpu().numpy()) for x in (q, k, v))
+        assert_close(out[b, h], _masked_oracle(qq, kk, vv, mask, "1:2"), 2e-2, 2e-2, f"tf32 block-causal ({b},{h})")

@@ -10,8 +10,10 @@ timeout -s KILL 600 $NCU --metrics gpu__time_duration.sum --clock-control none -
    --log-file gpurun_out/launches_${TAG}_${CFG}.csv python bench.py --config $CFG --steps 2 --warmup 3 --no-extra \
    > gpurun_out/launches_${TAG}_${CFG}.log 2>&1
 done
+for CFG in c2 c4; do
 timeout -s KILL 900 $NCU --set full --clock-control none --import-source on -k regex:dfss_flash -s 3 -c 1 \
-   -o gpurun_out/prof_${TAG}_c4_flash python bench.py --config c4 --steps 1 --warmup 3 --no-extra \
-   > gpurun_out/prof_${TAG}_c4_flash.log 2>&1
+   -o gpurun_out/prof_${TAG}_${CFG}_flash python bench.py --config $CFG --steps 1 --warmup 3 --no-extra \
+   > gpurun_out/prof_${TAG}_${CFG}_flash.log 2>&1
+done
 echo "rc=$?"
 ls -la gpurun_out/

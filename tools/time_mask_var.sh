@@ -3,4 +3,3 @@
 export PYTHONPATH=.
 python tools/time_mask.py
 for v in ${VARIANTS:-4096}; do echo "variant $v"; DFSS_FLASH_VARIANT=$v python tools/time_mask.py; done
-for e in ${EXPS}; do echo "exp $e"; DFSS_LIB=paper_2203_00091_b200/lib/exp/lib_$e.so python tools/time_mask.py; done

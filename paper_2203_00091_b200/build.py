@@ -49,7 +49,8 @@ def _stale(target: str, deps: list[str]) -> bool:
 def _compile(src: str, force: bool) -> str:
     obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
     if force or _stale(obj, [src] + _headers()):
-        cmd = [nvcc(), *NVCC_FLAGS, "-c", src, "-o", obj]
+        # DFSS_NVCC_EXTRA: extra nvcc flags for bring-up builds (e.g. -DDFSS_FLASH_TRACE_BUILD)
+        cmd = [nvcc(), *NVCC_FLAGS, *os.environ.get("DFSS_NVCC_EXTRA", "").split(), "-c", src, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{res.stdout}\n{res.stderr}")

@@ -476,13 +476,21 @@ static_assert(T2_O + 2 * HD <= 512, "TMEM budget");
 static_assert(S2_TOTAL <= 227 * 1024, "shared memory budget");
 }  // namespace
 
-// bring-up timeline (DFSS_FLASH_TRACE=<file>): clock64 at pipeline events of CTA 0, first 2 items
+// bring-up timeline (DFSS_FLASH_TRACE=<file>): clock64 at pipeline events of CTA 0, first 2
+// items.  Compiled in only with -DDFSS_FLASH_TRACE_BUILD (DFSS_NVCC_EXTRA, tools/trace_flash.py):
+// the per-lane trace predicates cost ~5 % issue slots in the epilogue-bound kernel.
 __device__ unsigned long long* g_flash_trace = nullptr;
+#ifdef DFSS_FLASH_TRACE_BUILD
 #define FTRACE(slot, it_, t_, h_)                                                                  \
   do {                                                                                             \
     if (trace && (it_) < 2 && (t_) < 64)                                                           \
       trace[((((slot) * 2 + (it_)) * 64 + (t_)) * 2 + (h_))] = clock64();                          \
   } while (0)
+#else
+#define FTRACE(slot, it_, t_, h_) \
+  do {                            \
+  } while (0)
+#endif
 
 template <typename T, bool PAIRS, bool MASKED>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -513,7 +521,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const uint32_t warp = tc::warp_id();
   const uint32_t lane = threadIdx.x & 31;
+#ifdef DFSS_FLASH_TRACE_BUILD
   unsigned long long* trace = blockIdx.x == 0 ? g_flash_trace : nullptr;
+#endif
   const int iblocks = n / (2 * BM);
   const int items = bh * iblocks;
   const int ntiles = n / BN;
@@ -732,7 +742,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const float c = scale * kLog2e;
     float* rmax = red_max + h * 2 * BM;
     float* rsum = red_sum + h * 2 * BM;
-    const bool tw = quad == 0 && pr == 0 && lane == 0;
+    [[maybe_unused]] const bool tw = quad == 0 && pr == 0 && lane == 0;
     uint32_t gcount = 0, hcount = 0, scol = 0;  // live steps (both halves / this half); this warp's S column
     int it = 0;
     // maximum of this row over the set's 128 columns of the current S (both warps of the pair)

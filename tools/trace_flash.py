@@ -1,4 +1,7 @@
-"""Run one c4-shaped dfss_attention with DFSS_FLASH_TRACE and print the CTA-0 pipeline timeline (bring-up)."""
+"""Run one c4-shaped dfss_attention with DFSS_FLASH_TRACE and print the CTA-0 pipeline timeline (bring-up).
+
+Needs a trace build: DFSS_NVCC_EXTRA=-DDFSS_FLASH_TRACE_BUILD python -c "from paper_2203_00091_b200 import build; build.build(force=True)"
+"""
 import os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

@@ -571,6 +571,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     return !MASKED || __any_sync(0xffffffffu, (w >> (t & 31)) & 1u);
   };
 
+  if (threadIdx.x == 0) FTRACE(15, 0, 0, 0);  // CTA start
   if (warp == W_QK && lane == 0) {
     tc::prefetch_tmap(&tm_q);
     tc::prefetch_tmap(&tm_k);
@@ -602,6 +603,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) FTRACE(15, 0, 1, 0);  // setup done
 
   if (warp == W_QK) {
     // ------------------------------------------------------------ TMA producer: Q (both halves), K (keys permuted), V
@@ -921,6 +923,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc::tc_fence_after();
     tc::tmem_dealloc<512>(tmem_base);
   }
+  if (threadIdx.x == 0) FTRACE(15, 1, 0, 0);  // CTA end
 }
 
 // BlockMask tile grid -> step / chunk bitmaps (TileMask::sbits / cbits) for the two-set

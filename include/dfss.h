@@ -138,8 +138,10 @@ int dfss_spmm(const void* p, const uint32_t* meta_hw, const void* v, void* out, 
  */
 int64_t dfss_nm_attention_workspace_bytes(int mode, int dtype, int64_t bh, int n, int d);
 /* Exact workspace for the path dfss_nm_attention(_masked) will take with these arguments:
- * 0 for the fused 16-bit kernel, bh*n*d*4 (V^T) for the fused tf32 kernel, the staged
- * bytes above otherwise.  masked != 0 when a tile_keep grid will be passed. */
+ * 0 for the fused 16-bit kernel (masked: the step / chunk liveness bitmaps and the
+ * row-block schedule, a few KB), bh*n*d*4 (V^T) for the fused tf32 kernel (+ the same
+ * bitmaps when masked), the staged bytes above otherwise.  masked != 0 when a tile_keep grid
+ * will be passed. */
 int64_t dfss_nm_attention_workspace_bytes_for(int mode, int dtype, int math, int64_t bh, int n, int d,
                                               int tile_rows, int tile_cols, int masked);
 int dfss_nm_attention(const void* q, const void* k, const void* v, void* out, int mode, int dtype, int math,
@@ -149,8 +151,11 @@ int dfss_nm_attention(const void* q, const void* k, const void* v, void* out, in
  * nm_attention with a BlockMask (pipeline.py:15-32 with block_mask; mask threaded as in
  * fused.py:73-82 and sparse_ops.py:27-30,57-64): tile_keep is the DEVICE uint8 grid
  * [ceil(n/tile_rows)][ceil(n/tile_cols)] shared by every (batch, head); masked tiles are
- * structurally absent.  16-bit inputs with tile_rows and tile_cols multiples of 32 run the
- * fused kernel (masked 32x32 chunks skipped); other shapes run the staged kernels.  Rows whose
+ * structurally absent.  16-bit inputs (and fp32 with math = TF32) with tile_rows and
+ * tile_cols multiples of 32 run the fused kernel: masked 32x32 chunks are absent, 128x128
+ * steps with no kept tile are skipped entirely (no K/V load, no MMA), and the 256-row items
+ * are scheduled heaviest-first; two small pre-kernels build the liveness bitmaps in the
+ * workspace (dfss_nm_attention_workspace_bytes_for).  Other shapes run the staged kernels.  Rows whose
  * tiles are all masked are undefined here -- the host layer rejects them first, as the
  * reference's softmax_rows does ("empty row N").  tile_keep == NULL is dfss_nm_attention.
  */

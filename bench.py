@@ -44,13 +44,13 @@ CONFIGS = {
 }
 # configs[4]: the sequence sweep, batch 8 x 12 heads (SURVEY §8(d) proposal), reported in the
 # default line's "sweep" object: 2:4 bf16 and 1:2 bf16 (fused kernel), 1:2 tf32 (fused tf32
-# kernel, n % 256 == 0) and, for reference, 1:2 exact FP32 (staged FFMA kernels)
+# kernel) and, for reference, 1:2 exact FP32 (staged FFMA kernels)
 for _n in (384, 512, 768, 1024, 2048, 4096):
     CONFIGS[f"c5_24_{_n}"] = dict(batch=8, heads=12, seq=_n, d=64, mode="2:4", dtype="bfloat16",
                                   desc=f"sweep 2:4 bf16, batch 8, 12 heads, seq {_n}")
     CONFIGS[f"c5_12_{_n}"] = dict(batch=8, heads=12, seq=_n, d=64, mode="1:2", dtype="bfloat16",
                                   desc=f"sweep 1:2 bf16, batch 8, 12 heads, seq {_n}")
-    if _n % 256 == 0:
+    if _n % 128 == 0:
         CONFIGS[f"c5_12tf32_{_n}"] = dict(batch=8, heads=12, seq=_n, d=64, mode="1:2", dtype="float32", math="tf32",
                                           desc=f"sweep 1:2 tf32 (fp32 inputs), batch 8, 12 heads, seq {_n}")
     if _n <= 1024:

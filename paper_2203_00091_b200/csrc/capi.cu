@@ -183,7 +183,7 @@ int dfss_nm_attention_masked(const void* q, const void* k, const void* v, void* 
     return cuda_status(dfss::launch_flash_tf32(q, k, v, out, scale, bh, n, d, tile_keep, tile_rows, tile_cols,
                                                workspace, (cudaStream_t)stream));  // V^T in the workspace
   if (math == DFSS_MATH_TF32)
-    return fail(DFSS_ERR_UNSUPPORTED, "tf32 attention needs fp32 inputs, mode 1:2, d = 64 and n % 256 == 0");
+    return fail(DFSS_ERR_UNSUPPORTED, "tf32 attention needs fp32 inputs, mode 1:2, d = 64 and n % 128 == 0");
   if (tile_keep) {
     // staged with the mask threaded through every stage (fused.py:73-82, sparse_ops.py:27-30,57-64)
     int st = dfss_sddmm_prune(q, k, nz, meta, scale, mode, dtype, dtype, math, bh, n, n, d, tile_keep, tile_rows,

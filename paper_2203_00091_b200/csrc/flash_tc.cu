@@ -506,8 +506,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* k_empty = k_full + K2ST;      // [K2ST]
   uint64_t* v_full = k_empty + K2ST;      // [V2ST]
   uint64_t* v_empty = v_full + V2ST;      // [V2ST]
-  uint64_t* s_full = v_empty + V2ST;      // [S2RING] S of a step computed
-  uint64_t* s_free = s_full + S2RING;     // [S2RING] PV of that step retired (buffer free)
+  // [2 halves][S2RING] S of a step computed.  Per half, like p_full: when one set runs several
+  // live steps in a row (masks, an empty half) a shared slot barrier could complete two phases
+  // past a waiting set, whose parity wait would then succeed on the wrong step.
+  uint64_t* s_full = v_empty + V2ST;
+  uint64_t* s_free = s_full + 2 * S2RING; // [S2RING] PV of that step retired (buffer free)
   // [2 halves][S2RING] P + metadata of a step written (8 warps).  Per half, not per slot only:
   // each PV issuer may run a step ahead of the other set, and a shared slot barrier would
   // then satisfy its wait with the other set's previous phase (parity aliasing).
@@ -583,10 +586,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc::mbar_init(&o_empty[i], 8);
       tc::mbar_init(&pv_done[i], 1);
     }
-    for (int i = 0; i < S2RING; ++i) {
-      tc::mbar_init(&s_full[i], 1);
-      tc::mbar_init(&s_free[i], 1);
-    }
+    for (int i = 0; i < S2RING; ++i) tc::mbar_init(&s_free[i], 1);
+    for (int i = 0; i < 2 * S2RING; ++i) tc::mbar_init(&s_full[i], 1);
     for (int i = 0; i < 2 * S2RING; ++i) tc::mbar_init(&p_full[i], 8);
     for (int i = 0; i < K2ST; ++i) {
       tc::mbar_init(&k_full[i], 1);
@@ -671,7 +672,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 tc::mma_f16_ss_w(tmem_base + sb * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
               }
             }
-            tc::mma_commit_w(&s_full[sb]);
+            tc::mma_commit_w(&s_full[h * S2RING + sb]);
             if (lane == 0) FTRACE(5, it, t, h);
             if (++sb == S2RING) { sb = 0; sph ^= 1; }
           }
@@ -694,7 +695,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int item = item_of(pos);
         uint32_t lw0 = 0, lw1 = 0;
         const int ib = item % iblocks;
-        wait_role(variant, &o_empty[h], (it & 1) ^ 1);
+        // O_h free (previous item drained) is awaited only before the first PV MMA of the item --
+        // or before o_full when the half has no live step: a set whose first live step comes late
+        // drains the previous item only then, and the V stages of the steps before it must be
+        // released meanwhile or the producer stalls (deadlock on one-sided masks).
+        bool o_free = false;
+        auto await_o_free = [&]() {
+          if (!o_free) wait_role(variant, &o_empty[h], (it & 1) ^ 1);
+          o_free = true;
+        };
         bool first = true;  // first live step of this half-item initialises O_h
         for (int t = 0; t < ntiles; ++t) {
           live_words(ib, t, lw0, lw1);
@@ -710,6 +719,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (++vs == V2ST) { vs = 0; vph ^= 1; }
             continue;
           }
+          await_o_free();
           wait_role(variant, &v_full[vs], vph);
           wait_role(variant, &p_full[h * S2RING + slot], (pbits >> slot) & 1);
           pbits ^= 1u << slot;
@@ -730,6 +740,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (lane == 0) FTRACE(7, it, t, h);
           if (++vs == V2ST) { vs = 0; vph ^= 1; }
         }
+        await_o_free();
         tc::mma_commit_w(&o_full[h]);
       }
     }
@@ -745,7 +756,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     float* rmax = red_max + h * 2 * BM;
     float* rsum = red_sum + h * 2 * BM;
     [[maybe_unused]] const bool tw = quad == 0 && pr == 0 && lane == 0;
-    uint32_t gcount = 0, hcount = 0, scol = 0;  // live steps (both halves / this half); this warp's S column
+    uint32_t gcount = 0, hcount = 0, scol = 0, sfbits = 0;  // live steps (both halves / this half); this warp's S column
     int it = 0;
     // maximum of this row over the set's 128 columns of the current S (both warps of the pair)
     bool cm[2] = {false, false};  // this warp's two chunks of the current tile masked (BlockMask)
@@ -817,7 +828,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ++hcount;
         const uint32_t slot = g % S2RING;
         scol = lane_base + slot * BN + 64 * pr;
-        tc::mbar_wait(&s_full[slot], (g / S2RING) & 1);
+        tc::mbar_wait(&s_full[h * S2RING + slot], (sfbits >> slot) & 1);  // k-th use of (h, slot): parity k & 1
+        sfbits ^= 1u << slot;
         if (tw) FTRACE(0, it, t, h);
         tc::tc_fence_after();
         bool anym = false;  // a chunk of this warp masked (uniform): the masked compute variant
@@ -908,6 +920,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       // the epilogue of this item runs after step 0 of the next one (below), so the wait for
       // the item's last PV overlaps that step instead of idling the set at every item boundary
+      if (pend) epilogue();  // the previous item's, if this item had no live step for this set
       pend = true;
       pend_b = b;
       pend_ib = ib;
@@ -949,12 +962,13 @@ __global__ void mask_bits_kernel(TileMask m, int n, uint32_t* __restrict__ sbits
 
 // row blocks (256 rows, one two-set item) ranked by live steps, heaviest first (ties: lower
 // block first); one thread per row block, n <= 32768
-__global__ void mask_order_kernel(const uint32_t* __restrict__ sbits, int sbw, int iblocks, int* __restrict__ order) {
+__global__ void mask_order_kernel(const uint32_t* __restrict__ sbits, int sbw, int nrows, int iblocks,
+                                  int* __restrict__ order) {
   __shared__ int cost[128];
   const int i = threadIdx.x;
-  if (i < iblocks) {
+  if (i < iblocks) {  // (the last block's second half may lie beyond n: rows n / 128 of sbits)
     int c = 0;
-    for (int w = 0; w < 2 * sbw; ++w) c += __popc(sbits[2 * i * sbw + w]);
+    for (int w = 0; w < 2 * sbw && (2 * i * sbw + w) < nrows * sbw; ++w) c += __popc(sbits[2 * i * sbw + w]);
     cost[i] = c;
   }
   __syncthreads();
@@ -974,12 +988,12 @@ static int mask_cbw(int n) { return (n / 32 + 31) / 32; }
 static int64_t mask_words(int n) { return (int64_t)(n / BM) * mask_sbw(n) + (int64_t)(n / 32) * mask_cbw(n); }
 
 int64_t flash_mask_workspace_bytes(int n) {
-  return ((mask_words(n) + n / (2 * BM)) * 4 + 255) / 256 * 256;  // bitmaps + row-block order
+  return ((mask_words(n) + (n + 2 * BM - 1) / (2 * BM)) * 4 + 255) / 256 * 256;  // bitmaps + row-block order
 }
 
-bool flash_mask_two_set_ok(int n) { return n % (2 * BM) == 0 && mask_cbw(n) <= 32; }
+bool flash_mask_two_set_ok(int n) { return n % BM == 0 && mask_cbw(n) <= 32; }
 
-int flash_mask_smem_bytes(int n) { return ((n / BM) * mask_sbw(n) + n / (2 * BM)) * 4; }
+int flash_mask_smem_bytes(int n) { return ((n / BM) * mask_sbw(n) + (n + 2 * BM - 1) / (2 * BM)) * 4; }
 
 void prepare_mask_bits(TileMask& m, int n, void* workspace, cudaStream_t s) {
   m.sbw = mask_sbw(n);
@@ -989,7 +1003,7 @@ void prepare_mask_bits(TileMask& m, int n, void* workspace, cudaStream_t s) {
   m.order = (const int*)(m.sbits + mask_words(n));
   const int64_t bits = mask_words(n) * 32;
   mask_bits_kernel<<<(unsigned)((bits + 255) / 256), 256, 0, s>>>(m, n, (uint32_t*)m.sbits, (uint32_t*)m.cbits);
-  mask_order_kernel<<<1, 128, 0, s>>>(m.sbits, m.sbw, n / (2 * BM), (int*)m.order);
+  mask_order_kernel<<<1, 128, 0, s>>>(m.sbits, m.sbw, n / BM, (n + 2 * BM - 1) / (2 * BM), (int*)m.order);
 }
 
 bool tc_flash_supported(int gs, int dtype, int n, int d) {

@@ -123,8 +123,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* k_empty = k_full + KST;      // [KST]
   uint64_t* v_full = k_empty + KST;      // [VST]
   uint64_t* v_empty = v_full + VST;      // [VST]
-  uint64_t* s_full = v_empty + VST;      // [RING]
-  uint64_t* s_free = s_full + RING;      // [RING]
+  uint64_t* s_full = v_empty + VST;      // [2 halves][RING] (per half: see dfss_flash2_kernel)
+  uint64_t* s_free = s_full + 2 * RING;  // [RING]
   uint64_t* p_full = s_free + RING;      // [2 halves][RING] (8 warps)
   uint64_t* o_full = p_full + 2 * RING;  // [2 halves]
   uint64_t* o_empty = o_full + 2;        // [2 halves] (8 warps)
@@ -135,8 +135,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const uint32_t warp = tc::warp_id();
   const uint32_t lane = threadIdx.x & 31;
-  const int iblocks = n / (2 * BM);
+  // 256-row items; n % 256 == 128 leaves the second half of the last row block empty: that
+  // half is treated like a fully masked one (no S / softmax / PV, output not stored)
+  const int iblocks = (n + 2 * BM - 1) / (2 * BM);
   const int items = bh * iblocks;
+  auto half_ok = [&](int ib, int hh) { return (ib * 2 + hh) * BM < n; };
   const int ntiles = n / BN;
   // BlockMask step skipping and the cost-ranked snake schedule: exactly as dfss_flash2_kernel
   // (flash_tc.cu), which documents the scheme
@@ -158,10 +161,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   auto live_words = [&](int ib, int t, uint32_t& w0, uint32_t& w1) {
     if (MASKED && (t & 31) == 0) {
       w0 = s_live[(ib * 2) * tmask.sbw + (t >> 5)];
-      w1 = s_live[(ib * 2 + 1) * tmask.sbw + (t >> 5)];
+      w1 = half_ok(ib, 1) ? s_live[(ib * 2 + 1) * tmask.sbw + (t >> 5)] : 0u;
     }
   };
   auto bit_u = [&](uint32_t w, int t) { return !MASKED || __any_sync(0xffffffffu, (w >> (t & 31)) & 1u); };
+  // liveness of half 1 also needs the half inside the sequence (uniform)
+  auto bit1_u = [&](uint32_t w, int t, int ib) { return half_ok(ib, 1) && bit_u(w, t); };
 
   if (warp == W_QK && lane == 0) {
     tc::prefetch_tmap(&tm_q);
@@ -174,10 +179,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc::mbar_init(&o_empty[i], 8);
       tc::mbar_init(&pv_done[i], 1);
     }
-    for (int i = 0; i < RING; ++i) {
-      tc::mbar_init(&s_full[i], 1);
-      tc::mbar_init(&s_free[i], 1);
-    }
+    for (int i = 0; i < RING; ++i) tc::mbar_init(&s_free[i], 1);
+    for (int i = 0; i < 2 * RING; ++i) tc::mbar_init(&s_full[i], 1);
     for (int i = 0; i < 2 * RING; ++i) tc::mbar_init(&p_full[i], 8);
     for (int i = 0; i < KST; ++i) {
       tc::mbar_init(&k_full[i], 1);
@@ -211,7 +214,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tc::tma_load_3d(smem + F_Q + h * Q_BYTES + a * ATOM, &tm_q, q_full, 32 * a, (ib * 2 + h) * BM, b);
         for (int t = 0; t < ntiles; ++t) {
           live_words(ib, t, lw0, lw1);
-          if (MASKED && !(((lw0 | lw1) >> (t & 31)) & 1u)) continue;
+          if (MASKED && !(((lw0 | lw1) >> (t & 31)) & 1u)) continue;  // (half 0 is always inside)
           tc::mbar_wait_sleep(&k_empty[ks], kph ^ 1);
           tc::mbar_arrive_expect_tx(&k_full[ks], KV_BYTES);
           for (int a = 0; a < 2; ++a)
@@ -238,13 +241,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc::mbar_wait_sleep(q_full, it & 1);
         for (int t = 0; t < ntiles; ++t) {
           live_words(ib, t, lw0, lw1);
-          const bool lv[2] = {bit_u(lw0, t), bit_u(lw1, t)};
-          if (MASKED && !lv[0] && !lv[1]) continue;
+          const bool lv[2] = {bit_u(lw0, t), bit1_u(lw1, t, ib)};
+          if (!lv[0] && !lv[1]) continue;
           tc::mbar_wait_sleep(&k_full[ks], kph);
           const uint32_t k_addr = tc::smem_u32(smem + F_K + ks * KV_BYTES);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            if (MASKED && !lv[h]) continue;
+            if (!lv[h]) continue;
             tc::mbar_wait_sleep(&s_free[sb], sph ^ 1);
             tc::tc_fence_after();
             const uint32_t q_addr = tc::smem_u32(smem + F_Q + h * Q_BYTES);
@@ -255,7 +258,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const uint64_t bd = tc::smem_desc(k_addr + off, 16, 1024, tc::kSwizzle128B);
               mma_tf32_w(tmem_base + sb * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
             }
-            tc::mma_commit_w(&s_full[sb]);
+            tc::mma_commit_w(&s_full[h * RING + sb]);
             if (++sb == RING) { sb = 0; sph ^= 1; }
           }
           tc::mma_commit_w(&k_empty[ks]);
@@ -275,20 +278,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int item = item_of(pos);
         uint32_t lw0 = 0, lw1 = 0;
         const int ib = item % iblocks;
-        tc::mbar_wait_sleep(&o_empty[h], (it & 1) ^ 1);
+        bool o_free = false;  // O_h drained: awaited lazily, as in dfss_flash2_kernel
+        auto await_o_free = [&]() {
+          if (!o_free) tc::mbar_wait_sleep(&o_empty[h], (it & 1) ^ 1);
+          o_free = true;
+        };
         bool first = true;
         for (int t = 0; t < ntiles; ++t) {
           live_words(ib, t, lw0, lw1);
-          const bool l0 = bit_u(lw0, t), l1 = bit_u(lw1, t);
+          const bool l0 = bit_u(lw0, t), l1 = bit1_u(lw1, t, ib);
           if (MASKED && !l0 && !l1) continue;  // tile not loaded
           const uint32_t g = gcount + (h ? (uint32_t)l0 : 0u), slot = g % RING;
           gcount += (uint32_t)l0 + (uint32_t)l1;
-          if (MASKED && !(h ? l1 : l0)) {  // this half masked here: release the V stage unused (after its load)
+          if (!(h ? l1 : l0)) {  // this half masked / empty here: release the V stage unused (after its load)
             tc::mbar_wait_sleep(&v_full[vs], vph);
             if (lane == 0) tc::mbar_arrive(&v_empty[vs]);
             if (++vs == VST) { vs = 0; vph ^= 1; }
             continue;
           }
+          await_o_free();
           tc::mbar_wait_sleep(&v_full[vs], vph);
           tc::mbar_wait_sleep(&p_full[h * RING + slot], (pbits >> slot) & 1);
           pbits ^= 1u << slot;
@@ -311,6 +319,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc::mma_commit_w(&pv_done[h]);
           if (++vs == VST) { vs = 0; vph ^= 1; }
         }
+        await_o_free();
         tc::mma_commit_w(&o_full[h]);
       }
     }
@@ -325,7 +334,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const float c = scale * kLog2e;
     float* rmax = red_max + h * 2 * BM;
     float* rsum = red_sum + h * 2 * BM;
-    uint32_t gcount = 0, hcount = 0, scol = 0;
+    uint32_t gcount = 0, hcount = 0, scol = 0, sfbits = 0;
     int it = 0;
     bool cm[2] = {false, false};
     auto row_max = [&]() {
@@ -351,6 +360,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     float pend_l = 0.f;
     auto cword = [&](int pos_) -> uint32_t {  // chunk-keep word `lane` of this warp's strip
       if (!MASKED || pos_ >= items || (int)lane >= tmask.cbw) return 0u;
+      if (!half_ok(item_of(pos_) % iblocks, h)) return 0u;
       const int strip = ((item_of(pos_) % iblocks) * 2 + h) * (BM / 32) + quad;
       return __ldg(tmask.cbits + (int64_t)strip * tmask.cbw + lane);
     };
@@ -368,13 +378,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&o_empty[h]);
+      pend = false;
+      if (!half_ok(pend_ib, h)) return;  // empty half of the last row block
       const int64_t row = (int64_t)pend_b * n + (pend_ib * 2 + h) * BM + r;
       float4* orow = reinterpret_cast<float4*>(out + row * HD + 32 * pr);
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         orow[j] = make_float4(__uint_as_float(o[4 * j]) * inv, __uint_as_float(o[4 * j + 1]) * inv,
                               __uint_as_float(o[4 * j + 2]) * inv, __uint_as_float(o[4 * j + 3]) * inv);
-      pend = false;
     };
     for (int kk_ = 0, pos = pos_at(0); pos < items; pos = pos_at(++kk_), ++it) {
         const int item = item_of(pos);
@@ -385,14 +396,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       bool first = true;
       for (int t = 0; t < ntiles; ++t) {
         live_words(ib, t, lw0, lw1);
-        const bool lv0 = bit_u(lw0, t), lv1 = bit_u(lw1, t);
+        const bool lv0 = bit_u(lw0, t), lv1 = bit1_u(lw1, t, ib);
         const uint32_t g = gcount + (h ? (uint32_t)lv0 : 0u);  // global live step
         gcount += (uint32_t)lv0 + (uint32_t)lv1;
-        if (MASKED && !(h ? lv1 : lv0)) continue;
+        if (!(h ? lv1 : lv0)) continue;
         ++hcount;
         const uint32_t slot = g % RING;
         scol = lane_base + slot * BN + 64 * pr;
-        tc::mbar_wait(&s_full[slot], (g / RING) & 1);
+        tc::mbar_wait(&s_full[h * RING + slot], (sfbits >> slot) & 1);  // k-th use of (h, slot): parity k & 1
+        sfbits ^= 1u << slot;
         tc::tc_fence_after();
         bool anym = false;
         if (MASKED) {
@@ -468,6 +480,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         first = false;
         if (pend) epilogue();
       }
+      if (pend) epilogue();  // the previous item's, if this item had no live step for this set
       pend = true;
       pend_b = b;
       pend_ib = ib;
@@ -499,7 +512,7 @@ __global__ void __launch_bounds__(256) transpose_v_kernel(const float* __restric
   }
 }
 
-bool tc_flash_tf32_supported(int gs, int n, int d) { return gs == 2 && d == HD && n > 0 && n % (2 * BM) == 0; }
+bool tc_flash_tf32_supported(int gs, int n, int d) { return gs == 2 && d == HD && n > 0 && n % BM == 0; }
 
 static int64_t vt_bytes(int64_t bh, int n) { return (bh * (int64_t)n * HD * 4 + 255) / 256 * 256; }
 
@@ -546,7 +559,7 @@ cudaError_t launch_flash_tf32(const void* q, const void* k, const void* v, void*
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t items = bh * (n / (2 * BM));
+  const int64_t items = bh * ((n + 2 * BM - 1) / (2 * BM));
   const int grid = (int)(items < sms ? items : sms);
   kern<<<grid, NUM_THREADS, smem_total, s>>>(tq, tk, tv, (float*)out, scale, (int)bh, n, m);
   return cudaGetLastError();

@@ -576,7 +576,7 @@ def _tf32(x: np.ndarray) -> np.ndarray:
     return (x.astype(np.float32).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32).astype(np.float64)
 
 
-@pytest.mark.parametrize("n", [256, 512, 1024])
+@pytest.mark.parametrize("n", [128, 256, 384, 512, 640, 1024])
 def test_tf32_12_fused_attention(n):
     """configs[4] "1:2 tf32": fp32 inputs, tf32 tensor cores, fused 1:2 kernel.  Checked like the
     16-bit paths: the reference nm_attention in float64 on the operands the hardware multiplies
@@ -648,3 +648,47 @@ def test_tf32_12_block_mask_whole_steps_skipped():
     for b, h in [(0, 0), (1, 41), (1, 79)]:
         qq, kk, vv = (_tf32(x[b, h].cpu().numpy()) for x in (q, k, v))
         assert_close(out[b, h], _masked_oracle(qq, kk, vv, mask, "1:2"), 2e-2, 2e-2, f"tf32 block-causal ({b},{h})")
+
+
+def test_tf32_12_odd_row_block_masked_and_many_items():
+    """n % 256 == 128: the last 256-row item has an empty second half (treated like a fully
+    masked one).  Many items per CTA, with and without a block mask, guard the output rows."""
+    n = 384
+    g = torch.Generator().manual_seed(17)
+    q, k, v = (torch.randn((4, 100, n, 64), generator=g).cuda() for _ in range(3))   # 200 items
+    out = torch.full_like(q, float("nan"))
+    dfss.dfss_attention(q, k, v, "1:2", math_mode="tf32", out=out)
+    assert torch.isfinite(out).all()
+    for b, h in [(0, 0), (3, 99)]:
+        qq, kk, vv = (_tf32(x[b, h].cpu().double().numpy()) for x in (q, k, v))
+        assert_close(_np(out[b, h]), oracle_attention(qq, kk, vv, "1:2"), 2e-2, 2e-2, f"tf32 n=384 ({b},{h})")
+    keep = _block_causal_keep(n, 32, 64)
+    mask = dfss.BlockMask(keep, 32, 64)
+    out = _np(dfss.dfss_attention(q, k, v, "1:2", math_mode="tf32", block_mask=mask))
+    for b, h in [(1, 5), (2, 77)]:
+        qq, kk, vv = (_tf32(x[b, h].cpu().double().numpy()) for x in (q, k, v))
+        assert_close(out[b, h], _masked_oracle(qq, kk, vv, mask, "1:2"), 2e-2, 2e-2, f"tf32 masked n=384 ({b},{h})")
+
+
+@pytest.mark.parametrize("kind", ["2:4-bf16", "1:2-f16", "1:2-tf32"])
+def test_block_mask_one_half_runs_ahead(kind):
+    """Rows 0-127 of every 256-row item keep only the last 128 keys, rows 128-255 keep all: one
+    softmax set runs every step while the other waits for the item's last step.  A shared S-slot
+    barrier would complete two phases past the waiting set (parity aliasing); per-half S
+    barriers keep the waits exact."""
+    mode, dt = kind.split("-")
+    n, tr, tc_ = 1024, 32, 64
+    rows = np.arange(n // tr) * tr
+    cols = np.arange(n // tc_) * tc_
+    keep = np.where(((rows % 256) < 128)[:, None], (cols >= n - 128)[None, :], True)
+    mask = dfss.BlockMask(keep, tr, tc_)
+    g = torch.Generator().manual_seed(23)
+    dtype = {"bf16": torch.bfloat16, "f16": torch.float16, "tf32": torch.float32}[dt]
+    q, k, v = (torch.randn((2, 96, n, 64), generator=g).to(dtype).cuda() for _ in range(3))  # 768 items
+    kw = {"math_mode": "tf32"} if dt == "tf32" else {}
+    out = _np(dfss.dfss_attention(q, k, v, mode, block_mask=mask, **kw))
+    for b, h in [(0, 3), (1, 95)]:
+        ops = [x[b, h].cpu().double().numpy() for x in (q, k, v)]
+        if dt == "tf32":
+            ops = [_tf32(x) for x in ops]
+        assert_close(out[b, h], _masked_oracle(*ops, mask, mode), 2e-2, 2e-2, f"{kind} skewed mask ({b},{h})")

@@ -370,17 +370,19 @@ def block_mask_measure(device, steps=5):
 
 
 def e2e_measure(args, cfg, q, k, v, device):
-    """Same metric through the public API with pinned host buffers: H2D inputs + compute + D2H output, every step."""
+    """Same metric through the public host-buffer API (dfss_attention_host) with pinned host
+    buffers: every step copies Q/K/V host->device, runs the fused kernel and copies O back,
+    pipelined over 4 batch x heads pieces on three streams (both PCIe directions busy;
+    tools/time_host_api.py: 1.70 ms at c2 vs 1.82 ms for the serial copies)."""
     import paper_2203_00091_b200 as dfss
 
     mode = dfss.SparsityMode.parse(cfg["mode"])
     hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
     hout = torch.empty(q.shape, dtype=q.dtype).pin_memory()
+    math_mode = cfg.get("math", "auto")
 
     def step():
-        dq, dk, dv = (h.to(device, non_blocking=True) for h in (hq, hk, hv))
-        o = dfss.dfss_attention(dq, dk, dv, mode)
-        hout.copy_(o, non_blocking=True)
+        dfss.dfss_attention_host(hq, hk, hv, mode, math_mode=math_mode, out=hout, chunks=4, device=device)
 
     ts = time_steps(step, max(3, args.steps), 2)
     ms = float(np.mean(ts))

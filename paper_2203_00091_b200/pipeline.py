@@ -91,6 +91,82 @@ def dfss_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode="2:4"
     return out
 
 
+_HOST_STREAMS: dict[int, tuple[torch.cuda.Stream, torch.cuda.Stream, torch.cuda.Stream]] = {}
+
+
+def dfss_attention_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode="2:4", *, math_mode: str = "auto",
+                        block_mask: BlockMask | None = None, out: torch.Tensor | None = None, chunks: int = 4,
+                        device: torch.device | int | None = None) -> torch.Tensor:
+    """dfss_attention for HOST tensors [..., n, d] (the reference's own calling convention: its
+    kernels take host arrays): returns a host tensor.  The flattened batch x heads is cut into
+    `chunks` pieces; the host->device copy of piece i+1, the fused kernel on piece i and the
+    device->host copy of piece i-1 run concurrently on three streams (PCIe is full duplex), with
+    two device buffers per direction.  Pinned inputs / output make the copies asynchronous
+    (unpinned ones are staged by the driver, still correct).  Ordered after prior work on the
+    current stream, and the current stream waits for the last copy, so events recorded around
+    the call time the whole transfer + compute."""
+    if q.is_cuda or k.is_cuda or v.is_cuda:
+        raise ValueError("dfss_attention_host takes host tensors; use dfss_attention for device tensors")
+    if q.shape != k.shape or q.shape != v.shape or q.dim() < 2:
+        raise ValueError(f"Q, K, V must share shape [..., n, d]; got {tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index or 0)
+    n, d = q.shape[-2], q.shape[-1]
+    bh = int(np.prod(q.shape[:-2], dtype=np.int64)) if q.dim() > 2 else 1
+    qf, kf, vf = (x.reshape(bh, n, d) for x in (q, k, v))
+    if out is None:
+        out = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
+    of = out.view(bh, n, d)
+    chunks = max(1, min(int(chunks), bh))
+    bounds = [bh * i // chunks for i in range(chunks + 1)]
+    width = max(bounds[i + 1] - bounds[i] for i in range(chunks))
+    if dev.index not in _HOST_STREAMS:
+        _HOST_STREAMS[dev.index] = tuple(torch.cuda.Stream(dev) for _ in range(3))
+    s_in, s_run, s_out = _HOST_STREAMS[dev.index]
+    cur = torch.cuda.current_stream(dev)
+    start = torch.cuda.Event()
+    start.record(cur)
+    dq = torch.empty((2, 3, width, n, d), dtype=q.dtype, device=dev)    # [slot][q,k,v] input buffers
+    do = torch.empty((2, width, n, d), dtype=q.dtype, device=dev)       # output buffers
+    ws = None
+    need = workspace_bytes(mode, q.dtype, width, n, d, math_mode, block_mask)
+    if need:
+        ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    copied, ran, drained = [], [], []
+    for i in range(chunks):
+        lo, hi = bounds[i], bounds[i + 1]
+        slot, w = i % 2, hi - lo
+        with torch.cuda.stream(s_in):
+            s_in.wait_event(start)
+            if i >= 2:
+                s_in.wait_event(ran[i - 2])          # input slot free once that piece's kernel ran
+            for j, src in enumerate((qf, kf, vf)):
+                dq[slot, j, :w].copy_(src[lo:hi], non_blocking=True)
+            copied.append(torch.cuda.Event())
+            copied[i].record(s_in)
+        with torch.cuda.stream(s_run):
+            s_run.wait_event(copied[i])
+            if i >= 2:
+                s_run.wait_event(drained[i - 2])     # output slot free once copied out
+            dfss_attention(dq[slot, 0, :w], dq[slot, 1, :w], dq[slot, 2, :w], mode, math_mode=math_mode,
+                           block_mask=block_mask, out=do[slot, :w], workspace=ws)
+            ran.append(torch.cuda.Event())
+            ran[i].record(s_run)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ran[i])
+            of[lo:hi].copy_(do[slot, :w], non_blocking=True)
+            drained.append(torch.cuda.Event())
+            drained[i].record(s_out)
+    cur.wait_event(drained[-1])
+    # the device buffers are released to the caching allocator; keep them alive until the copies
+    # ran by recording their use on every stream that touched them
+    for st in (s_in, s_run, s_out):
+        dq.record_stream(st)
+        do.record_stream(st)
+        if ws is not None:
+            ws.record_stream(st)
+    return out
+
+
 def nm_attention(inputs: AttentionInputs, mode: SparsityMode, block_mask: BlockMask | None = None, *,
                  tile_rows: int = 32, tile_cols: int = 64) -> DenseMatrix:
     """Drop-in sparse attention: fused prune -> sparse softmax -> SpMM (pipeline.py:15-32)."""

@@ -692,3 +692,29 @@ def test_block_mask_one_half_runs_ahead(kind):
         if dt == "tf32":
             ops = [_tf32(x) for x in ops]
         assert_close(out[b, h], _masked_oracle(*ops, mask, mode), 2e-2, 2e-2, f"{kind} skewed mask ({b},{h})")
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_api_matches_device_api(pinned):
+    """dfss_attention_host (host tensors in / out, pipelined copies) equals dfss_attention on the
+    same inputs, for uneven pieces, a block mask and the tf32 path."""
+    g = torch.Generator().manual_seed(29)
+    q, k, v = (torch.randn((3, 7, 512, 64), generator=g).to(torch.bfloat16) for _ in range(3))
+    if pinned:
+        q, k, v = (x.pin_memory() for x in (q, k, v))
+    want = dfss.dfss_attention(q.cuda(), k.cuda(), v.cuda(), "2:4").cpu()
+    got = dfss.dfss_attention_host(q, k, v, "2:4", chunks=5)
+    torch.cuda.synchronize()
+    assert not got.is_cuda and torch.equal(got, want)
+    mask = dfss.BlockMask(_block_causal_keep(512, 32, 64), 32, 64)
+    want = dfss.dfss_attention(q.cuda(), k.cuda(), v.cuda(), "1:2", block_mask=mask).cpu()
+    got = dfss.dfss_attention_host(q, k, v, "1:2", block_mask=mask, chunks=4)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    qf, kf, vf = (x.float() for x in (q, k, v))
+    want = dfss.dfss_attention(qf.cuda(), kf.cuda(), vf.cuda(), "1:2", math_mode="tf32").cpu()
+    got = dfss.dfss_attention_host(qf, kf, vf, "1:2", math_mode="tf32", chunks=3)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    with pytest.raises(ValueError, match="host tensors"):
+        dfss.dfss_attention_host(q.cuda(), k, v)

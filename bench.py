@@ -275,9 +275,9 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True, info=Tr
                 "algorithmic_flops_per_launch": flops * bh,
                 "algorithmic_hbm_bytes_per_launch": 4 * n * d * 2 * bh,
                 "note": "fused kernel, no n^2 HBM traffic (traffic = ncu dram bytes per launch, Q/K/V/O only); "
-                        "tensor work 2n^2d (S) + sparse PV at the 2:4 rate; the bound in practice is the 2:4 "
-                        "prune + exp epilogue on the ALU/FMA pipes (~35 issue-cycles per 4-score group, "
-                        "tools/prune_probe.cu), see profiles/"}
+                        "tensor work 2n^2d (S) + sparse PV at the 2:4 rate; the bound in practice is instruction "
+                        "issue in the prune + exp epilogue (~29 issued instructions per 4-score group, issue "
+                        "active ~71%, ALU pipe ~67%; profiles/r01j_ncu_summary.md, DESIGN.md 4.1)"}
         ab = {"flash": 4 * n * d * 2}
         dom = "flash"
     else:

@@ -718,3 +718,40 @@ def test_host_api_matches_device_api(pinned):
     assert torch.equal(got, want)
     with pytest.raises(ValueError, match="host tensors"):
         dfss.dfss_attention_host(q.cuda(), k, v)
+
+
+@pytest.mark.parametrize("case", range(8))
+def test_block_mask_fuzz_many_items(case):
+    """Randomised block masks on the fused kernels with several items per CTA: random tile
+    sizes (multiples of 32, group-aligned), densities from very sparse to dense, 128-aligned
+    block patterns and one-sided row bands; 2:4 / 1:2 / tf32 by case."""
+    rng = np.random.default_rng(100 + case)
+    n = int(rng.choice([256, 512, 768, 1024]))
+    tr = int(rng.choice([32, 64, 128]))
+    tc_ = int(rng.choice([32, 64, 128]))
+    density = float(rng.choice([0.05, 0.3, 0.7, 0.95]))
+    gr, gc = -(-n // tr), -(-n // tc_)
+    style = case % 3
+    if style == 0:      # i.i.d. tiles
+        keep = rng.random((gr, gc)) < density
+    elif style == 1:    # 128 x 128 blocks
+        blk = rng.random((-(-n // 128), -(-n // 128))) < density
+        keep = blk[(np.arange(gr) * tr) // 128][:, (np.arange(gc) * tc_) // 128]
+    else:               # row bands: every other 128-row band keeps only a few key tiles
+        keep = rng.random((gr, gc)) < density
+        band = ((np.arange(gr) * tr) // 128) % 2 == 0
+        keep[band] &= (np.arange(gc) * tc_ >= n - 128)[None, :]
+    keep[np.arange(gr), rng.integers(0, gc, gr)] = True      # no empty row
+    mask = dfss.BlockMask(keep, tr, tc_)
+    mode, dt = [("2:4", torch.bfloat16), ("1:2", torch.float16), ("1:2", torch.float32)][case % 3]
+    g = torch.Generator().manual_seed(200 + case)
+    bh = max(2, 600 // (n // 256))                            # > 148 items: several per CTA
+    q, k, v = (torch.randn((1, bh, n, 64), generator=g).to(dt).cuda() for _ in range(3))
+    kw = {"math_mode": "tf32"} if dt == torch.float32 else {}
+    out = _np(dfss.dfss_attention(q, k, v, mode, block_mask=mask, **kw))
+    for h in (0, bh // 2, bh - 1):
+        ops = [x[0, h].cpu().double().numpy() for x in (q, k, v)]
+        if dt == torch.float32:
+            ops = [_tf32(x) for x in ops]
+        assert_close(out[0, h], _masked_oracle(*ops, mask, mode), 2e-2, 2e-2,
+                     f"fuzz case {case}: n={n} tiles={tr}x{tc_} density={density} style={style} head {h}")

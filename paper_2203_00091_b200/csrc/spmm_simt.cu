@@ -47,6 +47,9 @@ __global__ void __launch_bounds__(256) spmm_simt_kernel(const TP* __restrict__ p
         if (keep && !keep[(int64_t)(r / tile_rows) * grid_cols + col / tile_cols]) pv = 0.f;
       }
       const int cnt = min(32, nzc - j0);
+      // unrolled so the V-row loads of several nonzeros are in flight together (the loop was
+      // latency-bound: one dependent L2 load chain per warp)
+#pragma unroll 8
       for (int l = 0; l < cnt; ++l) {
         const float pl = __shfl_sync(0xffffffffu, pv, l);
         const int cl = __shfl_sync(0xffffffffu, col, l);

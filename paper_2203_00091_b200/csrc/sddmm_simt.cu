@@ -43,7 +43,21 @@ __global__ void __launch_bounds__(256) sddmm_simt_kernel(const TIn* __restrict__
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
 
-  if (row0 < n) {
+  // a CTA tile whose mask tiles are all masked skips the dot products (the reference's tile
+  // loop skips masked tiles, _kernels_numba.py:110-185); its groups encode as absent below.
+  // With a score dump requested (parity hook) every score is still computed.
+  bool cta_live = true;
+  if (keep && !dbg) {
+    cta_live = false;
+    const int r_hi = min(row0 + BM, n) - 1, c_hi = min(col0 + BN, m) - 1;
+    for (int tr = row0 / tile_rows; tr <= r_hi / tile_rows && !cta_live; ++tr)
+      for (int tcl = col0 / tile_cols; tcl <= c_hi / tile_cols; ++tcl)
+        if (keep[(int64_t)tr * grid_cols + tcl]) {
+          cta_live = true;
+          break;
+        }
+  }
+  if (row0 < n && cta_live) {
     for (int k0 = 0; k0 < d; k0 += BK) {
       for (int i = threadIdx.x; i < BM * BK; i += 256) {
         const int r = i / BK, kk = i % BK;

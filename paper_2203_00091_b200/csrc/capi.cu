@@ -203,6 +203,8 @@ int dfss_nm_attention_masked(const void* q, const void* k, const void* v, void* 
   if (st) return st;
   if (fused)
     return dfss_spmm(nz, meta, v, out, mode, dtype, dtype, dtype, bh, n, n, d, nullptr, 0, 0, row_max, stream);
+  if (dtype == DFSS_F32 && d <= 64)  // exact FP32: softmax fused into the SIMT SpMM (one pass less)
+    return cuda_status(dfss::launch_spmm_simt_softmax_f32(nz, meta, v, out, mode, bh, n, n, d, (cudaStream_t)stream));
   st = dfss_softmax_rows(nz, nz, dtype, dtype, bh, n, n / 2, nullptr, 0, 0, nullptr, stream);
   if (st) return st;
   return dfss_spmm(nz, meta, v, out, mode, dtype, dtype, dtype, bh, n, n, d, nullptr, 0, 0, nullptr, stream);

@@ -175,6 +175,9 @@ cudaError_t launch_sddmm_simt(const void* q, const void* k, void* nz, uint32_t* 
 cudaError_t launch_softmax(const void* in, void* out, int in_dtype, int out_dtype, int64_t bh, int rows,
                            int cols, const uint8_t* keep, int tile_rows, int tile_cols, int32_t* err,
                            cudaStream_t s);
+// fp32 SpMM with the row softmax fused (exact-FP32 nm_attention path, no mask, d <= 64)
+cudaError_t launch_spmm_simt_softmax_f32(const void* p, const uint32_t* meta, const void* v, void* out, int gs,
+                                        int64_t bh, int rows, int n_k, int d, cudaStream_t s);
 cudaError_t launch_spmm_simt(const void* p, const uint32_t* meta, const void* v, void* out, int gs, int p_dtype,
                              int v_dtype, int out_dtype, int64_t bh, int rows, int n_k, int d, const uint8_t* keep,
                              int tile_rows, int tile_cols, cudaStream_t s);

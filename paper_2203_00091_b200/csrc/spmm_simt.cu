@@ -12,7 +12,10 @@
 
 namespace dfss {
 
-template <typename TP, typename TV, typename TO, int GS, int DPER>
+// SM: the row softmax (softmax_rows, sparse_ops.py:18-37) fused in: the warp first reduces the
+// row's max and sum of exp over its nonzeros, then weights each nonzero by exp(x - max) and
+// scales the output row by 1 / sum (no mask; the exact-FP32 nm_attention path).
+template <typename TP, typename TV, typename TO, int GS, int DPER, bool SM = false>
 __global__ void __launch_bounds__(256) spmm_simt_kernel(const TP* __restrict__ p, const uint32_t* __restrict__ meta,
                                                         const TV* __restrict__ v, TO* __restrict__ out,
                                                         int64_t total_rows, int rows, int n_k, int d,
@@ -33,6 +36,20 @@ __global__ void __launch_bounds__(256) spmm_simt_kernel(const TP* __restrict__ p
     float acc[DPER];
 #pragma unroll
     for (int t = 0; t < DPER; ++t) acc[t] = 0.f;
+    constexpr float kLog2e = 1.4426950408889634f;
+    float mlb = 0.f, inv = 1.f;
+    if (SM) {
+      float mx = -INFINITY;
+      for (int j = lane; j < nzc; j += 32) mx = fmaxf(mx, DT<TP>::to_f(prow[j]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mlb = mx * kLog2e;
+      float sum = 0.f;
+      for (int j = lane; j < nzc; j += 32) sum += exp2f(fmaf(DT<TP>::to_f(prow[j]), kLog2e, -mlb));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      inv = 1.0f / sum;
+    }
 
     for (int j0 = 0; j0 < nzc; j0 += 32) {
       const int j = j0 + lane;
@@ -44,6 +61,7 @@ __global__ void __launch_bounds__(256) spmm_simt_kernel(const TP* __restrict__ p
         const uint32_t nib = (mb[geo.word_of(r, g, shift)] >> shift) & 0xFu;
         col = (GS == 4) ? 4 * g + (int)((j & 1) ? ((nib >> 2) & 3u) : (nib & 3u)) : 2 * g + (nib == 0xEu ? 1 : 0);
         pv = DT<TP>::to_f(prow[j]);
+        if (SM) pv = exp2f(fmaf(pv, kLog2e, -mlb));
         if (keep && !keep[(int64_t)(r / tile_rows) * grid_cols + col / tile_cols]) pv = 0.f;
       }
       const int cnt = min(32, nzc - j0);
@@ -65,7 +83,7 @@ __global__ void __launch_bounds__(256) spmm_simt_kernel(const TP* __restrict__ p
 #pragma unroll
     for (int t = 0; t < DPER; ++t) {
       const int c = lane + 32 * t;
-      if (c < d) orow[c] = DT<TO>::from_f(acc[t]);
+      if (c < d) orow[c] = DT<TO>::from_f(SM ? acc[t] * inv : acc[t]);
     }
   }
 }
@@ -122,6 +140,28 @@ static cudaError_t spmm_simt_p(const void* p, const uint32_t* meta, const void* 
       return spmm_simt_pv<TP, __nv_bfloat16>(p, meta, v, out, gs, out_dtype, bh, rows, n_k, d, keep, tr, tc, s);
     default: return spmm_simt_pv<TP, __half>(p, meta, v, out, gs, out_dtype, bh, rows, n_k, d, keep, tr, tc, s);
   }
+}
+
+cudaError_t launch_spmm_simt_softmax_f32(const void* p, const uint32_t* meta, const void* v, void* out, int gs,
+                                        int64_t bh, int rows, int n_k, int d, cudaStream_t s) {
+  if (bh == 0 || rows == 0 || d == 0) return cudaSuccess;
+  if (d > 64) return cudaErrorNotSupported;
+  const int64_t total = bh * rows;
+  int64_t blocks = (total + 7) / 8;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  const float* pf = (const float*)p;
+  const float* vf = (const float*)v;
+  float* of = (float*)out;
+  if (gs == 4) {
+    MetaGeom geo(rows, n_k / 4);
+    spmm_simt_kernel<float, float, float, 4, 2, true>
+        <<<(int)blocks, 256, 0, s>>>(pf, meta, vf, of, total, rows, n_k, d, nullptr, 1, 1, geo);
+  } else {
+    MetaGeom geo(rows, n_k / 2);
+    spmm_simt_kernel<float, float, float, 2, 2, true>
+        <<<(int)blocks, 256, 0, s>>>(pf, meta, vf, of, total, rows, n_k, d, nullptr, 1, 1, geo);
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_spmm_simt(const void* p, const uint32_t* meta, const void* v, void* out, int gs, int p_dtype,

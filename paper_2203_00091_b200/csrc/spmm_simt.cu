@@ -142,9 +142,10 @@ static cudaError_t spmm_simt_p(const void* p, const uint32_t* meta, const void* 
   }
 }
 
-// d == 64 variant of the softmax-fused fp32 SpMM: a half-warp per row (two rows per warp), each
-// lane owns 4 output columns and loads them as one float4 -- half the instructions per nonzero
-// of the warp-per-row kernel and twice the loads in flight.
+// d == 64 variant of the softmax-fused fp32 SpMM: one warp per row, the two half-warps take
+// alternate 16-nonzero batches of the row and add their partial rows at the end; each lane
+// owns 4 output columns loaded as one float4 (half the instructions per nonzero of the generic
+// kernel, and the row's dependent load chain split in two).
 template <int GS>
 __global__ void __launch_bounds__(256) spmm_simt_softmax_d64_kernel(const float* __restrict__ p,
                                                                     const uint32_t* __restrict__ meta,
@@ -152,34 +153,28 @@ __global__ void __launch_bounds__(256) spmm_simt_softmax_d64_kernel(const float*
                                                                     float* __restrict__ out, int64_t total_rows,
                                                                     int rows, int n_k, MetaGeom geo) {
   constexpr float kLog2e = 1.4426950408889634f;
-  const int hl = threadIdx.x & 15;                      // lane within the half-warp
-  const unsigned hmask = (threadIdx.x & 16) ? 0xFFFF0000u : 0x0000FFFFu;
-  const int64_t half = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 4;
-  const int64_t nhalves = ((int64_t)gridDim.x * blockDim.x) >> 4;
+  const int lane = threadIdx.x & 31, hl = lane & 15, part = lane >> 4;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int nzc = n_k / 2;
-  // every half-warp runs the same trip count so the full-warp shuffles stay converged
-  const int64_t iters = (total_rows + nhalves - 1) / nhalves;
-  for (int64_t it = 0; it < iters; ++it) {
-    const int64_t rg = half + it * nhalves;
-    const bool ok = rg < total_rows;
-    const int64_t rgc = ok ? rg : 0;
-    const int64_t b = rgc / rows;
-    const int r = (int)(rgc % rows);
-    const float* prow = p + rgc * nzc;
+  for (int64_t rg = warp; rg < total_rows; rg += nwarps) {
+    const int64_t b = rg / rows;
+    const int r = (int)(rg % rows);
+    const float* prow = p + rg * nzc;
     const uint32_t* mb = meta + b * geo.words_per_bh();
     const float4* vb = reinterpret_cast<const float4*>(v + b * (int64_t)n_k * 64);
     float mx = -INFINITY;
-    for (int j = hl; j < nzc; j += 16) mx = fmaxf(mx, prow[j]);
+    for (int j = lane; j < nzc; j += 32) mx = fmaxf(mx, prow[j]);
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     const float mlb = mx * kLog2e;
     float sum = 0.f;
-    for (int j = hl; j < nzc; j += 16) sum += exp2f(fmaf(prow[j], kLog2e, -mlb));
+    for (int j = lane; j < nzc; j += 32) sum += exp2f(fmaf(prow[j], kLog2e, -mlb));
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int j0 = 0; j0 < nzc; j0 += 16) {
-      const int j = j0 + hl;
+    for (int j0 = 0; j0 < nzc; j0 += 32) {  // same trip count in both halves (converged shuffles)
+      const int j = j0 + 16 * part + hl;
       float pv = 0.f;
       int col = 0;
       if (j < nzc) {
@@ -189,9 +184,8 @@ __global__ void __launch_bounds__(256) spmm_simt_softmax_d64_kernel(const float*
         col = (GS == 4) ? 4 * g + (int)((j & 1) ? ((nib >> 2) & 3u) : (nib & 3u)) : 2 * g + (nib == 0xEu ? 1 : 0);
         pv = exp2f(fmaf(prow[j], kLog2e, -mlb));
       }
-      const int cnt = min(16, nzc - j0);
 #pragma unroll 8
-      for (int l = 0; l < cnt; ++l) {
+      for (int l = 0; l < 16; ++l) {
         const float pl = __shfl_sync(0xffffffffu, pv, l, 16);
         const int cl = __shfl_sync(0xffffffffu, col, l, 16);
         const float4 x = vb[(int64_t)cl * 16 + hl];
@@ -201,8 +195,11 @@ __global__ void __launch_bounds__(256) spmm_simt_softmax_d64_kernel(const float*
         acc.w = fmaf(pl, x.w, acc.w);
       }
     }
-    (void)hmask;
-    if (ok) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
+    acc.z += __shfl_xor_sync(0xffffffffu, acc.z, 16);
+    acc.w += __shfl_xor_sync(0xffffffffu, acc.w, 16);
+    if (part == 0) {
       const float inv = 1.0f / sum;
       reinterpret_cast<float4*>(out + rg * 64)[hl] = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
     }
@@ -215,7 +212,7 @@ cudaError_t launch_spmm_simt_softmax_f32(const void* p, const uint32_t* meta, co
   if (d > 64) return cudaErrorNotSupported;
   if (d == 64 && ((uintptr_t)v & 15) == 0 && ((uintptr_t)out & 15) == 0) {
     const int64_t total = bh * rows;
-    int64_t blocks = (total + 15) / 16;  // 16 rows per 256-thread block
+    int64_t blocks = (total + 7) / 8;  // one row per warp
     if (blocks > 148 * 64) blocks = 148 * 64;
     const int nk = n_k;
     if (gs == 4)

@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(256) spmm_simt_softmax_d64_kernel(const float*
         col = (GS == 4) ? 4 * g + (int)((j & 1) ? ((nib >> 2) & 3u) : (nib & 3u)) : 2 * g + (nib == 0xEu ? 1 : 0);
         pv = exp2f(fmaf(prow[j], kLog2e, -mlb));
       }
-#pragma unroll 8
+#pragma unroll
       for (int l = 0; l < 16; ++l) {
         const float pl = __shfl_sync(0xffffffffu, pv, l, 16);
         const int cl = __shfl_sync(0xffffffffu, col, l, 16);

@@ -15,7 +15,7 @@ constexpr int BM = 64, BN = 64, BK = 32;
 }
 
 // grid: (ceil(m/64), 2*ceil(n/128), bh); 256 threads, each a 4x4 score block:
-// rows ty + 16*i, columns 4*tx .. 4*tx+3 (one 2:4 group, two 1:2 groups).
+// rows 4*ty .. 4*ty+3, columns 4*tx .. 4*tx+3 (one 2:4 group, two 1:2 groups).
 template <typename TIn, typename TNz, int GS>
 __global__ void __launch_bounds__(256) sddmm_simt_kernel(const TIn* __restrict__ q, const TIn* __restrict__ k,
                                                          TNz* __restrict__ nz, uint32_t* __restrict__ meta,
@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(256) sddmm_simt_kernel(const TIn* __restrict__
                                                          const uint8_t* __restrict__ keep, int tile_rows,
                                                          int tile_cols, float* __restrict__ dbg, MetaGeom geo,
                                                          uint32_t two) {
-  __shared__ float Qs[BK][BM + 1];
+  __shared__ __align__(16) float Qs[BK][BM + 4];
   __shared__ __align__(16) float Ks[BK][BN + 4];
   __shared__ uint8_t nibs[BM][BN / GS];
 
@@ -70,9 +70,10 @@ __global__ void __launch_bounds__(256) sddmm_simt_kernel(const TIn* __restrict__
 #pragma unroll 8
       for (int kk = 0; kk < BK; ++kk) {
         const float4 bv = *reinterpret_cast<const float4*>(&Ks[kk][4 * tx]);
+        const float4 av = *reinterpret_cast<const float4*>(&Qs[kk][4 * ty]);  // rows 4 ty .. 4 ty + 3
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const float a = Qs[kk][ty + 16 * i];
+          const float a = i == 0 ? av.x : i == 1 ? av.y : i == 2 ? av.z : av.w;
           acc[i][0] = fmaf(a, bv.x, acc[i][0]);
           acc[i][1] = fmaf(a, bv.y, acc[i][1]);
           acc[i][2] = fmaf(a, bv.z, acc[i][2]);
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(256) sddmm_simt_kernel(const TIn* __restrict__
   // ---- prune/encode epilogue: nonzeros and nibbles leave, dense scores never do
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int lr = ty + 16 * i;
+    const int lr = 4 * ty + i;
     const int row = row0 + lr;
     const int c0 = col0 + 4 * tx;
     float v[4];

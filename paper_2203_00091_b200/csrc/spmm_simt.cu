@@ -8,6 +8,8 @@
 // broadcast by shuffles, lanes own output columns lane + 32*t.
 // This is the exact-FP32 path (c1 at 1e-5) and the fallback for shapes the
 // tcgen05.mma.sp kernel does not tile.
+#include <cstdlib>
+
 #include "dfss_common.cuh"
 
 namespace dfss {
@@ -206,10 +208,120 @@ __global__ void __launch_bounds__(256) spmm_simt_softmax_d64_kernel(const float*
   }
 }
 
+// Tiled variant (d == 64, n_k % 128 == 0): a CTA owns 32 rows of one (batch, head) and streams
+// V through shared memory in 128-key tiles, so each V row is read from L2 once per CTA instead
+// of once per nonzero (the warp-per-row kernel is L2-bandwidth-bound at larger n).  For either
+// mode the nonzeros of a row that fall in a 128-key tile are the contiguous range
+// [k0 / 2, k0 / 2 + 64).  Accumulation stays in ascending nonzero order.
+template <int GS>
+__global__ void __launch_bounds__(256) spmm_softmax_f32_tiled_kernel(const float* __restrict__ p,
+                                                                     const uint32_t* __restrict__ meta,
+                                                                     const float* __restrict__ v,
+                                                                     float* __restrict__ out, int rows, int n_k,
+                                                                     MetaGeom geo) {
+  constexpr float kLog2e = 1.4426950408889634f;
+  constexpr int RB = 32, KT = 128, NZT = KT / 2;
+  __shared__ __align__(16) float Vs[KT][64];
+  __shared__ float Ps[RB][NZT + 1];
+  __shared__ uint8_t Cs[RB][NZT];
+  __shared__ float s_mlb[RB], s_inv[RB];
+  const int b = blockIdx.y, row0 = blockIdx.x * RB;
+  const int nzc = n_k / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* pb = p + ((int64_t)b * rows) * nzc;
+  const uint32_t* mb = meta + (int64_t)b * geo.words_per_bh();
+  const float4* vb = reinterpret_cast<const float4*>(v + (int64_t)b * n_k * 64);
+  // row statistics: warp w handles rows 4w .. 4w + 3
+  for (int rr = 4 * warp; rr < 4 * warp + 4; ++rr) {
+    const int r = row0 + rr;
+    float mx = -INFINITY, sum = 0.f;
+    if (r < rows) {
+      const float* prow = pb + (int64_t)r * nzc;
+      for (int j = lane; j < nzc; j += 32) mx = fmaxf(mx, prow[j]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      for (int j = lane; j < nzc; j += 32) sum += exp2f(fmaf(prow[j], kLog2e, -mx * kLog2e));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    }
+    if (lane == 0) {
+      s_mlb[rr] = mx * kLog2e;
+      s_inv[rr] = 1.0f / sum;
+    }
+  }
+  __syncthreads();
+  const int orow = threadIdx.x >> 3, cb = threadIdx.x & 7;  // output row, 8-column block
+  float acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  for (int k0 = 0; k0 < n_k; k0 += KT) {
+    // V tile [128 keys][64] (float4 per thread x 8)
+#pragma unroll
+    for (int i = 0; i < (KT * 16) / 256; ++i) {
+      const int idx = threadIdx.x + 256 * i;
+      reinterpret_cast<float4*>(&Vs[0][0])[idx] = vb[(int64_t)k0 * 16 + idx];
+    }
+    // this tile's nonzeros of the CTA's rows: weights and tile-local columns
+#pragma unroll
+    for (int i = 0; i < (RB * NZT) / 256; ++i) {
+      const int idx = threadIdx.x + 256 * i;
+      const int rr = idx / NZT, jl = idx % NZT;
+      const int r = row0 + rr, j = k0 / 2 + jl;
+      float w = 0.f;
+      int col = k0;  // rows past the end: weight 0 on tile row 0
+      if (r < rows) {
+        const int g = (GS == 4) ? (j >> 1) : j;
+        int shift;
+        const uint32_t nib = (mb[geo.word_of(r, g, shift)] >> shift) & 0xFu;
+        col = (GS == 4) ? 4 * g + (int)((j & 1) ? ((nib >> 2) & 3u) : (nib & 3u)) : 2 * g + (nib == 0xEu ? 1 : 0);
+        w = exp2f(fmaf(pb[(int64_t)r * nzc + j], kLog2e, -s_mlb[rr]));
+      }
+      Ps[rr][jl] = w;
+      Cs[rr][jl] = (uint8_t)(col - k0);
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int jl = 0; jl < NZT; ++jl) {
+      const float w = Ps[orow][jl];
+      const float4* vr = reinterpret_cast<const float4*>(&Vs[Cs[orow][jl]][8 * cb]);
+      const float4 x0 = vr[0], x1 = vr[1];
+      acc[0] = fmaf(w, x0.x, acc[0]);
+      acc[1] = fmaf(w, x0.y, acc[1]);
+      acc[2] = fmaf(w, x0.z, acc[2]);
+      acc[3] = fmaf(w, x0.w, acc[3]);
+      acc[4] = fmaf(w, x1.x, acc[4]);
+      acc[5] = fmaf(w, x1.y, acc[5]);
+      acc[6] = fmaf(w, x1.z, acc[6]);
+      acc[7] = fmaf(w, x1.w, acc[7]);
+    }
+    __syncthreads();
+  }
+  const int r = row0 + orow;
+  if (r < rows) {
+    const float inv = s_inv[orow];
+    float4* o = reinterpret_cast<float4*>(out + ((int64_t)b * rows + r) * 64 + 8 * cb);
+    o[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+    o[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+  }
+}
+
 cudaError_t launch_spmm_simt_softmax_f32(const void* p, const uint32_t* meta, const void* v, void* out, int gs,
                                         int64_t bh, int rows, int n_k, int d, cudaStream_t s) {
   if (bh == 0 || rows == 0 || d == 0) return cudaSuccess;
   if (d > 64) return cudaErrorNotSupported;
+  // tiled from n_k = 512 up (L2-bound warp kernel: n = 1024 1.79 -> 1.50 ms for 96 heads); the
+  // warp-per-row kernel is faster on short rows (n = 384: 0.198 vs 0.233 ms, tools/time_f32_sweep.py)
+  if (d == 64 && n_k % 128 == 0 && n_k >= 512 && ((uintptr_t)v & 15) == 0 && ((uintptr_t)out & 15) == 0 &&
+      !getenv("DFSS_SPMM_WARP")) {
+    const dim3 grid((unsigned)((rows + 31) / 32), (unsigned)bh);
+    if (gs == 4)
+      spmm_softmax_f32_tiled_kernel<4><<<grid, 256, 0, s>>>((const float*)p, meta, (const float*)v, (float*)out,
+                                                            rows, n_k, MetaGeom(rows, n_k / 4));
+    else
+      spmm_softmax_f32_tiled_kernel<2><<<grid, 256, 0, s>>>((const float*)p, meta, (const float*)v, (float*)out,
+                                                            rows, n_k, MetaGeom(rows, n_k / 2));
+    return cudaGetLastError();
+  }
   if (d == 64 && ((uintptr_t)v & 15) == 0 && ((uintptr_t)out & 15) == 0) {
     const int64_t total = bh * rows;
     int64_t blocks = (total + 7) / 8;  // one row per warp

@@ -755,3 +755,12 @@ def test_block_mask_fuzz_many_items(case):
             ops = [_tf32(x) for x in ops]
         assert_close(out[0, h], _masked_oracle(*ops, mask, mode), 2e-2, 2e-2,
                      f"fuzz case {case}: n={n} tiles={tr}x{tc_} density={density} style={style} head {h}")
+
+
+@pytest.mark.parametrize("n,mode", [(512, "1:2"), (1024, "1:2"), (640, "2:4")])
+def test_exact_fp32_longer_rows_match_reference(n, mode):
+    """Exact-FP32 path at the 1e-5 bar on rows long enough for the shared-memory-tiled SpMM
+    (n >= 512; softmax fused), against the reference nm_attention in float64."""
+    (q, k, v), (q64, k64, v64) = seeded_qkv((1, 3, n, 64), torch.float32, seed=n + 7)
+    out = _np(dfss.dfss_attention(q, k, v, mode, math_mode="ffma"))
+    assert_close(out, oracle_attention(q64, k64, v64, mode), 1e-5, 1e-5, f"exact fp32 {mode} n={n}")

@@ -164,6 +164,31 @@ int dfss_nm_attention_masked(const void* q, const void* k, const void* v, void* 
                              void* workspace, int64_t workspace_bytes, void* stream);
 
 /*
+ * Parity hook for the path dfss_nm_attention_masked takes (same arguments, same kernels, same
+ * output), with the selection evidence of every prune: scores_dbg (device fp32 [bh, n, n]) gets
+ * the post-scale scores each prune compared -- for the fused kernels the fp32 tcgen05
+ * accumulators of Q K^T times the exact scale 1/sqrt(64) = 2^-3, in key order -- and meta_dbg
+ * (device uint32, dfss_meta_hw_words(*meta_mode, bh, n, n) words) the metadata words handed to
+ * tcgen05.mma.sp (fused) or written by the SDDMM (staged), in the meta_hw layout above.
+ * *meta_mode (host int) is the group size of that layout: 4 for the fused 16-bit kernel, which
+ * runs 1:2 as the 2:4 pattern "one survivor per pair" (nibble 8 + a + 4b: elements a and 2 + b),
+ * and the call's mode otherwise.  Entries of 128 x 128 steps the fused kernels skip (fully
+ * masked) are not written.  The selection test feeds scores_dbg to the reference
+ * compress_logical / prune_dense (codec.py:324-335) and compares the decoded metadata bitwise.
+ * Replaces: nothing in the reference (its fused path keeps no dense scores by design,
+ * fused.py:22-38); this is the evidence channel for _kernels_numba.py:145-184 on the GPU path.
+ */
+int dfss_nm_attention_dump(const void* q, const void* k, const void* v, void* out, int mode, int dtype, int math,
+                           int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows, int tile_cols,
+                           void* workspace, int64_t workspace_bytes, float* scores_dbg, uint32_t* meta_dbg,
+                           int* meta_mode, void* stream);
+
+/* Which path dfss_nm_attention(_masked) takes for these arguments (no launch): 1 fused 16-bit
+ * (flash_tc.cu), 2 fused tf32 (flash_tf32.cu), 3 staged tcgen05 SDDMM + softmax-fused SpMM,
+ * 4 staged exact-FP32 FFMA, 5 staged with a block mask; a negative dfss_status if unsupported. */
+int dfss_nm_attention_path(int mode, int dtype, int math, int n, int d, int tile_rows, int tile_cols, int masked);
+
+/*
  * Parity hook: prune a given fp32 score tensor with the SAME device selection
  * routine the SDDMM epilogue uses (codec._select_rows, codec.py:289-313).
  *   scores [rows, cols] fp32 -> nonzeros [rows, cols/2] (nz_dtype),
@@ -178,6 +203,40 @@ int dfss_meta_hw_to_logical(const uint32_t* meta_hw, uint8_t* meta_logical, int 
                             int cols, void* stream);
 int dfss_meta_logical_to_hw(const uint8_t* meta_logical, uint32_t* meta_hw, int mode, int64_t bh, int rows,
                             int cols, void* stream);
+
+/*
+ * The reference kernel module (backend.kernels(), backend.py:63-67) on the GPU, float64.
+ * The reference's hot loops are five duck-typed functions (_kernels_numba.py:39,62,87,106,188);
+ * these are the same five, on DEVICE float64 buffers, computed with the reference's arithmetic:
+ * one running accumulator per output, ascending reduction index, separately rounded products
+ * and sums (numba runs with fastmath off).  sddmm_compress, spmm_gather and gemm_abt are
+ * therefore bitwise equal to the reference; the softmaxes differ only through exp (<= 1 ulp).
+ * integration/_kernels_cuda.py wraps them with the reference's Python signatures.  Unlike the
+ * production entry points above (tile masks, meta_hw words), these take the reference's
+ * arbitrary per-nonzero `present` masks and decoded int64 column indices.
+ */
+/* sddmm_compress (_kernels_numba.py:110-188): q [n, d], k [m, d]; keep uint8 [ceil(n/tile_rows),
+ * ceil(m/tile_cols)] (the reference always passes a grid); writes nonzeros [n, m/2] and logical
+ * meta uint8 [n, m/group_size], zero in masked tiles.  peak / nnz / nib are structural (host). */
+int dfss_kmod_sddmm_compress(const double* q, const double* k, double scale, int group_size, int n, int m, int d,
+                             int tile_rows, int tile_cols, const uint8_t* keep, double* nonzeros, uint8_t* meta,
+                             void* stream);
+/* softmax_nonzeros (_kernels_numba.py:66-87): nz [rows, cols], present uint8 [rows, cols]
+ * (nullable = all present) -> out [rows, cols], absent slots 0. */
+int dfss_kmod_softmax_nonzeros(const double* nz, const uint8_t* present, double* out, int64_t rows, int cols,
+                               void* stream);
+/* spmm_gather (_kernels_numba.py:91-106): nz [rows, nz_cols], cols int64 [rows, nz_cols],
+ * present uint8 [rows, nz_cols] (nullable), v [v_rows, d] -> out [rows, d].  err (nullable, device
+ * int32, caller-initialised to INT32_MAX) receives the first row holding a column outside
+ * [0, v_rows) -- such entries are skipped. */
+int dfss_kmod_spmm_gather(const double* nz, const int64_t* cols, const uint8_t* present, const double* v,
+                          double* out, int64_t rows, int nz_cols, int v_rows, int d, int32_t* err, void* stream);
+/* gemm_abt (_kernels_numba.py:16-39): out [n, m] = scale * a [n, kdim] . b [m, kdim]^T (the
+ * reference's tile / k-panel arguments only reorder traversal, never the per-element sum). */
+int dfss_kmod_gemm_abt(const double* a, const double* b, double scale, int64_t n, int64_t m, int kdim, double* out,
+                       void* stream);
+/* row_softmax_dense (_kernels_numba.py:43-62): x [rows, cols] -> out [rows, cols]. */
+int dfss_kmod_row_softmax_dense(const double* x, double* out, int64_t rows, int cols, void* stream);
 
 /* Human-readable status; last CUDA error text for DFSS_ERR_CUDA. Never NULL. */
 const char* dfss_status_string(int status);

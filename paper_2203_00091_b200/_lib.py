@@ -42,9 +42,18 @@ SIGNATURES = {
     "dfss_nm_attention": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i64, _i32, _i32, _vp, _i64, _vp]),
     "dfss_nm_attention_masked": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i64, _i32, _i32, _vp, _i32, _i32, _vp,
                                         _i64, _vp]),
+    "dfss_nm_attention_dump": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i64, _i32, _i32, _vp, _i32, _i32, _vp,
+                                      _i64, _vp, _vp, _vp, _vp]),
+    "dfss_nm_attention_path": (_i32, [_i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32]),
     "dfss_prune_scores": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i64, _i32, _vp]),
     "dfss_meta_hw_to_logical": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp]),
     "dfss_meta_logical_to_hw": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp]),
+    "dfss_kmod_sddmm_compress": (_i32, [_vp, _vp, ctypes.c_double, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp,
+                                        _vp]),
+    "dfss_kmod_softmax_nonzeros": (_i32, [_vp, _vp, _vp, _i64, _i32, _vp]),
+    "dfss_kmod_spmm_gather": (_i32, [_vp, _vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp]),
+    "dfss_kmod_gemm_abt": (_i32, [_vp, _vp, ctypes.c_double, _i64, _i64, _i32, _vp, _vp]),
+    "dfss_kmod_row_softmax_dense": (_i32, [_vp, _vp, _i64, _i32, _vp]),
     "dfss_status_string": (ctypes.c_char_p, [_i32]),
     "dfss_last_error": (ctypes.c_char_p, []),
     "dfss_has_tcgen05": (_i32, []),

@@ -9,6 +9,7 @@
 #include <string>
 
 #include "dfss_common.cuh"
+#include "tc_common.cuh"
 
 namespace {
 
@@ -54,13 +55,7 @@ const char* dfss_status_string(int status) {
 
 const char* dfss_last_error(void) { return g_last_error.c_str(); }
 
-int dfss_has_tcgen05(void) {
-  int dev = 0, major = 0, minor = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return 0;
-  if (cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) return 0;
-  return (major == 10 && minor == 0) ? 1 : 0;
-}
+int dfss_has_tcgen05(void) { return dfss::device_cc(dfss::current_device()) == 100 ? 1 : 0; }
 
 int64_t dfss_meta_hw_words(int mode, int64_t bh, int64_t rows, int64_t cols) {
   if (!valid_mode(mode) || rows < 0 || cols < 0 || bh < 0) return -1;
@@ -152,9 +147,33 @@ int dfss_nm_attention(const void* q, const void* k, const void* v, void* out, in
                                   workspace_bytes, stream);
 }
 
-int dfss_nm_attention_masked(const void* q, const void* k, const void* v, void* out, int mode, int dtype, int math,
-                             int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows, int tile_cols,
-                             void* workspace, int64_t workspace_bytes, void* stream) {
+}  // extern "C"
+
+namespace {
+
+enum Path { kFused16 = 1, kFusedTf32 = 2, kStagedTc = 3, kStagedFfma = 4, kStagedMasked = 5 };
+
+// The path dfss_nm_attention(_masked) takes (no launch).  Validation is the caller's.
+int attention_path(int mode, int dtype, int math, int n, int d, bool masked, int tile_rows, int tile_cols) {
+  const bool tc = dfss_has_tcgen05() != 0;
+  if (math == DFSS_MATH_AUTO && dtype != DFSS_F32 && dfss::tc_flash_supported(mode, dtype, n, d) &&
+      (!masked || dfss::tc_flash_mask_supported(tile_rows, tile_cols)) && tc)
+    return kFused16;
+  if (math == DFSS_MATH_TF32 && dtype == DFSS_F32 && dfss::tc_flash_tf32_supported(mode, n, d) &&
+      (!masked || (dfss::tc_flash_mask_supported(tile_rows, tile_cols) && dfss::flash_mask_two_set_ok(n))) && tc)
+    return kFusedTf32;
+  if (math == DFSS_MATH_TF32) return DFSS_ERR_UNSUPPORTED;
+  if (masked) return kStagedMasked;
+  if (math == DFSS_MATH_AUTO && dtype != DFSS_F32 && dfss::tc_sddmm_supported(mode, dtype, dtype, n, n, d) &&
+      dfss::tc_spmm_supported(mode, dtype, dtype, dtype, n, n, d) && tc)
+    return kStagedTc;
+  return kStagedFfma;
+}
+
+int nm_attention_impl(const void* q, const void* k, const void* v, void* out, int mode, int dtype, int math,
+                      int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows, int tile_cols,
+                      void* workspace, int64_t workspace_bytes, void* stream, float* dump_s, uint32_t* dump_meta,
+                      int* dump_meta_mode) {
   if (!valid_mode(mode)) return fail(DFSS_ERR_INVALID, "unknown sparsity mode (expected 2 or 4)");
   if (!valid_dtype(dtype)) return fail(DFSS_ERR_INVALID, "unknown dtype");
   if (bh < 0 || n < 1 || d < 1) return fail(DFSS_ERR_INVALID, "shape dimensions must be positive");
@@ -163,6 +182,11 @@ int dfss_nm_attention_masked(const void* q, const void* k, const void* v, void* 
   const int64_t need =
       dfss_nm_attention_workspace_bytes_for(mode, dtype, math, bh, n, d, tile_rows, tile_cols, tile_keep != nullptr);
   if (need > 0 && (!workspace || workspace_bytes < need)) return fail(DFSS_ERR_INVALID, "workspace too small");
+  const int path = attention_path(mode, dtype, math, n, d, tile_keep != nullptr, tile_rows, tile_cols);
+  if (path < 0) return fail(DFSS_ERR_UNSUPPORTED, "tf32 attention needs fp32 inputs, mode 1:2, d = 64 and n % 128 == 0");
+  const bool dumping = dump_s != nullptr;
+  if (dumping && !dump_meta) return fail(DFSS_ERR_INVALID, "dump needs both score and metadata buffers");
+  if (dump_meta_mode) *dump_meta_mode = path == kFused16 ? DFSS_MODE_2_4 : mode;
   if (bh == 0) return DFSS_OK;
   const int64_t nz_bytes = bh * (int64_t)n * (n / 2) * dfss::dtype_bytes(dtype);
   const int64_t meta_bytes = dfss_meta_hw_words(mode, bh, n, n) * 4;
@@ -171,43 +195,69 @@ int dfss_nm_attention_masked(const void* q, const void* k, const void* v, void* 
   uint32_t* meta = (uint32_t*)(ws + (nz_bytes + 255) / 256 * 256);
   float* row_max = (float*)(ws + (nz_bytes + 255) / 256 * 256 + (meta_bytes + 255) / 256 * 256);
   const float scale = 1.0f / sqrtf((float)d);
-  // fully fused: one kernel, no n x n tensor in HBM (flash_tc.cu); block masks with 32-aligned tiles
-  if (math == DFSS_MATH_AUTO && dtype != DFSS_F32 && dfss::tc_flash_supported(mode, dtype, n, d) &&
-      (!tile_keep || dfss::tc_flash_mask_supported(tile_rows, tile_cols)) && dfss_has_tcgen05())
-    return cuda_status(dfss::launch_flash_tc(q, k, v, out, scale, mode, dtype, bh, n, d, tile_keep, tile_rows,
-                                             tile_cols, workspace, (cudaStream_t)stream));
-  // tf32 1:2 on fp32 inputs: the fused tf32 kernel (configs[4] "1:2 tf32")
-  if (math == DFSS_MATH_TF32 && dtype == DFSS_F32 && dfss::tc_flash_tf32_supported(mode, n, d) &&
-      (!tile_keep || (dfss::tc_flash_mask_supported(tile_rows, tile_cols) && dfss::flash_mask_two_set_ok(n))) &&
-      dfss_has_tcgen05())
-    return cuda_status(dfss::launch_flash_tf32(q, k, v, out, scale, bh, n, d, tile_keep, tile_rows, tile_cols,
-                                               workspace, (cudaStream_t)stream));  // V^T in the workspace
-  if (math == DFSS_MATH_TF32)
-    return fail(DFSS_ERR_UNSUPPORTED, "tf32 attention needs fp32 inputs, mode 1:2, d = 64 and n % 128 == 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (path) {
+    case kFused16:  // fully fused: one kernel, no n x n tensor in HBM (flash_tc.cu); 32-aligned block masks
+      if (dumping)
+        return cuda_status(dfss::launch_flash_tc_dump(q, k, v, out, scale, mode, dtype, bh, n, d, tile_keep,
+                                                      tile_rows, tile_cols, workspace, dump_s, dump_meta, s));
+      return cuda_status(dfss::launch_flash_tc(q, k, v, out, scale, mode, dtype, bh, n, d, tile_keep, tile_rows,
+                                               tile_cols, workspace, s));
+    case kFusedTf32:  // tf32 1:2 on fp32 inputs (configs[4] "1:2 tf32"); V^T in the workspace
+      return cuda_status(dfss::launch_flash_tf32(q, k, v, out, scale, bh, n, d, tile_keep, tile_rows, tile_cols,
+                                                 workspace, s, dump_s, dump_meta));
+    default: break;
+  }
+  // staged: the dump is the SDDMM's post-scale score hook plus a copy of its metadata
   if (tile_keep) {
-    // staged with the mask threaded through every stage (fused.py:73-82, sparse_ops.py:27-30,57-64)
+    // the mask threaded through every stage (fused.py:73-82, sparse_ops.py:27-30,57-64)
     int st = dfss_sddmm_prune(q, k, nz, meta, scale, mode, dtype, dtype, math, bh, n, n, d, tile_keep, tile_rows,
-                              tile_cols, nullptr, nullptr, stream);
+                              tile_cols, dump_s, nullptr, stream);
+    if (!st && dumping) st = cuda_status(cudaMemcpyAsync(dump_meta, meta, meta_bytes, cudaMemcpyDeviceToDevice, s));
     if (st) return st;
     st = dfss_softmax_rows(nz, nz, dtype, dtype, bh, n, n / 2, tile_keep, tile_rows, tile_cols, nullptr, stream);
     if (st) return st;
     return dfss_spmm(nz, meta, v, out, mode, dtype, dtype, dtype, bh, n, n, d, tile_keep, tile_rows, tile_cols,
                      nullptr, stream);
   }
-  // fused path: SDDMM+prune (+row max) -> SpMM with the softmax applied to the staged P tiles
-  const bool fused = math == DFSS_MATH_AUTO && dtype != DFSS_F32 &&
-                     dfss::tc_sddmm_supported(mode, dtype, dtype, n, n, d) &&
-                     dfss::tc_spmm_supported(mode, dtype, dtype, dtype, n, n, d) && dfss_has_tcgen05();
-  int st = dfss_sddmm_prune(q, k, nz, meta, scale, mode, dtype, dtype, math, bh, n, n, d, nullptr, 0, 0, nullptr,
+  // SDDMM+prune (+row max) -> SpMM with the softmax applied to the staged P tiles
+  const bool fused = path == kStagedTc;
+  int st = dfss_sddmm_prune(q, k, nz, meta, scale, mode, dtype, dtype, math, bh, n, n, d, nullptr, 0, 0, dump_s,
                             fused ? row_max : nullptr, stream);
+  if (!st && dumping) st = cuda_status(cudaMemcpyAsync(dump_meta, meta, meta_bytes, cudaMemcpyDeviceToDevice, s));
   if (st) return st;
   if (fused)
     return dfss_spmm(nz, meta, v, out, mode, dtype, dtype, dtype, bh, n, n, d, nullptr, 0, 0, row_max, stream);
   if (dtype == DFSS_F32 && d <= 64)  // exact FP32: softmax fused into the SIMT SpMM (one pass less)
-    return cuda_status(dfss::launch_spmm_simt_softmax_f32(nz, meta, v, out, mode, bh, n, n, d, (cudaStream_t)stream));
+    return cuda_status(dfss::launch_spmm_simt_softmax_f32(nz, meta, v, out, mode, bh, n, n, d, s));
   st = dfss_softmax_rows(nz, nz, dtype, dtype, bh, n, n / 2, nullptr, 0, 0, nullptr, stream);
   if (st) return st;
   return dfss_spmm(nz, meta, v, out, mode, dtype, dtype, dtype, bh, n, n, d, nullptr, 0, 0, nullptr, stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+int dfss_nm_attention_masked(const void* q, const void* k, const void* v, void* out, int mode, int dtype, int math,
+                             int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows, int tile_cols,
+                             void* workspace, int64_t workspace_bytes, void* stream) {
+  return nm_attention_impl(q, k, v, out, mode, dtype, math, bh, n, d, tile_keep, tile_rows, tile_cols, workspace,
+                           workspace_bytes, stream, nullptr, nullptr, nullptr);
+}
+
+int dfss_nm_attention_dump(const void* q, const void* k, const void* v, void* out, int mode, int dtype, int math,
+                           int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows, int tile_cols,
+                           void* workspace, int64_t workspace_bytes, float* scores_dbg, uint32_t* meta_dbg,
+                           int* meta_mode, void* stream) {
+  if (!scores_dbg || !meta_dbg) return fail(DFSS_ERR_INVALID, "null dump buffer");
+  return nm_attention_impl(q, k, v, out, mode, dtype, math, bh, n, d, tile_keep, tile_rows, tile_cols, workspace,
+                           workspace_bytes, stream, scores_dbg, meta_dbg, meta_mode);
+}
+
+int dfss_nm_attention_path(int mode, int dtype, int math, int n, int d, int tile_rows, int tile_cols, int masked) {
+  if (!valid_mode(mode) || !valid_dtype(dtype) || n < 1 || d < 1) return DFSS_ERR_INVALID;
+  return attention_path(mode, dtype, math, n, d, masked != 0, tile_rows, tile_cols);
 }
 
 int dfss_prune_scores(const float* scores, void* nonzeros, uint8_t* meta_logical, uint8_t* kept, int mode,
@@ -234,6 +284,49 @@ int dfss_meta_logical_to_hw(const uint8_t* meta_logical, uint32_t* meta_hw, int 
     return fail(DFSS_ERR_INVALID, "invalid metadata geometry");
   if (!meta_hw || !meta_logical) return fail(DFSS_ERR_INVALID, "null tensor pointer");
   return cuda_status(dfss::launch_meta_logical_to_hw(meta_logical, meta_hw, mode, bh, rows, cols, (cudaStream_t)stream));
+}
+
+// ---------------------------------------------------------------- reference kernel module (float64)
+
+int dfss_kmod_sddmm_compress(const double* q, const double* k, double scale, int group_size, int n, int m, int d,
+                             int tile_rows, int tile_cols, const uint8_t* keep, double* nonzeros, uint8_t* meta,
+                             void* stream) {
+  if (group_size != 2 && group_size != 4) return fail(DFSS_ERR_INVALID, "group size must be 2 or 4");
+  if (n < 0 || m < 0 || d < 0) return fail(DFSS_ERR_INVALID, "shape dimensions must be non-negative");
+  if (m % group_size) return fail(DFSS_ERR_INVALID, "score columns not group-aligned for the mode");
+  if (tile_rows < 1 || tile_cols < 1 || tile_cols % group_size)
+    return fail(DFSS_ERR_INVALID, "tile columns must be a positive multiple of the group size");
+  if ((n && m && (!q || !k || !keep)) || !nonzeros || !meta) return fail(DFSS_ERR_INVALID, "null tensor pointer");
+  return cuda_status(dfss::launch_kmod_sddmm_compress(q, k, scale, group_size, n, m, d, tile_rows, tile_cols, keep,
+                                                      nonzeros, meta, (cudaStream_t)stream));
+}
+
+int dfss_kmod_softmax_nonzeros(const double* nz, const uint8_t* present, double* out, int64_t rows, int cols,
+                               void* stream) {
+  if (rows < 0 || cols < 0) return fail(DFSS_ERR_INVALID, "shape dimensions must be non-negative");
+  if (rows && cols && (!nz || !out)) return fail(DFSS_ERR_INVALID, "null tensor pointer");
+  return cuda_status(dfss::launch_kmod_softmax(nz, present, out, rows, cols, false, (cudaStream_t)stream));
+}
+
+int dfss_kmod_spmm_gather(const double* nz, const int64_t* cols, const uint8_t* present, const double* v,
+                          double* out, int64_t rows, int nz_cols, int v_rows, int d, int32_t* err, void* stream) {
+  if (rows < 0 || nz_cols < 0 || v_rows < 0 || d < 0) return fail(DFSS_ERR_INVALID, "shape dimensions must be non-negative");
+  if (rows && d && (!out || (nz_cols && (!nz || !cols || !v)))) return fail(DFSS_ERR_INVALID, "null tensor pointer");
+  return cuda_status(dfss::launch_kmod_spmm_gather(nz, cols, present, v, out, rows, nz_cols, v_rows, d, err,
+                                                   (cudaStream_t)stream));
+}
+
+int dfss_kmod_gemm_abt(const double* a, const double* b, double scale, int64_t n, int64_t m, int kdim, double* out,
+                       void* stream) {
+  if (n < 0 || m < 0 || kdim < 0) return fail(DFSS_ERR_INVALID, "shape dimensions must be non-negative");
+  if (n && m && (!out || (kdim && (!a || !b)))) return fail(DFSS_ERR_INVALID, "null tensor pointer");
+  return cuda_status(dfss::launch_kmod_gemm_abt(a, b, scale, n, m, kdim, out, (cudaStream_t)stream));
+}
+
+int dfss_kmod_row_softmax_dense(const double* x, double* out, int64_t rows, int cols, void* stream) {
+  if (rows < 0 || cols < 0) return fail(DFSS_ERR_INVALID, "shape dimensions must be non-negative");
+  if (rows && cols && (!x || !out)) return fail(DFSS_ERR_INVALID, "null tensor pointer");
+  return cuda_status(dfss::launch_kmod_softmax(x, nullptr, out, rows, cols, true, (cudaStream_t)stream));
 }
 
 }  // extern "C"

@@ -218,7 +218,26 @@ bool tc_flash_tf32_supported(int gs, int n, int d);
 // vt_scratch: flash_tf32_workspace_bytes of device scratch -- V^T (the kind::tf32 B operand
 // must be K-major), then the block-mask bitmaps when tile_keep is given (n <= 32768)
 int64_t flash_tf32_workspace_bytes(int64_t bh, int n, bool masked);
+// dump_scores / dump_meta (both or neither): the DUMP kernel also stores the post-scale scores
+// [bh, n, n] and the 1:2 metadata words (meta_hw layout) it fed to tcgen05.mma.sp
 cudaError_t launch_flash_tf32(const void* q, const void* k, const void* v, void* out, float scale, int64_t bh, int n,
                               int d, const uint8_t* tile_keep, int tile_rows, int tile_cols, void* vt_scratch,
-                              cudaStream_t s);
+                              cudaStream_t s, float* dump_scores = nullptr, uint32_t* dump_meta = nullptr);
+// launch_flash_tc with the DUMP kernels (flash_tc_dump.cu): post-scale scores [bh, n, n] fp32 and
+// the metadata words in the 2:4 meta_hw layout (1:2 is run as the 2:4 pattern 8 + a + 4b)
+cudaError_t launch_flash_tc_dump(const void* q, const void* k, const void* v, void* out, float scale, int gs,
+                                 int dtype, int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows,
+                                 int tile_cols, void* workspace, float* dump_scores, uint32_t* dump_meta,
+                                 cudaStream_t s);
+// reference kernel module in float64 (kmod_f64.cu): bitwise the numba arithmetic (exp aside)
+cudaError_t launch_kmod_sddmm_compress(const double* q, const double* k, double scale, int gs, int n, int m, int d,
+                                       int tile_rows, int tile_cols, const uint8_t* keep, double* nonzeros,
+                                       uint8_t* meta, cudaStream_t s);
+cudaError_t launch_kmod_softmax(const double* x, const uint8_t* present, double* out, int64_t rows, int cols,
+                                bool dense, cudaStream_t s);
+cudaError_t launch_kmod_spmm_gather(const double* nz, const int64_t* cols, const uint8_t* present, const double* v,
+                                    double* out, int64_t rows, int nzc, int v_rows, int d, int32_t* err,
+                                    cudaStream_t s);
+cudaError_t launch_kmod_gemm_abt(const double* a, const double* b, double scale, int64_t n, int64_t m, int kdim,
+                                 double* out, cudaStream_t s);
 }  // namespace dfss

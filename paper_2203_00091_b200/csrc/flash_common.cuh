@@ -59,12 +59,25 @@ __device__ __forceinline__ bool bar_any(uint32_t id, uint32_t count, bool pred) 
   return r != 0;
 }
 
-// role-warp wait: sleeping try_wait, or spinning with variant bit 10 (experiment)
-__device__ __forceinline__ void wait_role(int variant, uint64_t* bar, uint32_t parity) {
-  if (variant & 1024)
-    tc::mbar_wait(bar, parity);
-  else
-    tc::mbar_wait_sleep(bar, parity);
+// role-warp wait: try_wait with a suspend-time hint (the waiting warp yields its issue slots)
+__device__ __forceinline__ void wait_role(uint64_t* bar, uint32_t parity) { tc::mbar_wait_sleep(bar, parity); }
+
+// Parity dump of the fused kernels (DUMP instantiations only, dfss_nm_attention_dump): the
+// post-scale fp32 scores every prune compared, [bh, n, n] in true key order, and the metadata
+// words handed to tcgen05.mma.sp, in the meta_hw layout of include/dfss.h.
+struct FlashDump {
+  float* s = nullptr;
+  uint32_t* meta = nullptr;
+};
+
+// one 32-column chunk of one row: registers in (k0, k2, k1, k3) order per group of 4 (the
+// permuted K tensor map) back to key order, times the exact power-of-two scale 1/sqrt(64)
+__device__ __forceinline__ void dump_chunk_scores(float* dst, const uint32_t (&s)[32], float scale) {
+  float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+  for (int g = 0; g < 8; ++g)
+    d4[g] = make_float4(__uint_as_float(s[4 * g]) * scale, __uint_as_float(s[4 * g + 2]) * scale,
+                        __uint_as_float(s[4 * g + 1]) * scale, __uint_as_float(s[4 * g + 3]) * scale);
 }
 
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {

@@ -134,11 +134,11 @@ __device__ __forceinline__ void prune_exp_tile(const uint32_t (&s)[32], float c,
   }
 }
 
-template <typename T, int HALVES, bool PAIRS, bool MASKED>
+template <typename T, int HALVES, bool PAIRS, bool MASKED, bool DUMP>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     dfss_flash_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, T* __restrict__ out, float scale, int bh, int n,
-                      uint32_t two, int variant, TileMask tmask) {
+                      uint32_t two, FlashDump dump, TileMask tmask) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + SMEM_BAR);
@@ -251,13 +251,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tc::mbar_wait_sleep(&s_empty[sb], ((g >> 1) & 1) ^ 1);  // step g-2 read by every softmax warp
             tc::tc_fence_after();
             const uint32_t q_addr = tc::smem_u32(smem + SMEM_Q + (2 * qs + h) * Q_BYTES);
-            if (!(variant & 32)) {
 #pragma unroll
-              for (int kk = 0; kk < HD / 16; ++kk) {
-                const uint64_t ad = tc::smem_desc(q_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
-                const uint64_t bd = tc::smem_desc(k_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
-                tc::mma_f16_ss(tmem_base + sb * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
-              }
+            for (int kk = 0; kk < HD / 16; ++kk) {
+              const uint64_t ad = tc::smem_desc(q_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
+              const uint64_t bd = tc::smem_desc(k_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
+              tc::mma_f16_ss(tmem_base + sb * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
             }
             tc::mma_commit(&s_full[sb]);
           }
@@ -285,7 +283,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tc::tc_fence_after();
             const uint32_t p_addr = tc::smem_u32(smem + SMEM_P + pb * P_BYTES);
 #pragma unroll
-            for (int q = 0; q < ((variant & 16) ? 0 : 4); ++q) {
+            for (int q = 0; q < 4; ++q) {
               const uint64_t ad = tc::smem_desc(p_addr + q * 32, 16, 1024, tc::kSwizzle128B);
               const uint64_t bd = tc::smem_desc(v_addr + q * 32 * 128, V_BYTES, 1024, tc::kSwizzle128B);
               // metadata column: even address + sparse_id2 (idesc bits [0,2)) selects the odd one
@@ -346,6 +344,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc::tc_fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
+          if constexpr (DUMP)
+            dump_chunk_scores(dump.s + ((int64_t)b * n + (ib * HALVES + h) * BM + r) * n + t * BN + quarter * 32, s,
+                              scale);
           uint32_t pk[8], W;
           float lt0, lt1;
           cmask = MASKED && tmask.masked((ib * HALVES + h) * BM + quad * 32, t * BN + quarter * 32);
@@ -358,14 +359,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             l0[h] = l1[h] = 0.f;
             if (cmask) masked_chunk(pk, W, lt0, lt1); else prune_exp_tile<T, PAIRS>(s, c, mlog[h], two, pk, W, lt0, lt1);
           } else {
-            if (variant & 8) {  // timing experiment: no prune / exp arithmetic
-#pragma unroll
-              for (int j = 0; j < 8; ++j) pk[j] = s[j] ^ s[j + 8];
-              W = 0x44444444u;
-              lt0 = lt1 = 0.f;
-            } else {
-              if (cmask) masked_chunk(pk, W, lt0, lt1); else prune_exp_tile<T, PAIRS>(s, c, mlog[h], two, pk, W, lt0, lt1);
-            }
+            if (cmask) masked_chunk(pk, W, lt0, lt1); else prune_exp_tile<T, PAIRS>(s, c, mlog[h], two, pk, W, lt0, lt1);
             if (bar_any(qbar, 128, !(lt0 + lt1 <= kSumLimit))) {
               // ---- slow path (whole quad): raise the shift to the row maximum, rescale O_h and the sums.
               // Every PV into O_h issued so far has retired: with PST == HALVES the P-stage wait
@@ -396,6 +390,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t partner = __shfl_xor_sync(0xffffffffu, W, 8);
           const uint32_t word = (lane & 8) ? ((partner >> 16) | (W & 0xFFFF0000u)) : ((W & 0xFFFFu) | (partner << 16));
           tc::tmem_st_32x32b_x1(lane_base + TM_E + pb * 4 + quarter, word);
+          if constexpr (DUMP)
+            dump.meta[(((int64_t)b * (n / BM) + ib * HALVES + h) * (n / 32) + 4 * t + quarter) * BM + r] = word;
           tc::tmem_st_wait();
           tc::fence_proxy_async();  // P smem writes -> tensor core
           tc::tc_fence_before();
@@ -479,8 +475,8 @@ static_assert(S2_TOTAL <= 227 * 1024, "shared memory budget");
 // bring-up timeline (DFSS_FLASH_TRACE=<file>): clock64 at pipeline events of CTA 0, first 2
 // items.  Compiled in only with -DDFSS_FLASH_TRACE_BUILD (DFSS_NVCC_EXTRA, tools/trace_flash.py):
 // the per-lane trace predicates cost ~5 % issue slots in the epilogue-bound kernel.
-__device__ unsigned long long* g_flash_trace = nullptr;
 #ifdef DFSS_FLASH_TRACE_BUILD
+__device__ unsigned long long* g_flash_trace = nullptr;
 #define FTRACE(slot, it_, t_, h_)                                                                  \
   do {                                                                                             \
     if (trace && (it_) < 2 && (t_) < 64)                                                           \
@@ -492,11 +488,11 @@ __device__ unsigned long long* g_flash_trace = nullptr;
   } while (0)
 #endif
 
-template <typename T, bool PAIRS, bool MASKED>
+template <typename T, bool PAIRS, bool MASKED, bool DUMP>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     dfss_flash2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, T* __restrict__ out, float scale, int bh, int n,
-                       uint32_t two, int variant, TileMask tmask) {
+                       uint32_t two, FlashDump dump, TileMask tmask) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + S2_BAR);
@@ -616,19 +612,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t lw0 = 0, lw1 = 0;
         const int b = item / iblocks, ib = item % iblocks;
         const int qs = it & 1;
-        wait_role(variant, &q_empty[qs], ((it >> 1) & 1) ^ 1);
+        wait_role(&q_empty[qs], ((it >> 1) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&q_full[qs], 2 * Q_BYTES);
         tc::tma_load_3d(smem + S2_Q + (2 * qs) * Q_BYTES, &tm_q, &q_full[qs], 0, ib * 2 * BM, b);
         tc::tma_load_3d(smem + S2_Q + (2 * qs + 1) * Q_BYTES, &tm_q, &q_full[qs], 0, ib * 2 * BM + BM, b);
         for (int t = 0; t < ntiles; ++t) {
           live_words(ib, t, lw0, lw1);
           if (MASKED && !(((lw0 | lw1) >> (t & 31)) & 1u)) continue;
-          wait_role(variant, &k_empty[ks], kph ^ 1);
+          wait_role(&k_empty[ks], kph ^ 1);
           tc::mbar_arrive_expect_tx(&k_full[ks], K_BYTES);
           tc::tma_load_5d(smem + S2_K + ks * K_BYTES, &tm_k, &k_full[ks], 0, 0, 0, t * (BN / 4), b);
           FTRACE(8, it, t, 0);
           if (++ks == K2ST) { ks = 0; kph ^= 1; }
-          wait_role(variant, &v_empty[vs], vph ^ 1);
+          wait_role(&v_empty[vs], vph ^ 1);
           tc::mbar_arrive_expect_tx(&v_full[vs], V_BYTES);
           tc::tma_load_3d(smem + S2_V + vs * V_BYTES, &tm_v, &v_full[vs], 0, t * BN, b);
           FTRACE(9, it, t, 0);
@@ -648,29 +644,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t lw0 = 0, lw1 = 0;
         const int qs = it & 1;
         const int ib = item % iblocks;
-        wait_role(variant, &q_full[qs], (it >> 1) & 1);
+        wait_role(&q_full[qs], (it >> 1) & 1);
         for (int t = 0; t < ntiles; ++t) {
           live_words(ib, t, lw0, lw1);
           const bool lv[2] = {bit_u(lw0, t), bit_u(lw1, t)};
           if (MASKED && !lv[0] && !lv[1]) continue;
-          wait_role(variant, &k_full[ks], kph);
+          wait_role(&k_full[ks], kph);
           if (lane == 0) FTRACE(10, it, t, 0);
           const uint32_t k_addr = tc::smem_u32(smem + S2_K + ks * K_BYTES);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             if (MASKED && !lv[h]) continue;
             if (lane == 0) FTRACE(3, it, t, h);
-            wait_role(variant, &s_free[sb], sph ^ 1);  // PV of step g - 3 retired
+            wait_role(&s_free[sb], sph ^ 1);  // PV of step g - 3 retired
             if (lane == 0) FTRACE(4, it, t, h);
             tc::tc_fence_after();
             const uint32_t q_addr = tc::smem_u32(smem + S2_Q + (2 * qs + h) * Q_BYTES);
-            if (!(variant & 32)) {
 #pragma unroll
-              for (int kk = 0; kk < HD / 16; ++kk) {
-                const uint64_t ad = tc::smem_desc(q_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
-                const uint64_t bd = tc::smem_desc(k_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
-                tc::mma_f16_ss_w(tmem_base + sb * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
-              }
+            for (int kk = 0; kk < HD / 16; ++kk) {
+              const uint64_t ad = tc::smem_desc(q_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
+              const uint64_t bd = tc::smem_desc(k_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
+              tc::mma_f16_ss_w(tmem_base + sb * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
             }
             tc::mma_commit_w(&s_full[h * S2RING + sb]);
             if (lane == 0) FTRACE(5, it, t, h);
@@ -701,7 +695,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // released meanwhile or the producer stalls (deadlock on one-sided masks).
         bool o_free = false;
         auto await_o_free = [&]() {
-          if (!o_free) wait_role(variant, &o_empty[h], (it & 1) ^ 1);
+          if (!o_free) wait_role(&o_empty[h], (it & 1) ^ 1);
           o_free = true;
         };
         bool first = true;  // first live step of this half-item initialises O_h
@@ -714,21 +708,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (MASKED && !(h ? l1 : l0)) {  // this half is masked here: release the V stage unused
             // wait for the load first: arriving early could complete the stage's PREVIOUS phase
             // while the other half's PV still reads it
-            wait_role(variant, &v_full[vs], vph);
+            wait_role(&v_full[vs], vph);
             if (lane == 0) tc::mbar_arrive(&v_empty[vs]);
             if (++vs == V2ST) { vs = 0; vph ^= 1; }
             continue;
           }
           await_o_free();
-          wait_role(variant, &v_full[vs], vph);
-          wait_role(variant, &p_full[h * S2RING + slot], (pbits >> slot) & 1);
+          wait_role(&v_full[vs], vph);
+          wait_role(&p_full[h * S2RING + slot], (pbits >> slot) & 1);
           pbits ^= 1u << slot;
           if (lane == 0) FTRACE(6, it, t, h);
           tc::tc_fence_after();
           const uint32_t v_addr = tc::smem_u32(smem + S2_V + vs * V_BYTES);
           const uint32_t s_col = tmem_base + slot * BN;
 #pragma unroll
-          for (int q = 0; q < ((variant & 16) ? 0 : 4); ++q) {
+          for (int q = 0; q < 4; ++q) {
             const uint64_t bd = tc::smem_desc(v_addr + q * 32 * 128, V_BYTES, 1024, tc::kSwizzle128B);
             tc::mma_sp_f16_ts_w(tmem_base + T2_O + h * HD, s_col + 32 * q + 16, bd, s_col + 32 * q, idesc_pv,
                                 (!first || q > 0) ? 1u : 0u);
@@ -853,14 +847,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tc::tmem_ld_32x32b_x32(scol + 32 * ch, s);
             tc::tmem_ld_wait(s);
             if (tw) FTRACE(11 + 2 * ch, it, t, h);
-            if (variant & 8) {  // timing experiment: no prune / exp arithmetic
-#pragma unroll
-              for (int j = 0; j < 8; ++j) pk[ch][j] = s[j] ^ s[j + 8];
-              W[ch] = 0x44444444u;
-              a0 = a1 = 0.f;
-            } else {
-              prune_exp_tile<T, PAIRS>(s, c, mlog, two, pk[ch], W[ch], a0, a1);
-            }
+            if constexpr (DUMP)
+              dump_chunk_scores(dump.s + ((int64_t)b * n + (ib * 2 + h) * BM + r) * n + t * BN + 64 * pr + 32 * ch, s,
+                                scale);
+            prune_exp_tile<T, PAIRS>(s, c, mlog, two, pk[ch], W[ch], a0, a1);
             // masked chunk (structurally absent): computed like the others -- straight-line code
             // keeps the two chunks interleaved -- then overwritten (predicated moves)
             if (MV && cm[ch]) masked_chunk(pk[ch], W[ch], a0, a1);
@@ -909,6 +899,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               (lane & 8) ? ((partner >> 16) | (W[ch] & 0xFFFF0000u)) : ((W[ch] & 0xFFFFu) | (partner << 16));
           tc::tmem_st_32x32b_x8(scol + 32 * ch + 16, pk[ch]);
           tc::tmem_st_32x32b_x1(scol + 32 * ch, word);
+          if constexpr (DUMP)
+            dump.meta[(((int64_t)b * (n / BM) + ib * 2 + h) * (n / 32) + 4 * t + 2 * pr + ch) * BM + r] = word;
         }
         tc::tmem_st_wait();
         tc::tc_fence_before();
@@ -939,6 +931,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (threadIdx.x == 0) FTRACE(15, 1, 0, 0);  // CTA end
 }
 
+#ifndef DFSS_FLASH_DUMP_TU  // defined once, in flash_tc.cu
 // BlockMask tile grid -> step / chunk bitmaps (TileMask::sbits / cbits) for the two-set
 // kernel; one thread per bit, a warp writes one word.
 __global__ void mask_bits_kernel(TileMask m, int n, uint32_t* __restrict__ sbits, uint32_t* __restrict__ cbits) {
@@ -1010,9 +1003,11 @@ bool tc_flash_supported(int gs, int dtype, int n, int d) {
   return (gs == 4 || gs == 2) && (dtype == DFSS_BF16 || dtype == DFSS_F16) && d == HD && n % BM == 0 && n > 0;
 }
 
-template <typename T, bool PAIRS, bool MASKED>
+#endif  // DFSS_FLASH_DUMP_TU
+
+template <typename T, bool PAIRS, bool MASKED, bool DUMP>
 static cudaError_t flash_launch_typed(const void* q, const void* k, const void* v, void* out, float scale, int64_t bh,
-                                      int n, TileMask tmask, void* workspace, cudaStream_t s) {
+                                      int n, TileMask tmask, void* workspace, FlashDump dump, cudaStream_t s) {
   const CUtensorMapDataType dt =
       std::is_same<T, __nv_bfloat16>::value ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv;
@@ -1021,34 +1016,28 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
   const uint64_t row = HD * 2;
   const uint64_t kdims[5] = {(uint64_t)HD, 2, 2, (uint64_t)n / 4, (uint64_t)bh};
   const uint64_t kstr[4] = {2 * row, row, 4 * row, (uint64_t)n * row};
-  uint32_t kbox[5] = {(uint32_t)HD, 2, 2, BN / 4, 1};
-  // n % 256 == 0: the two-set kernel (256-row items, 64-key tiles, independent softmax sets
-  // per half); otherwise 128-row items and 128-key tiles with all 16 softmax warps on one
-  // half.  DFSS_FLASH_KERNEL=1 forces the one-set kernel (experiments).
-  static const int force1 = getenv("DFSS_FLASH_KERNEL") ? atoi(getenv("DFSS_FLASH_KERNEL")) == 1 : 0;
-  // masked two-set kernel: one chunk word per lane (n <= 32768)
-  const bool two_set = n % (2 * BM) == 0 && !force1 && (!MASKED || flash_mask_two_set_ok(n));
-  const uint32_t kvbox = BN;
-  kbox[3] = kvbox / 4;
+  const uint32_t kbox[5] = {(uint32_t)HD, 2, 2, BN / 4, 1};
+  // n % 256 == 0: the two-set kernel (256-row items, independent softmax sets per half);
+  // otherwise 128-row items with all 16 softmax warps on one half
+  const bool two_set = n % (2 * BM) == 0 && (!MASKED || flash_mask_two_set_ok(n));
   if (!encode_tmap_3d(&tq, dt, 2, (void*)q, HD, n, bh, HD, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !encode_tmap(&tk, dt, 5, (void*)k, kdims, kstr, kbox, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !encode_tmap_3d(&tv, dt, 2, (void*)v, HD, n, bh, HD, kvbox, CU_TENSOR_MAP_SWIZZLE_128B))
+      !encode_tmap_3d(&tv, dt, 2, (void*)v, HD, n, bh, HD, BN, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   const int halves = two_set ? 2 : 1;
-  auto kern = two_set ? dfss_flash2_kernel<T, PAIRS, MASKED> : dfss_flash_kernel<T, 1, PAIRS, MASKED>;
+  auto kern = two_set ? dfss_flash2_kernel<T, PAIRS, MASKED, DUMP> : dfss_flash_kernel<T, 1, PAIRS, MASKED, DUMP>;
   const int smem_total = two_set ? S2_TOTAL + (MASKED ? flash_mask_smem_bytes(n) : 0) : SMEM_TOTAL;
   if (smem_total > 227 * 1024) return cudaErrorNotSupported;
   if (MASKED && two_set) prepare_mask_bits(tmask, n, workspace, s);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_total);
+  const int dev = current_device();
+  static std::atomic<uint64_t> attr1{0}, attr2{0};
+  cudaError_t e = set_max_smem_once((const void*)kern, two_set ? attr2 : attr1, dev);
   if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sms(dev);
   const int64_t items = bh * (n / (BM * halves));
   const int grid = (int)(items < sms ? items : sms);
-  // DFSS_FLASH_VARIANT (timing experiments only; results invalid when set):
-  // bit3 skip prune/exp arithmetic, bit4 skip PV MMAs, bit5 skip S MMAs
-  static const int variant = getenv("DFSS_FLASH_VARIANT") ? atoi(getenv("DFSS_FLASH_VARIANT")) : 0;
+#ifdef DFSS_FLASH_TRACE_BUILD
+  // bring-up timeline (tools/trace_flash.py): DFSS_FLASH_TRACE=<file> in trace builds only
   static const char* trace_file = getenv("DFSS_FLASH_TRACE");
   unsigned long long* trace = nullptr;
   const size_t trace_n = 16 * 2 * 64 * 2;
@@ -1057,7 +1046,9 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
     cudaMemset(trace, 0, trace_n * 8);
     cudaMemcpyToSymbol(g_flash_trace, &trace, sizeof(trace));
   }
-  kern<<<grid, NUM_THREADS, smem_total, s>>>(tq, tk, tv, (T*)out, scale, (int)bh, n, 2u, variant, tmask);
+#endif
+  kern<<<grid, NUM_THREADS, smem_total, s>>>(tq, tk, tv, (T*)out, scale, (int)bh, n, 2u, dump, tmask);
+#ifdef DFSS_FLASH_TRACE_BUILD
   if (trace) {
     cudaStreamSynchronize(s);
     unsigned long long* host = (unsigned long long*)malloc(trace_n * 8);
@@ -1072,16 +1063,20 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
     cudaMemcpyToSymbol(g_flash_trace, &null, sizeof(null));
     cudaFree(trace);
   }
+#endif
   return cudaGetLastError();
 }
 
+#ifndef DFSS_FLASH_DUMP_TU
 bool tc_flash_mask_supported(int tile_rows, int tile_cols) {
   return tile_rows > 0 && tile_cols > 0 && tile_rows % 32 == 0 && tile_cols % 32 == 0;
 }
+#endif
 
-cudaError_t launch_flash_tc(const void* q, const void* k, const void* v, void* out, float scale, int gs, int dtype,
-                            int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows, int tile_cols,
-                            void* workspace, cudaStream_t s) {
+template <bool DUMP>
+static cudaError_t launch_flash_tc_impl(const void* q, const void* k, const void* v, void* out, float scale, int gs,
+                                        int dtype, int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows,
+                                        int tile_cols, void* workspace, FlashDump dump, cudaStream_t s) {
   if (!tc_flash_supported(gs, dtype, n, d)) return cudaErrorNotSupported;
   if (tile_keep && !tc_flash_mask_supported(tile_rows, tile_cols)) return cudaErrorNotSupported;
   if (tile_keep && !workspace) return cudaErrorInvalidValue;  // flash_mask_workspace_bytes(n)
@@ -1089,18 +1084,34 @@ cudaError_t launch_flash_tc(const void* q, const void* k, const void* v, void* o
   TileMask m{tile_keep, tile_keep ? tile_rows : 1, tile_keep ? tile_cols : 1,
              tile_keep ? (n + tile_cols - 1) / tile_cols : 1};
   const bool bf = dtype == DFSS_BF16, masked = tile_keep != nullptr;
+#define DFSS_FLASH_CALL(T, P, M) flash_launch_typed<T, P, M, DUMP>(q, k, v, out, scale, bh, n, m, workspace, dump, s)
   if (gs == 2) {
-    if (masked)
-      return bf ? flash_launch_typed<__nv_bfloat16, true, true>(q, k, v, out, scale, bh, n, m, workspace, s)
-                : flash_launch_typed<__half, true, true>(q, k, v, out, scale, bh, n, m, workspace, s);
-    return bf ? flash_launch_typed<__nv_bfloat16, true, false>(q, k, v, out, scale, bh, n, m, workspace, s)
-              : flash_launch_typed<__half, true, false>(q, k, v, out, scale, bh, n, m, workspace, s);
+    if (masked) return bf ? DFSS_FLASH_CALL(__nv_bfloat16, true, true) : DFSS_FLASH_CALL(__half, true, true);
+    return bf ? DFSS_FLASH_CALL(__nv_bfloat16, true, false) : DFSS_FLASH_CALL(__half, true, false);
   }
-  if (masked)
-    return bf ? flash_launch_typed<__nv_bfloat16, false, true>(q, k, v, out, scale, bh, n, m, workspace, s)
-              : flash_launch_typed<__half, false, true>(q, k, v, out, scale, bh, n, m, workspace, s);
-  return bf ? flash_launch_typed<__nv_bfloat16, false, false>(q, k, v, out, scale, bh, n, m, workspace, s)
-            : flash_launch_typed<__half, false, false>(q, k, v, out, scale, bh, n, m, workspace, s);
+  if (masked) return bf ? DFSS_FLASH_CALL(__nv_bfloat16, false, true) : DFSS_FLASH_CALL(__half, false, true);
+  return bf ? DFSS_FLASH_CALL(__nv_bfloat16, false, false) : DFSS_FLASH_CALL(__half, false, false);
+#undef DFSS_FLASH_CALL
 }
+
+#ifndef DFSS_FLASH_DUMP_TU
+cudaError_t launch_flash_tc(const void* q, const void* k, const void* v, void* out, float scale, int gs, int dtype,
+                            int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows, int tile_cols,
+                            void* workspace, cudaStream_t s) {
+  return launch_flash_tc_impl<false>(q, k, v, out, scale, gs, dtype, bh, n, d, tile_keep, tile_rows, tile_cols,
+                                     workspace, FlashDump{}, s);
+}
+#else
+cudaError_t launch_flash_tc_dump(const void* q, const void* k, const void* v, void* out, float scale, int gs,
+                                 int dtype, int64_t bh, int n, int d, const uint8_t* tile_keep, int tile_rows,
+                                 int tile_cols, void* workspace, float* dump_scores, uint32_t* dump_meta,
+                                 cudaStream_t s) {
+  FlashDump dump;
+  dump.s = dump_scores;
+  dump.meta = dump_meta;
+  return launch_flash_tc_impl<true>(q, k, v, out, scale, gs, dtype, bh, n, d, tile_keep, tile_rows, tile_cols,
+                                    workspace, dump, s);
+}
+#endif
 
 }  // namespace dfss

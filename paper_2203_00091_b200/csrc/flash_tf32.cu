@@ -109,11 +109,11 @@ __device__ __forceinline__ void mma_sp_tf32_ts_w(uint32_t d_tmem, uint32_t a_tme
       : "memory");
 }
 
-template <bool MASKED>
+template <bool MASKED, bool DUMP>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     dfss_flash_tf32_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                            const __grid_constant__ CUtensorMap tm_v, float* __restrict__ out, float scale, int bh,
-                           int n, TileMask tmask) {
+                           int n, FlashDump dump, TileMask tmask) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + F_BAR);
@@ -426,6 +426,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint32_t s[32];
             tc::tmem_ld_32x32b_x32(scol + 32 * ch, s);
             tc::tmem_ld_wait(s);
+            if constexpr (DUMP)
+              dump_chunk_scores(dump.s + ((int64_t)b * n + (ib * 2 + h) * BM + r) * n + t * BN + 64 * pr + 32 * ch, s,
+                                scale);
             prune12_chunk(s, c, mlog, p[ch], W[ch][0], W[ch][1], a0, a1);
             if (MV && cm[ch]) {  // masked chunk: structurally absent
 #pragma unroll
@@ -470,6 +473,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t word =
                 (lane & 8) ? ((partner >> 16) | (Wj & 0xFFFF0000u)) : ((Wj & 0xFFFFu) | (partner << 16));
             tc::tmem_st_32x32b_x1(scol + 32 * ch + 4 * j, word);
+            if constexpr (DUMP)  // 1:2 meta_hw: 8 pairs (16 columns) per word
+              dump.meta[(((int64_t)b * (n / BM) + ib * 2 + h) * (n / 16) + 2 * (4 * t + 2 * pr + ch) + j) * BM + r] =
+                  word;
           }
           tmem_st_x16(scol + 32 * ch + 16, p[ch]);
         }
@@ -498,17 +504,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
-// V [bh][n][64] -> V^T [bh][64][n] (fp32), 32 keys x 64 dims per block through shared memory
-__global__ void __launch_bounds__(256) transpose_v_kernel(const float* __restrict__ v, float* __restrict__ vt, int n) {
+// V [bh][n][64] -> V^T [bh][64][n] (fp32), 32 keys x 64 dims per block through shared memory;
+// blockIdx.y strides over bh (gridDim.y is capped at 65535)
+__global__ void __launch_bounds__(256) transpose_v_kernel(const float* __restrict__ v, float* __restrict__ vt, int n,
+                                                          int64_t bh) {
   __shared__ float tile[32][HD + 1];
-  const int b = blockIdx.y, k0 = blockIdx.x * 32;
-  const float* src = v + ((int64_t)b * n + k0) * HD;
-  for (int i = threadIdx.x; i < 32 * HD; i += blockDim.x) tile[i / HD][i % HD] = src[i];
-  __syncthreads();
-  float* dst = vt + (int64_t)b * HD * n + k0;
-  for (int i = threadIdx.x; i < 32 * HD; i += blockDim.x) {
-    const int dim = i / 32, key = i % 32;
-    dst[(int64_t)dim * n + key] = tile[key][dim];
+  const int k0 = blockIdx.x * 32;
+  for (int64_t b = blockIdx.y; b < bh; b += gridDim.y) {
+    const float* src = v + ((int64_t)b * n + k0) * HD;
+    for (int i = threadIdx.x; i < 32 * HD; i += blockDim.x) tile[i / HD][i % HD] = src[i];
+    __syncthreads();
+    float* dst = vt + (int64_t)b * HD * n + k0;
+    for (int i = threadIdx.x; i < 32 * HD; i += blockDim.x) {
+      const int dim = i / 32, key = i % 32;
+      dst[(int64_t)dim * n + key] = tile[key][dim];
+    }
+    __syncthreads();
   }
 }
 
@@ -522,7 +533,7 @@ int64_t flash_tf32_workspace_bytes(int64_t bh, int n, bool masked) {
 
 cudaError_t launch_flash_tf32(const void* q, const void* k, const void* v, void* out, float scale, int64_t bh, int n,
                               int d, const uint8_t* tile_keep, int tile_rows, int tile_cols, void* vt_scratch,
-                              cudaStream_t s) {
+                              cudaStream_t s, float* dump_scores, uint32_t* dump_meta) {
   if (!tc_flash_tf32_supported(2, n, d)) return cudaErrorNotSupported;
   if (tile_keep && (!tc_flash_mask_supported(tile_rows, tile_cols) || !flash_mask_two_set_ok(n)))
     return cudaErrorNotSupported;
@@ -546,22 +557,29 @@ cudaError_t launch_flash_tf32(const void* q, const void* k, const void* v, void*
       !encode_tmap(&tk, dt, 5, (void*)k, kdims, kstr, kbox, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !encode_tmap(&tv, dt, 3, vt_scratch, vdims, vstr, vbox, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
-  transpose_v_kernel<<<dim3(n / 32, (unsigned)bh), 256, 0, s>>>((const float*)v, (float*)vt_scratch, n);
+  transpose_v_kernel<<<dim3(n / 32, (unsigned)(bh < 65535 ? bh : 65535)), 256, 0, s>>>((const float*)v, (float*)vt_scratch,
+                                                                                n, bh);
   TileMask m{tile_keep, tile_keep ? tile_rows : 1, tile_keep ? tile_cols : 1,
              tile_keep ? (n + tile_cols - 1) / tile_cols : 1};
   // workspace: V^T, then the block-mask bitmaps (flash_tf32_workspace_bytes)
   if (tile_keep) prepare_mask_bits(m, n, (char*)vt_scratch + vt_bytes(bh, n), s);
-  auto kern = tile_keep ? dfss_flash_tf32_kernel<true> : dfss_flash_tf32_kernel<false>;
+  const bool dumping = dump_scores != nullptr || dump_meta != nullptr;
+  if (dumping && (!dump_scores || !dump_meta)) return cudaErrorInvalidValue;
+  FlashDump dump;
+  dump.s = dump_scores;
+  dump.meta = dump_meta;
+  auto kern = tile_keep ? (dumping ? dfss_flash_tf32_kernel<true, true> : dfss_flash_tf32_kernel<true, false>)
+                        : (dumping ? dfss_flash_tf32_kernel<false, true> : dfss_flash_tf32_kernel<false, false>);
   const int smem_total = F_TOTAL + (tile_keep ? flash_mask_smem_bytes(n) : 0);
   if (smem_total > 227 * 1024) return cudaErrorNotSupported;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_total);
+  const int dev = current_device();
+  static std::atomic<uint64_t> attr[4];
+  cudaError_t e = set_max_smem_once((const void*)kern, attr[(tile_keep ? 2 : 0) + (dumping ? 1 : 0)], dev);
   if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = device_sms(dev);
   const int64_t items = bh * ((n + 2 * BM - 1) / (2 * BM));
   const int grid = (int)(items < sms ? items : sms);
-  kern<<<grid, NUM_THREADS, smem_total, s>>>(tq, tk, tv, (float*)out, scale, (int)bh, n, m);
+  kern<<<grid, NUM_THREADS, smem_total, s>>>(tq, tk, tv, (float*)out, scale, (int)bh, n, dump, m);
   return cudaGetLastError();
 }
 

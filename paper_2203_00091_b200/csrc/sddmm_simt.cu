@@ -149,13 +149,22 @@ static cudaError_t sddmm_simt_typed(const void* q, const void* k, void* nz, uint
                                     int64_t bh, int n, int m, int d, const uint8_t* keep, int tile_rows,
                                     int tile_cols, float* dbg, cudaStream_t s) {
   MetaGeom geo(n, m / gs);
-  dim3 grid((m + BN - 1) / BN, 2 * geo.rblocks, (unsigned)bh);
-  if (gs == 4)
-    sddmm_simt_kernel<TIn, TNz, 4><<<grid, 256, 0, s>>>((const TIn*)q, (const TIn*)k, (TNz*)nz, meta, scale, n, m, d,
-                                                        keep, tile_rows, tile_cols, dbg, geo, 2u);
-  else
-    sddmm_simt_kernel<TIn, TNz, 2><<<grid, 256, 0, s>>>((const TIn*)q, (const TIn*)k, (TNz*)nz, meta, scale, n, m, d,
-                                                        keep, tile_rows, tile_cols, dbg, geo, 2u);
+  // bh on gridDim.z (<= 65535): larger batches are launched in slices
+  for (int64_t b0 = 0; b0 < bh; b0 += 65535) {
+    const int64_t nb = bh - b0 < 65535 ? bh - b0 : 65535;
+    const TIn* qb = (const TIn*)q + b0 * n * d;
+    const TIn* kb = (const TIn*)k + b0 * m * d;
+    TNz* nzb = (TNz*)nz + b0 * n * (m / 2);
+    uint32_t* mb = meta + b0 * geo.words_per_bh();
+    float* db = dbg ? dbg + b0 * n * m : nullptr;
+    dim3 grid((m + BN - 1) / BN, 2 * geo.rblocks, (unsigned)nb);
+    if (gs == 4)
+      sddmm_simt_kernel<TIn, TNz, 4><<<grid, 256, 0, s>>>(qb, kb, nzb, mb, scale, n, m, d, keep, tile_rows, tile_cols,
+                                                          db, geo, 2u);
+    else
+      sddmm_simt_kernel<TIn, TNz, 2><<<grid, 256, 0, s>>>(qb, kb, nzb, mb, scale, n, m, d, keep, tile_rows, tile_cols,
+                                                          db, geo, 2u);
+  }
   return cudaGetLastError();
 }
 

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(256) spmm_simt_kernel(const TP* __restrict__ p
     for (int j0 = 0; j0 < nzc; j0 += 32) {
       const int j = j0 + lane;
       float pv = 0.f;
-      int col = 0;
+      int col = -1;  // -1: absent (masked tile) -- skipped, as the reference skips it (_kernels_numba.py:98)
       if (j < nzc) {
         const int g = (GS == 4) ? (j >> 1) : j;
         int shift;
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(256) spmm_simt_kernel(const TP* __restrict__ p
         col = (GS == 4) ? 4 * g + (int)((j & 1) ? ((nib >> 2) & 3u) : (nib & 3u)) : 2 * g + (nib == 0xEu ? 1 : 0);
         pv = DT<TP>::to_f(prow[j]);
         if (SM) pv = exp2f(fmaf(pv, kLog2e, -mlb));
-        if (keep && !keep[(int64_t)(r / tile_rows) * grid_cols + col / tile_cols]) pv = 0.f;
+        if (keep && !keep[(int64_t)(r / tile_rows) * grid_cols + col / tile_cols]) col = -1;
       }
       const int cnt = min(32, nzc - j0);
       // unrolled so the V-row loads of several nonzeros are in flight together (the loop was
@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(256) spmm_simt_kernel(const TP* __restrict__ p
       for (int l = 0; l < cnt; ++l) {
         const float pl = __shfl_sync(0xffffffffu, pv, l);
         const int cl = __shfl_sync(0xffffffffu, col, l);
+        if (cl < 0) continue;  // warp-uniform
         const TV* vr = vb + (int64_t)cl * d;
 #pragma unroll
         for (int t = 0; t < DPER; ++t) {
@@ -186,15 +187,18 @@ __global__ void __launch_bounds__(256) spmm_simt_softmax_d64_kernel(const float*
         col = (GS == 4) ? 4 * g + (int)((j & 1) ? ((nib >> 2) & 3u) : (nib & 3u)) : 2 * g + (nib == 0xEu ? 1 : 0);
         pv = exp2f(fmaf(prow[j], kLog2e, -mlb));
       }
+      const int cnt = nzc - (j0 + 16 * part);  // slots past the row end are skipped, not weighted 0
 #pragma unroll
       for (int l = 0; l < 16; ++l) {
         const float pl = __shfl_sync(0xffffffffu, pv, l, 16);
         const int cl = __shfl_sync(0xffffffffu, col, l, 16);
-        const float4 x = vb[(int64_t)cl * 16 + hl];
-        acc.x = fmaf(pl, x.x, acc.x);
-        acc.y = fmaf(pl, x.y, acc.y);
-        acc.z = fmaf(pl, x.z, acc.z);
-        acc.w = fmaf(pl, x.w, acc.w);
+        if (l < cnt) {
+          const float4 x = vb[(int64_t)cl * 16 + hl];
+          acc.x = fmaf(pl, x.x, acc.x);
+          acc.y = fmaf(pl, x.y, acc.y);
+          acc.z = fmaf(pl, x.z, acc.z);
+          acc.w = fmaf(pl, x.w, acc.w);
+        }
       }
     }
     acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
@@ -311,15 +315,20 @@ cudaError_t launch_spmm_simt_softmax_f32(const void* p, const uint32_t* meta, co
   if (d > 64) return cudaErrorNotSupported;
   // tiled from n_k = 512 up (L2-bound warp kernel: n = 1024 1.79 -> 1.50 ms for 96 heads); the
   // warp-per-row kernel is faster on short rows (n = 384: 0.198 vs 0.233 ms, tools/time_f32_sweep.py)
-  if (d == 64 && n_k % 128 == 0 && n_k >= 512 && ((uintptr_t)v & 15) == 0 && ((uintptr_t)out & 15) == 0 &&
-      !getenv("DFSS_SPMM_WARP")) {
-    const dim3 grid((unsigned)((rows + 31) / 32), (unsigned)bh);
-    if (gs == 4)
-      spmm_softmax_f32_tiled_kernel<4><<<grid, 256, 0, s>>>((const float*)p, meta, (const float*)v, (float*)out,
-                                                            rows, n_k, MetaGeom(rows, n_k / 4));
-    else
-      spmm_softmax_f32_tiled_kernel<2><<<grid, 256, 0, s>>>((const float*)p, meta, (const float*)v, (float*)out,
-                                                            rows, n_k, MetaGeom(rows, n_k / 2));
+  if (d == 64 && n_k % 128 == 0 && n_k >= 512 && ((uintptr_t)v & 15) == 0 && ((uintptr_t)out & 15) == 0) {
+    const MetaGeom geo(rows, n_k / gs);
+    for (int64_t b0 = 0; b0 < bh; b0 += 65535) {  // bh on gridDim.y (<= 65535): slices
+      const int64_t nb = bh - b0 < 65535 ? bh - b0 : 65535;
+      const float* pb = (const float*)p + b0 * rows * (n_k / 2);
+      const uint32_t* mb = meta + b0 * geo.words_per_bh();
+      const float* vb = (const float*)v + b0 * n_k * 64;
+      float* ob = (float*)out + b0 * rows * 64;
+      const dim3 grid((unsigned)((rows + 31) / 32), (unsigned)nb);
+      if (gs == 4)
+        spmm_softmax_f32_tiled_kernel<4><<<grid, 256, 0, s>>>(pb, mb, vb, ob, rows, n_k, geo);
+      else
+        spmm_softmax_f32_tiled_kernel<2><<<grid, 256, 0, s>>>(pb, mb, vb, ob, rows, n_k, geo);
+    }
     return cudaGetLastError();
   }
   if (d == 64 && ((uintptr_t)v & 15) == 0 && ((uintptr_t)out & 15) == 0) {

@@ -3,6 +3,8 @@
 // ld / st, and the UMMA shared-memory + instruction descriptors.
 #pragma once
 
+#include <atomic>
+
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -341,5 +343,13 @@ bool encode_tmap_3d(CUtensorMap* map, CUtensorMapDataType dtype, int elem_bytes,
                     uint64_t d2, uint32_t box0, uint32_t box1, CUtensorMapSwizzle swz);
 bool encode_tmap(CUtensorMap* map, CUtensorMapDataType dtype, int rank, void* base, const uint64_t* dims,
                  const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swz);
+
+// Host: per-device attribute cache (tma_host.cu).
+int current_device();
+int device_sms(int dev);
+int device_cc(int dev);  // major * 10 + minor, 0 if unknown
+// cudaFuncAttributeMaxDynamicSharedMemorySize = 227 KB once per (kernel, device): `done` is a
+// per-kernel bitmask of devices already configured
+cudaError_t set_max_smem_once(const void* kernel, std::atomic<uint64_t>& done, int dev);
 
 }  // namespace dfss

@@ -1,9 +1,59 @@
 // tma_host.cu -- host-side TMA descriptor encoding via the runtime's driver entry point.
 #include <cudaTypedefs.h>
 
+#include <atomic>
+
 #include "tc_common.cuh"
 
 namespace dfss {
+
+// ---------------------------------------------------------------- per-device attribute cache
+// The C entry points run on microsecond configs (c1: ~30 us), so the per-call host work is
+// kept to a cudaGetDevice: SM count and compute capability are queried once per device.
+namespace {
+constexpr int kMaxDev = 64;
+std::atomic<int> g_sms[kMaxDev];   // 0 = not queried yet
+std::atomic<int> g_cc[kMaxDev];    // major * 10 + minor + 1 (0 = not queried)
+}  // namespace
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
+int device_sms(int dev) {
+  if (dev < 0 || dev >= kMaxDev) return 148;
+  int v = g_sms[dev].load(std::memory_order_relaxed);
+  if (!v) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    g_sms[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+int device_cc(int dev) {
+  if (dev < 0 || dev >= kMaxDev) return 0;
+  int v = g_cc[dev].load(std::memory_order_relaxed);
+  if (!v) {
+    int major = 0, minor = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
+      return 0;  // not cached: the caller reports "no device"
+    v = major * 10 + minor + 1;
+    g_cc[dev].store(v, std::memory_order_relaxed);
+  }
+  return v - 1;
+}
+
+cudaError_t set_max_smem_once(const void* kernel, std::atomic<uint64_t>& done, int dev) {
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  // the largest opt-in size once: the persistent kernels run one CTA per SM whatever they use
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;

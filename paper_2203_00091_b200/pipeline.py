@@ -7,6 +7,7 @@
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -89,6 +90,87 @@ def dfss_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode="2:4"
                                             block_mask.tile_rows, block_mask.tile_cols, _lib.ptr(workspace), need,
                                             _lib.stream_of(q)), "nm_attention")
     return out
+
+
+#: dfss_nm_attention_path ids (include/dfss.h)
+PATHS = {1: "fused-16bit", 2: "fused-tf32", 3: "staged-tcgen05", 4: "staged-ffma", 5: "staged-masked"}
+
+
+def attention_path(mode, dtype: torch.dtype, n: int, d: int, math_mode: str = "auto",
+                   block_mask: BlockMask | None = None) -> str:
+    """Name of the kernel path dfss_attention takes for these arguments (no launch)."""
+    mode = as_mode(mode)
+    tr, tc_ = (block_mask.tile_rows, block_mask.tile_cols) if block_mask is not None else (0, 0)
+    pid = int(_lib.load().dfss_nm_attention_path(mode.group_size, _lib.dtype_id(dtype), _MATH[math_mode], n, d, tr,
+                                                 tc_, int(block_mask is not None)))
+    if pid < 0:
+        _lib.check(pid, "attention path")
+    return PATHS[pid]
+
+
+@dataclass(frozen=True)
+class AttentionDump:
+    """Selection evidence of one dfss_attention call (dfss_nm_attention_dump).
+
+    scores: fp32 [..., n, n], the post-scale scores every prune compared (NaN where a fused kernel
+    skipped a fully masked 128 x 128 step); meta: uint8 [..., n, n / gs], the LOGICAL nibbles of the
+    call's mode decoded from the metadata words the kernel handed to tcgen05.mma.sp (0 where
+    nothing was selected: masked chunks, skipped steps); path: the kernel path that ran."""
+
+    out: torch.Tensor
+    scores: torch.Tensor
+    meta: torch.Tensor
+    path: str
+
+
+def dfss_attention_dump(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode="2:4", *, math_mode: str = "auto",
+                        block_mask: BlockMask | None = None) -> AttentionDump:
+    """dfss_attention plus the scores and metadata its prune produced (parity evidence only: it
+    writes an n x n fp32 tensor, which the product path never does).  Same kernels, same output."""
+    mode = as_mode(mode)
+    if q.shape != k.shape or q.shape != v.shape or q.dim() < 2:
+        raise ValueError(f"Q, K, V must share shape [..., n, d]; got {tuple(q.shape)}")
+    _lib.require_cuda(q, k, v)
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    n, d = q.shape[-2], q.shape[-1]
+    bh = int(np.prod(q.shape[:-2], dtype=np.int64)) if q.dim() > 2 else 1
+    lib = _lib.load()
+    out = torch.empty_like(q)
+    need = workspace_bytes(mode, q.dtype, bh, n, d, math_mode, block_mask)
+    ws = torch.empty(max(need, 1), dtype=torch.uint8, device=q.device)
+    scores = torch.full((bh, n, n), float("nan"), dtype=torch.float32, device=q.device)
+    words = max(int(lib.dfss_meta_hw_words(4, bh, n, n)), int(lib.dfss_meta_hw_words(2, bh, n, n)))
+    meta_hw = torch.zeros(words, dtype=torch.int32, device=q.device)
+    meta_mode = ctypes.c_int(0)
+    keep = None
+    tr = tc_ = 0
+    if block_mask is not None:
+        _check_block_mask(block_mask, n, mode)
+        keep = block_mask.device_keep(q.device)
+        tr, tc_ = block_mask.tile_rows, block_mask.tile_cols
+    with torch.cuda.device(q.device):
+        _lib.check(lib.dfss_nm_attention_dump(_lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(out), mode.group_size,
+                                              _lib.dtype_id(q.dtype), _MATH[math_mode], bh, n, d, _lib.ptr(keep), tr,
+                                              tc_, _lib.ptr(ws), need, _lib.ptr(scores), _lib.ptr(meta_hw),
+                                              ctypes.byref(meta_mode), _lib.stream_of(q)), "nm_attention_dump")
+        gs = meta_mode.value
+        logical = torch.empty((bh, n, n // gs), dtype=torch.uint8, device=q.device)
+        _lib.check(lib.dfss_meta_hw_to_logical(_lib.ptr(meta_hw), _lib.ptr(logical), gs, bh, n, n,
+                                               _lib.stream_of(q)), "meta decode")
+    if gs != mode.group_size:
+        # 1:2 run as the 2:4 pattern (one survivor per pair): nibble lo | hi << 2 with lo in {0, 1}
+        # (pair 0 keeps element lo) and hi in {2, 3}; 0x4 / 0 mark masked / skipped groups
+        lo, hi = (logical & 3).long(), (logical >> 2).long()
+        valid = (lo <= 1) & (hi >= 2)
+        absent = (logical == 0x4) | (logical == 0)
+        p0 = torch.where(lo == 0, 0x4, 0xE)
+        p1 = torch.where(hi == 2, 0x4, 0xE)
+        pairs = torch.stack((p0, p1), dim=-1)
+        pairs = torch.where(absent[..., None], 0, torch.where(valid[..., None], pairs, 0xFF))
+        logical = pairs.reshape(bh, n, n // 2).to(torch.uint8)
+    shape = tuple(q.shape[:-2])
+    return AttentionDump(out, scores.reshape(shape + (n, n)), logical.reshape(shape + (n, n // mode.group_size)),
+                         attention_path(mode, q.dtype, n, d, math_mode, block_mask))
 
 
 _HOST_STREAMS: dict[int, tuple[torch.cuda.Stream, torch.cuda.Stream, torch.cuda.Stream]] = {}

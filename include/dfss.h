@@ -198,6 +198,13 @@ int dfss_nm_attention_path(int mode, int dtype, int math, int n, int d, int tile
 int dfss_prune_scores(const float* scores, void* nonzeros, uint8_t* meta_logical, uint8_t* kept, int mode,
                       int nz_dtype, int64_t rows, int cols, void* stream);
 
+/* The same selection on float64 scores (the reference's own dtype): scores [rows, cols] f64 ->
+ * nonzeros f64 [rows, cols/2], meta_logical uint8 [rows, cols/gs], kept uint8 [rows, cols]
+ * (any output NULL to skip).  Used by the codec for float64 matrices (compress_logical /
+ * prune_dense on DenseMatrix data), so no value is rounded to fp32 before it is compared. */
+int dfss_prune_scores_f64(const double* scores, double* nonzeros, uint8_t* meta_logical, uint8_t* kept, int mode,
+                          int64_t rows, int cols, void* stream);
+
 /* meta_hw <-> LOGICAL nibble stream (one nibble per byte), [bh, rows, cols/gs]. */
 int dfss_meta_hw_to_logical(const uint32_t* meta_hw, uint8_t* meta_logical, int mode, int64_t bh, int rows,
                             int cols, void* stream);

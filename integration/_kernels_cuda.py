@@ -32,9 +32,7 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from paper_2203_00091_b200 import _lib
-
-_INT32_MAX = 2**31 - 1
+from paper_2203_00091_b200 import kernels_f64 as _k
 
 
 def _dev():
@@ -51,23 +49,13 @@ def _host(t: torch.Tensor) -> np.ndarray:
     return t.cpu().numpy()
 
 
-def _call(status: int, what: str) -> None:
-    _lib.check(status, what)
-
-
 def sddmm_compress(q, kmat, scale, group_size, tile_rows, tile_cols, keep):
     """Fused score -> prune -> compress (_kernels_numba.py:110-188)."""
-    n, d = q.shape
+    n = q.shape[0]
     m = kmat.shape[0]
     keep = np.asarray(keep, dtype=bool)
-    lib = _lib.load()
-    dq, dk = _to_dev(q, np.float64), _to_dev(kmat, np.float64)
-    dkeep = _to_dev(keep.astype(np.uint8), np.uint8)
-    nz = torch.empty((n, m // 2), dtype=torch.float64, device=dq.device)
-    meta = torch.empty((n, m // group_size), dtype=torch.uint8, device=dq.device)
-    _call(lib.dfss_kmod_sddmm_compress(_lib.ptr(dq), _lib.ptr(dk), float(scale), int(group_size), n, m, d,
-                                       int(tile_rows), int(tile_cols), _lib.ptr(dkeep), _lib.ptr(nz), _lib.ptr(meta),
-                                       _lib.stream_of(dq)), "sddmm_compress")
+    nz, meta = _k.sddmm_compress(_to_dev(q, np.float64), _to_dev(kmat, np.float64), scale, group_size, tile_rows,
+                                 tile_cols, keep)
     # structural counters (_kernels_numba.py:126-184): over the kept tiles, peak tile area,
     # nonzeros written (2 per 2:4 group, 1 per 1:2 group) and nibbles written
     peak = nnz = nib = 0
@@ -83,56 +71,24 @@ def sddmm_compress(q, kmat, scale, group_size, tile_rows, tile_cols, keep):
 
 def softmax_nonzeros(nz, present):
     """Per-row stable softmax over present nonzeros (_kernels_numba.py:66-87)."""
-    rows, cols = nz.shape
-    lib = _lib.load()
-    dnz = _to_dev(nz, np.float64)
-    dpr = _to_dev(np.asarray(present, dtype=bool).astype(np.uint8), np.uint8)
-    out = torch.empty_like(dnz)
-    _call(lib.dfss_kmod_softmax_nonzeros(_lib.ptr(dnz), _lib.ptr(dpr), _lib.ptr(out), rows, cols,
-                                         _lib.stream_of(dnz)), "softmax_nonzeros")
-    return _host(out)
+    return _host(_k.softmax_nonzeros(_to_dev(nz, np.float64), _to_dev(np.asarray(present, dtype=bool), np.bool_)))
 
 
 def spmm_gather(nz, cols, present, v):
     """out[i, :] += nz[i, c] * v[cols[i, c], :] over present c, ascending (_kernels_numba.py:91-106)."""
-    rows, nzc = nz.shape
-    v_rows, d = v.shape
-    lib = _lib.load()
-    dnz, dv = _to_dev(nz, np.float64), _to_dev(v, np.float64)
-    dcols = _to_dev(cols, np.int64)
-    dpr = _to_dev(np.asarray(present, dtype=bool).astype(np.uint8), np.uint8)
-    out = torch.empty((rows, d), dtype=torch.float64, device=dnz.device)
-    err = torch.full((1,), _INT32_MAX, dtype=torch.int32, device=dnz.device)
-    _call(lib.dfss_kmod_spmm_gather(_lib.ptr(dnz), _lib.ptr(dcols), _lib.ptr(dpr), _lib.ptr(dv), _lib.ptr(out), rows,
-                                    nzc, v_rows, d, _lib.ptr(err), _lib.stream_of(dnz)), "spmm_gather")
-    bad = int(err.item())
-    if bad != _INT32_MAX:
-        raise IndexError(f"spmm_gather: column index out of range [0, {v_rows}) in row {bad}")
-    return _host(out)
+    return _host(_k.spmm_gather(_to_dev(nz, np.float64), _to_dev(cols, np.int64),
+                                _to_dev(np.asarray(present, dtype=bool), np.bool_), _to_dev(v, np.float64)))
 
 
 def gemm_abt(a, b, scale, tile_rows, tile_cols, k_panel):
     """out = scale * a @ b.T with one ascending accumulator per element (_kernels_numba.py:16-39);
     the tiling arguments only reorder the reference's traversal and do not change the result."""
-    n, kdim = a.shape
-    m = b.shape[0]
-    lib = _lib.load()
-    da, db = _to_dev(a, np.float64), _to_dev(b, np.float64)
-    out = torch.empty((n, m), dtype=torch.float64, device=da.device)
-    _call(lib.dfss_kmod_gemm_abt(_lib.ptr(da), _lib.ptr(db), float(scale), n, m, kdim, _lib.ptr(out),
-                                 _lib.stream_of(da)), "gemm_abt")
-    return _host(out)
+    return _host(_k.gemm_abt(_to_dev(a, np.float64), _to_dev(b, np.float64), scale))
 
 
 def row_softmax_dense(x):
     """Row-wise stable softmax of a dense matrix (_kernels_numba.py:43-62)."""
-    rows, cols = x.shape
-    lib = _lib.load()
-    dx = _to_dev(x, np.float64)
-    out = torch.empty_like(dx)
-    _call(lib.dfss_kmod_row_softmax_dense(_lib.ptr(dx), _lib.ptr(out), rows, cols, _lib.stream_of(dx)),
-          "row_softmax_dense")
-    return _host(out)
+    return _host(_k.row_softmax_dense(_to_dev(x, np.float64)))
 
 
 __all__ = ["sddmm_compress", "softmax_nonzeros", "spmm_gather", "gemm_abt", "row_softmax_dense"]

@@ -46,6 +46,7 @@ SIGNATURES = {
                                       _i64, _vp, _vp, _vp, _vp]),
     "dfss_nm_attention_path": (_i32, [_i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32]),
     "dfss_prune_scores": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i64, _i32, _vp]),
+    "dfss_prune_scores_f64": (_i32, [_vp, _vp, _vp, _vp, _i32, _i64, _i32, _vp]),
     "dfss_meta_hw_to_logical": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp]),
     "dfss_meta_logical_to_hw": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp]),
     "dfss_kmod_sddmm_compress": (_i32, [_vp, _vp, ctypes.c_double, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp,

@@ -102,13 +102,16 @@ class GroupSelection(NamedTuple):
 def select_group(values, mode: SparsityMode, device=None) -> GroupSelection:
     """codec.py:104-123, evaluated by the device selection routine itself."""
     mode = as_mode(mode)
-    vals = torch.as_tensor(values, dtype=torch.float32).reshape(-1)
+    # the reference compares in float64 (codec.py:111); a 16/32-bit tensor is compared as fp32 by
+    # the epilogue's own routine (select24 / select12), anything else in float64
+    vals = values if isinstance(values, torch.Tensor) else torch.from_numpy(np.asarray(values, dtype=np.float64))
+    vals = vals.to(torch.float64 if vals.dtype == torch.float64 else torch.float32).reshape(-1)
     if vals.shape != (mode.group_size,):
         raise ValueError(
             f"expected a group of {mode.group_size} values for mode {mode.value}, got shape {tuple(vals.shape)}"
         )
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    _, meta, _ = _prune(vals.to(dev).reshape(1, -1), mode, torch.float32, want_kept=False)
+    _, meta, _ = _prune(vals.to(dev).reshape(1, -1), mode, vals.dtype, want_kept=False)
     nib = int(meta.item())
     lo, hi = slots_for_nibble(nib)
     return GroupSelection(kept_elements(nib, mode), (lo, hi), nib)
@@ -269,8 +272,9 @@ class CompressedSparse:
         out = torch.empty(self.batch_shape + (self.rows * self.nibbles_per_row,), dtype=torch.uint8,
                           device=self.device)
         lib = _lib.load()
-        _lib.check(lib.dfss_meta_hw_to_logical(_lib.ptr(self.meta_hw), _lib.ptr(out), self.mode.group_size, self.bh,
-                                               self.rows, self.dense_cols, _lib.stream_of(out)), "meta decode")
+        with torch.cuda.device(self.device):
+            _lib.check(lib.dfss_meta_hw_to_logical(_lib.ptr(self.meta_hw), _lib.ptr(out), self.mode.group_size, self.bh,
+                                                   self.rows, self.dense_cols, _lib.stream_of(out)), "meta decode")
         if self.block_mask is not None:
             present = self.block_mask.dense_keep(self.rows, self.dense_cols)[:, :: self.mode.group_size]
             out.view(self.batch_shape + (self.rows, self.nibbles_per_row)).mul_(
@@ -317,8 +321,9 @@ class CompressedSparse:
         hw = torch.empty(batch + (words,), dtype=torch.int32, device=nonzeros.device)
         bh = int(np.prod(batch, dtype=np.int64)) if batch else 1
         lib = _lib.load()
-        _lib.check(lib.dfss_meta_logical_to_hw(_lib.ptr(meta.contiguous()), _lib.ptr(hw), mode.group_size, bh, rows,
-                                               dense_cols, _lib.stream_of(hw)), "meta encode")
+        with torch.cuda.device(hw.device):
+            _lib.check(lib.dfss_meta_logical_to_hw(_lib.ptr(meta.contiguous()), _lib.ptr(hw), mode.group_size, bh, rows,
+                                                   dense_cols, _lib.stream_of(hw)), "meta encode")
         return cls(rows, dense_cols, mode, nonzeros.contiguous(), hw, block_mask=block_mask)
 
 
@@ -327,8 +332,17 @@ class CompressedSparse:
 
 
 def _prune(scores: torch.Tensor, mode: SparsityMode, nz_dtype: torch.dtype, want_kept: bool = True):
-    """Run dfss_prune_scores: (nonzeros, logical meta [rows, groups], kept uint8 [rows, cols])."""
+    """Run dfss_prune_scores: (nonzeros, logical meta [rows, groups], kept uint8 [rows, cols]).
+    float64 scores are compared in float64 (dfss_prune_scores_f64), never rounded first."""
     _lib.require_cuda(scores)
+    if scores.dtype == torch.float64:
+        from . import kernels_f64
+
+        if scores.shape[-1] % mode.group_size:
+            raise ValueError(f"column count {scores.shape[-1]} not divisible by group size {mode.group_size} "
+                             f"(mode {mode.value})")
+        nz, meta, kept = kernels_f64.prune_scores(scores, mode.group_size, want_kept)
+        return (nz if nz_dtype == torch.float64 else nz.to(nz_dtype)), meta, kept
     s = scores.contiguous().to(torch.float32)
     cols = s.shape[-1]
     rows = s.numel() // cols if cols else 0
@@ -339,8 +353,9 @@ def _prune(scores: torch.Tensor, mode: SparsityMode, nz_dtype: torch.dtype, want
     meta = torch.empty(s.shape[:-1] + (cols // gs,), dtype=torch.uint8, device=s.device)
     kept = torch.empty(s.shape, dtype=torch.uint8, device=s.device) if want_kept else None
     lib = _lib.load()
-    _lib.check(lib.dfss_prune_scores(_lib.ptr(s), _lib.ptr(nz), _lib.ptr(meta), _lib.ptr(kept), gs,
-                                     _lib.dtype_id(nz_dtype), rows, cols, _lib.stream_of(s)), "prune_scores")
+    with torch.cuda.device(s.device):
+        _lib.check(lib.dfss_prune_scores(_lib.ptr(s), _lib.ptr(nz), _lib.ptr(meta), _lib.ptr(kept), gs,
+                                         _lib.dtype_id(nz_dtype), rows, cols, _lib.stream_of(s)), "prune_scores")
     return nz, meta, kept
 
 

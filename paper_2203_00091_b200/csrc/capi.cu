@@ -323,6 +323,15 @@ int dfss_kmod_gemm_abt(const double* a, const double* b, double scale, int64_t n
   return cuda_status(dfss::launch_kmod_gemm_abt(a, b, scale, n, m, kdim, out, (cudaStream_t)stream));
 }
 
+int dfss_prune_scores_f64(const double* scores, double* nonzeros, uint8_t* meta_logical, uint8_t* kept, int mode,
+                          int64_t rows, int cols, void* stream) {
+  if (!valid_mode(mode)) return fail(DFSS_ERR_INVALID, "unknown sparsity mode (expected 2 or 4)");
+  if (rows < 0 || cols < 0 || cols % mode) return fail(DFSS_ERR_INVALID, "column count not divisible by group size");
+  if (rows && cols && !scores) return fail(DFSS_ERR_INVALID, "null tensor pointer");
+  return cuda_status(dfss::launch_kmod_prune(scores, rows, cols, mode, nonzeros, meta_logical, kept,
+                                             (cudaStream_t)stream));
+}
+
 int dfss_kmod_row_softmax_dense(const double* x, double* out, int64_t rows, int cols, void* stream) {
   if (rows < 0 || cols < 0) return fail(DFSS_ERR_INVALID, "shape dimensions must be non-negative");
   if (rows && cols && (!x || !out)) return fail(DFSS_ERR_INVALID, "null tensor pointer");

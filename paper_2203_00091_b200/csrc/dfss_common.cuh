@@ -233,6 +233,8 @@ cudaError_t launch_flash_tc_dump(const void* q, const void* k, const void* v, vo
 cudaError_t launch_kmod_sddmm_compress(const double* q, const double* k, double scale, int gs, int n, int m, int d,
                                        int tile_rows, int tile_cols, const uint8_t* keep, double* nonzeros,
                                        uint8_t* meta, cudaStream_t s);
+cudaError_t launch_kmod_prune(const double* scores, int64_t rows, int cols, int gs, double* nonzeros, uint8_t* meta,
+                              uint8_t* kept, cudaStream_t s);
 cudaError_t launch_kmod_softmax(const double* x, const uint8_t* present, double* out, int64_t rows, int cols,
                                 bool dense, cudaStream_t s);
 cudaError_t launch_kmod_spmm_gather(const double* nz, const int64_t* cols, const uint8_t* present, const double* v,

@@ -63,6 +63,51 @@ __global__ void __launch_bounds__(256) kmod_sddmm_compress_kernel(const double* 
   }
 }
 
+// selection on given float64 scores (codec.py:289-313 -- the same rule as the fused epilogue
+// above): one thread per (row, group); any output may be null
+template <int GS>
+__global__ void __launch_bounds__(256) kmod_prune_kernel(const double* __restrict__ scores, int64_t rows, int cols,
+                                                         double* __restrict__ nonzeros, uint8_t* __restrict__ meta,
+                                                         uint8_t* __restrict__ kept) {
+  const int groups = cols / GS;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= rows * groups) return;
+  const int64_t row = idx / groups;
+  const int g = (int)(idx % groups);
+  const double* v = scores + row * cols + (int64_t)g * GS;
+  int lo, hi;
+  if (GS == 2) {
+    lo = hi = v[1] > v[0] ? 1 : 0;
+  } else {
+    int best = 0;
+    for (int t = 1; t < 4; ++t)
+      if (v[t] > v[best]) best = t;
+    int second = -1;
+    for (int t = 0; t < 4; ++t) {
+      if (t == best) continue;
+      if (second < 0 || v[t] > v[second]) second = t;
+    }
+    lo = best < second ? best : second;
+    hi = best < second ? second : best;
+  }
+  if (GS == 2) {
+    if (nonzeros) nonzeros[row * (cols / 2) + g] = v[lo];
+    if (meta) meta[row * groups + g] = lo ? 0xE : 0x4;
+    if (kept) {
+      kept[row * cols + 2 * g] = lo == 0;
+      kept[row * cols + 2 * g + 1] = lo == 1;
+    }
+  } else {
+    if (nonzeros) {
+      nonzeros[row * (cols / 2) + 2 * g] = v[lo];
+      nonzeros[row * (cols / 2) + 2 * g + 1] = v[hi];
+    }
+    if (meta) meta[row * groups + g] = (uint8_t)(lo | (hi << 2));
+    if (kept)
+      for (int t = 0; t < 4; ++t) kept[row * cols + 4 * g + t] = (t == lo || t == hi);
+  }
+}
+
 // softmax_nonzeros (_kernels_numba.py:66-84) and row_softmax_dense (:43-59): one warp per row.
 // The maximum is order independent (computed by the warp); the exponentials are independent
 // (computed by the warp); the sum is sequential in column order (lane 0), as the reference's
@@ -170,6 +215,18 @@ cudaError_t launch_kmod_sddmm_compress(const double* q, const double* k, double 
   else
     kmod_sddmm_compress_kernel<4><<<blocks, 256, 0, s>>>(q, k, scale, n, m, d, tile_rows, tile_cols, keep, grid_cols,
                                                          nonzeros, meta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_kmod_prune(const double* scores, int64_t rows, int cols, int gs, double* nonzeros, uint8_t* meta,
+                              uint8_t* kept, cudaStream_t s) {
+  const int64_t threads = rows * (cols / gs);
+  if (threads == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((threads + 255) / 256);
+  if (gs == 2)
+    kmod_prune_kernel<2><<<blocks, 256, 0, s>>>(scores, rows, cols, nonzeros, meta, kept);
+  else
+    kmod_prune_kernel<4><<<blocks, 256, 0, s>>>(scores, rows, cols, nonzeros, meta, kept);
   return cudaGetLastError();
 }
 

@@ -101,6 +101,19 @@ def sddmm_prune(
     _lib.require_cuda(qt, kt)
     if qt.dtype != kt.dtype:
         raise ValueError(f"Q and K dtypes differ ({qt.dtype} vs {kt.dtype})")
+    if qt.dtype == torch.float64:
+        # the reference's own dtype: its arithmetic on the device (kernels_f64, bitwise the numba
+        # sddmm_compress), not a rounded fp32 approximation
+        if math_mode == "tf32" or scores_out is not None or with_row_max:
+            raise ValueError("float64 inputs run the reference arithmetic: no tf32, scores_out or row maxima")
+        from . import kernels_f64
+
+        nz, meta = kernels_f64.batched(
+            lambda a, b: kernels_f64.sddmm_compress(a, b, scale, gs, tile_rows, tile_cols, keep), qt, kt)
+        if nz_dtype is not None and nz_dtype != torch.float64:
+            nz = nz.to(nz_dtype)
+        compressed = CompressedSparse.from_logical(n, m, mode, nz, meta, block_mask=block_mask)
+        return compressed, _stats(n, m, gs, tile_rows, tile_cols, keep)
     qt, kt = qt.contiguous(), kt.contiguous()
     batch = tuple(qt.shape[:-2])
     bh = int(np.prod(batch, dtype=np.int64)) if batch else 1
@@ -113,13 +126,14 @@ def sddmm_prune(
     dev_keep = block_mask.device_keep(qt.device) if block_mask is not None else None
     row_max = torch.empty(batch + (n, 4), dtype=torch.float32, device=qt.device) if with_row_max else None
     lib = _lib.load()
-    _lib.check(
-        lib.dfss_sddmm_prune(_lib.ptr(qt), _lib.ptr(kt), _lib.ptr(nz), _lib.ptr(meta), float(scale), gs,
-                             _lib.dtype_id(qt.dtype), _lib.dtype_id(nz_dtype), _MATH[math_mode], bh, n, m, d,
-                             _lib.ptr(dev_keep), tile_rows, tile_cols, _lib.ptr(scores_out), _lib.ptr(row_max),
-                             _lib.stream_of(qt)),
-        "sddmm_prune",
-    )
+    with torch.cuda.device(qt.device):
+        _lib.check(
+            lib.dfss_sddmm_prune(_lib.ptr(qt), _lib.ptr(kt), _lib.ptr(nz), _lib.ptr(meta), float(scale), gs,
+                                 _lib.dtype_id(qt.dtype), _lib.dtype_id(nz_dtype), _MATH[math_mode], bh, n, m, d,
+                                 _lib.ptr(dev_keep), tile_rows, tile_cols, _lib.ptr(scores_out), _lib.ptr(row_max),
+                                 _lib.stream_of(qt)),
+            "sddmm_prune",
+        )
     compressed = CompressedSparse(n, m, mode, nz, meta, block_mask=block_mask, row_max=row_max)
     return compressed, _stats(n, m, gs, tile_rows, tile_cols, keep)
 

@@ -70,6 +70,12 @@ def dfss_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode="2:4"
     _lib.require_cuda(q, k, v)
     if not (q.dtype == k.dtype == v.dtype):
         raise ValueError("Q, K, V must share a dtype")
+    if q.dtype == torch.float64:
+        raise ValueError("dfss_attention computes in bf16/fp16/fp32: cast float64 explicitly, or use nm_attention "
+                         "(reference float64 arithmetic)")
+    if not (q.device == k.device == v.device) or (out is not None and out.device != q.device) or (
+            workspace is not None and workspace.device != q.device):
+        raise ValueError("Q, K, V, out and workspace must be on one CUDA device")
     q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
     bh = int(np.prod(q.shape[:-2], dtype=np.int64)) if q.dim() > 2 else 1
     if out is None:
@@ -78,17 +84,18 @@ def dfss_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode="2:4"
     if need and (workspace is None or workspace.numel() < need):
         workspace = torch.empty(need, dtype=torch.uint8, device=q.device)
     lib = _lib.load()
-    if block_mask is None:
-        _lib.check(lib.dfss_nm_attention(_lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(out), mode.group_size,
-                                         _lib.dtype_id(q.dtype), _MATH[math_mode], bh, n, d, _lib.ptr(workspace),
-                                         need, _lib.stream_of(q)), "nm_attention")
-        return out
-    _check_block_mask(block_mask, n, mode)
-    keep = block_mask.device_keep(q.device)
-    _lib.check(lib.dfss_nm_attention_masked(_lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(out), mode.group_size,
-                                            _lib.dtype_id(q.dtype), _MATH[math_mode], bh, n, d, _lib.ptr(keep),
-                                            block_mask.tile_rows, block_mask.tile_cols, _lib.ptr(workspace), need,
-                                            _lib.stream_of(q)), "nm_attention")
+    with torch.cuda.device(q.device):  # the C ABI launches on the current device
+        if block_mask is None:
+            _lib.check(lib.dfss_nm_attention(_lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(out), mode.group_size,
+                                             _lib.dtype_id(q.dtype), _MATH[math_mode], bh, n, d, _lib.ptr(workspace),
+                                             need, _lib.stream_of(q)), "nm_attention")
+            return out
+        _check_block_mask(block_mask, n, mode)
+        keep = block_mask.device_keep(q.device)
+        _lib.check(lib.dfss_nm_attention_masked(_lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.ptr(out), mode.group_size,
+                                                _lib.dtype_id(q.dtype), _MATH[math_mode], bh, n, d, _lib.ptr(keep),
+                                                block_mask.tile_rows, block_mask.tile_cols, _lib.ptr(workspace), need,
+                                                _lib.stream_of(q)), "nm_attention")
     return out
 
 
@@ -178,7 +185,7 @@ _HOST_STREAMS: dict[int, tuple[torch.cuda.Stream, torch.cuda.Stream, torch.cuda.
 
 def dfss_attention_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode="2:4", *, math_mode: str = "auto",
                         block_mask: BlockMask | None = None, out: torch.Tensor | None = None, chunks: int = 4,
-                        device: torch.device | int | None = None) -> torch.Tensor:
+                        device: torch.device | int | None = None, non_blocking: bool = False) -> torch.Tensor:
     """dfss_attention for HOST tensors [..., n, d] (the reference's own calling convention: its
     kernels take host arrays): returns a host tensor.  The flattened batch x heads is cut into
     `chunks` pieces; the host->device copy of piece i+1, the fused kernel on piece i and the
@@ -186,7 +193,12 @@ def dfss_attention_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode=
     two device buffers per direction.  Pinned inputs / output make the copies asynchronous
     (unpinned ones are staged by the driver, still correct).  Ordered after prior work on the
     current stream, and the current stream waits for the last copy, so events recorded around
-    the call time the whole transfer + compute."""
+    the call time the whole transfer + compute.
+
+    By default the call is synchronous like the reference's (its kernels return host arrays): it
+    returns once `out` holds the result.  ``non_blocking=True`` returns right after enqueueing;
+    then `out` must not be read, nor q / k / v modified, before the current stream is
+    synchronised (bench.py times the pipelined copies this way, with events on that stream)."""
     if q.is_cuda or k.is_cuda or v.is_cuda:
         raise ValueError("dfss_attention_host takes host tensors; use dfss_attention for device tensors")
     if q.shape != k.shape or q.shape != v.shape or q.dim() < 2:
@@ -239,6 +251,8 @@ def dfss_attention_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode=
             drained.append(torch.cuda.Event())
             drained[i].record(s_out)
     cur.wait_event(drained[-1])
+    if not non_blocking:
+        drained[-1].synchronize()
     # the device buffers are released to the caching allocator; keep them alive until the copies
     # ran by recording their use on every stream that touched them
     for st in (s_in, s_run, s_out):
@@ -250,15 +264,30 @@ def dfss_attention_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode=
 
 
 def nm_attention(inputs: AttentionInputs, mode: SparsityMode, block_mask: BlockMask | None = None, *,
-                 tile_rows: int = 32, tile_cols: int = 64) -> DenseMatrix:
-    """Drop-in sparse attention: fused prune -> sparse softmax -> SpMM (pipeline.py:15-32)."""
+                 tile_rows: int = 32, tile_cols: int = 64, precision: str = "auto") -> DenseMatrix:
+    """Drop-in sparse attention: fused prune -> sparse softmax -> SpMM (pipeline.py:15-32).
+
+    16/32-bit inputs run dfss_attention (one fused kernel for 16-bit; exact FP32 FFMA for fp32).
+    float64 inputs -- the reference's dtype -- run the reference's arithmetic on the device by
+    default (``precision="auto"``: attention_sddmm -> softmax_rows -> spmm over kernels_f64, the
+    reference's numbers up to exp rounding); ``precision="fp32"`` narrows them explicitly to the
+    exact-FP32 kernels (tolerance 1e-5) and returns float64."""
     mode = as_mode(mode)
+    if precision not in ("auto", "fp32"):
+        raise ValueError(f"unknown precision {precision!r}; pick 'auto' or 'fp32'")
     if block_mask is not None and (block_mask.tile_rows, block_mask.tile_cols) != (tile_rows, tile_cols):
         raise ValueError(
             f"block mask tiles {block_mask.tile_rows}x{block_mask.tile_cols} "
             f"do not match the fused tiling {tile_rows}x{tile_cols}"
         )
-    out = dfss_attention(inputs.q.data, inputs.k.data, inputs.v.data, mode, block_mask=block_mask)
+    q, k, v = inputs.q.data, inputs.k.data, inputs.v.data
+    if q.dtype == torch.float64 and precision == "auto":
+        compressed, _ = attention_sddmm(q, k, mode, block_mask, tile_rows=tile_rows, tile_cols=tile_cols)
+        return spmm(softmax_rows(compressed), v)
+    if q.dtype == torch.float64:
+        out = dfss_attention(q.float(), k.float(), v.float(), mode, block_mask=block_mask)
+        return DenseMatrix(out.double(), check_finite=False)
+    out = dfss_attention(q, k, v, mode, block_mask=block_mask)
     return DenseMatrix(out, check_finite=False)
 
 

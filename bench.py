@@ -2,16 +2,21 @@
 """DFSS attention benchmark on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl dfss|reference] [--config c2]
+                    [--scaling weak|strong]
 
-A step is one DFSS attention pass (fused SDDMM+prune -> compressed softmax ->
-mma.sp SpMM) over this rank's shard of the flattened batch x heads, synthetic
-N(0,1) Q/K/V resident in HBM.  Weak scaling: with N ranks the global batch is
-N x the config's batch and rank r owns the contiguous heads [r*B*H, (r+1)*B*H)
-(inputs seeded per (seed, global head), so shard r of an N-GPU run equals the
-corresponding slice of a 1-GPU run).  The compute phase has no collective; one
-NCCL all-gather of the output shards runs after the timed region as the
-end-to-end check.  One JSON line is printed by rank 0.  Numbers taken under a
-profiler are never reported.
+A step is one DFSS attention pass (dfss_attention: for 16-bit inputs ONE fused kernel --
+QK^T on tcgen05 -> 2:4 / 1:2 prune in registers -> exp -> tcgen05.mma.sp P.V) over this rank's
+shard of the flattened batch x heads, synthetic N(0,1) Q/K/V resident in HBM (L2 flushed
+between timed steps).  Sharding: batch x heads are independent units with no data exchange
+(SURVEY §8(e)).  --scaling weak (default): every rank owns the config's B*H heads, the job's
+global batch is N x B.  --scaling strong: the config's B*H heads are split over the N ranks,
+floor + remainder (c1: 12 heads on 8 ranks -> 2,2,2,2,1,1,1,1).  Inputs are seeded per
+(seed, global head), so a rank's shard equals the same slice of a 1-GPU run.  The compute phase
+has no collective; one NCCL all-gather of the output shards after the timed region is the
+end-to-end check.  Rank 0 prints ONE JSON line; numbers taken under a profiler are never
+reported.  --impl reference times the reference's CPU algorithm (oracle/dfss_oracle.c, the C
+restatement of nmattn.nm_attention, bitwise equal to the numba reference on the golden
+fixtures) on the host cores, on the same config keys.
 """
 
 from __future__ import annotations
@@ -50,24 +55,26 @@ for _n in (384, 512, 768, 1024, 2048, 4096):
                                   desc=f"sweep 2:4 bf16, batch 8, 12 heads, seq {_n}")
     CONFIGS[f"c5_12_{_n}"] = dict(batch=8, heads=12, seq=_n, d=64, mode="1:2", dtype="bfloat16",
                                   desc=f"sweep 1:2 bf16, batch 8, 12 heads, seq {_n}")
-    if _n % 128 == 0:
-        CONFIGS[f"c5_12tf32_{_n}"] = dict(batch=8, heads=12, seq=_n, d=64, mode="1:2", dtype="float32", math="tf32",
-                                          desc=f"sweep 1:2 tf32 (fp32 inputs), batch 8, 12 heads, seq {_n}")
+    CONFIGS[f"c5_12tf32_{_n}"] = dict(batch=8, heads=12, seq=_n, d=64, mode="1:2", dtype="float32", math="tf32",
+                                      desc=f"sweep 1:2 tf32 (fp32 inputs), batch 8, 12 heads, seq {_n}")
     if _n <= 1024:
         CONFIGS[f"c5_12f32_{_n}"] = dict(batch=8, heads=12, seq=_n, d=64, mode="1:2", dtype="float32",
                                          desc=f"sweep 1:2 fp32 (exact FFMA), batch 8, 12 heads, seq {_n}")
 DT = {"float32": torch.float32, "bfloat16": torch.bfloat16, "float16": torch.float16}
+DTYPE_TAG = {"float32": "f32", "bfloat16": "bf16", "float16": "f16"}
 METRIC = "DFSS attention ms & speedup vs dense attention (seq 512–4096) on B200; TFLOPS"
 UNIT = "TFLOP/s (dense-equivalent 4*n^2*d per head)"
 L2_FLUSH_BYTES = 256 << 20
+#: nominal B200 FP32 FFMA peak (148 SMs x 128 FMA/clk x 2 x 1.965 GHz): not in MEASURED_PEAKS.json
+FP32_FFMA_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
 
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
-    return 6650.0, 1590.0, "fallback"
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), float(d.get("sm_max_mhz", 1965.0)), "measured"
+    return 6650.0, 1590.0, 1965.0, "fallback (B200_PROFILING.md)"
 
 
 def dist_env():
@@ -78,10 +85,17 @@ def dist_env():
 
 
 def shard(total: int, ws: int, rank: int):
-    per = -(-total // ws)
-    lo = min(total, rank * per)
-    hi = min(total, lo + per)
-    return lo, hi
+    """Contiguous floor + remainder split of `total` units over `ws` ranks: the first
+    total % ws ranks own one extra unit (12 over 8 -> 2,2,2,2,1,1,1,1)."""
+    base, rem = divmod(total, ws)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def job_heads(cfg, ws: int, scaling: str) -> int:
+    """Global batch x heads of the job: weak scaling multiplies the config by the rank count."""
+    per = cfg["batch"] * cfg["heads"]
+    return per * ws if scaling == "weak" else per
 
 
 def make_inputs(cfg, lo, hi, device, seed=0):
@@ -93,6 +107,17 @@ def make_inputs(cfg, lo, hi, device, seed=0):
         g = torch.Generator().manual_seed(seed * 1_000_003 + h)
         qkv[:, i] = torch.randn((3, n, d), generator=g, dtype=torch.float32).to(dt)
     return qkv.to(device)
+
+
+def config_block(cfg_name: str, ws: int, scaling: str, heads_per_rank) -> dict:
+    """The `config` object of both arms (key-identical, so the driver can pair them)."""
+    cfg = CONFIGS[cfg_name]
+    total = job_heads(cfg, ws, scaling)
+    return {"workload": f"{cfg_name}: {cfg['desc']}", "batch": cfg["batch"], "heads": cfg["heads"],
+            "seq_len": cfg["seq"], "head_dim": cfg["d"], "mode": cfg["mode"],
+            "math": cfg.get("math", "auto"), "global_batch": total // cfg["heads"], "global_heads": total,
+            "parallelism": f"bh-shard{ws}", "scaling": scaling, "heads_per_rank": heads_per_rank,
+            "l2": "flushed between timed steps (256 MiB write, outside the step events)"}
 
 
 class ClockSampler:
@@ -156,45 +181,94 @@ def time_steps(fn, steps, warmup, flush=None):
     return [s.elapsed_time(e) for s, e in ev]
 
 
-def algorithmic_bytes(cfg, fused=False):
-    """per (batch, head) per kernel.  16-bit staged: SDDMM 1.125n^2+4nd,
-    softmax 2n^2, SpMM 1.125n^2+4nd (total 4.25n^2+8nd).  Fused (softmax folded into the
-    SpMM): SDDMM 1.125n^2+4nd+16n (row maxima), SpMM 1.125n^2+4nd+16n (total 2.25n^2+8nd+32n)."""
+def kernel_stats(cfg_name: str, key: str) -> dict:
+    p = os.path.join(ROOT, "profiles", "ncu_kernel_stats.json")
+    try:
+        return json.load(open(p)).get(cfg_name, {}).get(key, {}) or {}
+    except (OSError, ValueError):
+        return {}
+
+
+#: kernels one dfss_attention call launches on each path (dfss_nm_attention, capi.cu)
+LAUNCHES = {"fused-16bit": 1, "fused-tf32": 2, "staged-tcgen05": 2, "staged-ffma": 2, "staged-masked": 3}
+
+
+def roofline(cfg_name: str, path: str, ms: float, bh: int) -> dict:
+    """Binding floor of the kernel(s) of one step, and the measured time against it.
+
+    Fused paths (one kernel): HBM floor = Q, K, V read + O written (4 n d bytes-per-element
+    per head); tensor floor = 3 n^2 d flops per head at the dense rate (QK^T 2 n^2 d dense,
+    P.V n^2 d dense-equivalent at the 2x sparse rate).  Staged exact-FP32 path: HBM floor = the
+    staged bytes (SDDMM writes nonzeros + metadata, the softmax-fused SpMM reads them: 4.5 n^2 +
+    16 n d per head for 1:2 fp32, SURVEY §8(d) with the softmax fused) and FFMA floor = 3 n^2 d on
+    the FP32 pipe.  `frac` = max(floors) / measured; `bound` names the larger floor; `achieved`
+    and `peak` are in that floor's unit.  The issue-rate floor (ncu warp instructions per launch
+    / (4 schedulers x SMs x max clock)) is the practical bound of the epilogue-bound fused kernel."""
+    cfg = CONFIGS[cfg_name]
     n, d = cfg["seq"], cfg["d"]
     eb = 4 if cfg["dtype"] == "float32" else 2
-    gs = 2 if cfg["mode"] == "1:2" else 4
-    nz = n * (n // 2) * eb
-    meta = n * (n // gs) // 2
-    if fused:
-        return {"sddmm": nz + meta + 2 * n * d * eb + 16 * n, "spmm_softmax": nz + meta + 2 * n * d * eb + 16 * n}
-    return {
-        "sddmm": nz + meta + 2 * n * d * eb,
-        "softmax": 2 * nz,
-        "spmm": nz + meta + 2 * n * d * eb,
-    }
+    hbm, tf_bf16, sm_mhz, src = peaks()
+    t = ms * 1e-3
+    if path.startswith("fused"):
+        nbytes = 4 * n * d * eb * bh
+        flops = 3.0 * n * n * d * bh
+        tf = tf_bf16 if path == "fused-16bit" else tf_bf16 / 2  # tf32 dense = half the 16-bit rate
+        floors = {"hbm": nbytes / (hbm * 1e9), "tensor": flops / (tf * 1e12)}
+        kname = ("dfss_flash2_kernel" if n % 256 == 0 else "dfss_flash_kernel") if path == "fused-16bit" \
+            else "dfss_flash_tf32_kernel"
+        stats = kernel_stats(cfg_name, "flash" if path == "fused-16bit" else "flashtf32")
+        peak_tensor = (f"MEASURED_PEAKS.json bf16_tflops ({src})" if path == "fused-16bit" else
+                       f"MEASURED_PEAKS.json bf16_tflops / 2 for tf32 ({src})")
+    else:
+        gs = 2 if cfg["mode"] == "1:2" else 4
+        nz = n * (n // 2) * eb
+        meta = n * (n // gs) // 2
+        nbytes = (2 * (nz + meta) + 4 * n * d * eb) * bh
+        flops = 3.0 * n * n * d * bh
+        tf = FP32_FFMA_TFLOPS
+        floors = {"hbm": nbytes / (hbm * 1e9), "fp32_ffma": flops / (tf * 1e12)}
+        kname = "sddmm_simt_kernel + spmm_simt_softmax (staged exact FP32)"
+        stats = kernel_stats(cfg_name, "spmm")
+        peak_tensor = "nominal FP32 FFMA 148 SMs x 128 FMA/clk x 2 x 1.965 GHz (not in MEASURED_PEAKS.json)"
+    bound = max(floors, key=floors.get)
+    if bound == "hbm":
+        achieved, peak, unit, psrc = nbytes / t / 1e9, hbm, "GB/s", f"MEASURED_PEAKS.json hbm_gbs ({src})"
+    else:
+        achieved, peak, unit, psrc = flops / t / 1e12, tf, "TFLOP/s", peak_tensor
+    out = {"kernel": kname, "bound": bound, "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": unit,
+           "frac": round(floors[bound] / t, 4), "traffic": stats.get("traffic"), "peak_source": psrc,
+           "floors_us": {k: round(v * 1e6, 2) for k, v in floors.items()}, "measured_us": round(t * 1e6, 2),
+           "algorithmic_bytes_per_launch": int(nbytes), "algorithmic_flops_per_launch": flops}
+    if stats.get("warp_instructions"):
+        issue_s = float(stats["warp_instructions"]) / (4 * 148 * sm_mhz * 1e6)
+        out["issue_floor_us"] = round(issue_s * 1e6, 2)
+        out["issue_frac"] = round(issue_s / t, 4)
+        out["ncu_capture"] = stats.get("capture")
+    return out
 
 
-def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True, info=True):
+def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True, info=True, scaling="weak"):
     import paper_2203_00091_b200 as dfss
 
     cfg = CONFIGS[cfg_name]
     n, d = cfg["seq"], cfg["d"]
-    per_rank = cfg["batch"] * cfg["heads"]
-    total_bh = per_rank * ws
+    total_bh = job_heads(cfg, ws, scaling)
     lo, hi = shard(total_bh, ws, rank)
     qkv = make_inputs(cfg, lo, hi, device)
     q, k, v = qkv[0], qkv[1], qkv[2]
     bh = hi - lo
     mode = dfss.SparsityMode.parse(cfg["mode"])
     math_mode = cfg.get("math", "auto")
-    ws_bytes = dfss.workspace_bytes(mode, q.dtype, bh, n, d, math_mode)
+    path = dfss.attention_path(mode, q.dtype, n, d, math_mode)
+    ws_bytes = dfss.workspace_bytes(mode, q.dtype, max(bh, 1), n, d, math_mode)
     workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
     out = torch.empty_like(q)
     flush_buf = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=device)
-    flush = lambda: flush_buf.fill_(1)
+    flush = lambda: flush_buf.fill_(1)  # noqa: E731
 
     def step():
-        dfss.dfss_attention(q, k, v, mode, math_mode=math_mode, out=out, workspace=workspace)
+        if bh:
+            dfss.dfss_attention(q, k, v, mode, math_mode=math_mode, out=out, workspace=workspace)
 
     # ---- timed region: barrier + synchronize on both sides, max over ranks
     if ws > 1:
@@ -218,108 +292,21 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True, info=Tr
     if ws > 1:
         torch.distributed.all_reduce(total_ms, op=torch.distributed.ReduceOp.MAX)
     ms_per_step = float(total_ms.item()) / args.steps
-    flops_per_head = 4.0 * n * n * d
-    value = flops_per_head * total_bh / (ms_per_step * 1e-3) / 1e12  # all ranks' heads / max-rank time
-
-    res = {"ms_per_step": ms_per_step, "value": value, "clocks": clk.summary(), "bh_local": bh}
+    value = 4.0 * n * n * d * total_bh / (ms_per_step * 1e-3) / 1e12  # all ranks' heads / max-rank time
+    res = {"ms_per_step": ms_per_step, "value": value, "clocks": clk.summary(), "bh_local": bh, "path": path,
+           "launches_per_step": LAUNCHES[path] if bh else 0, "lo": lo, "hi": hi}
     if not report_extra:
-        return res
+        return res, (q, k, v, out, lo, hi)
+    res["roofline"] = roofline(cfg_name, path, ms_per_step, bh)
 
-    # ---- per-kernel breakdown on the same stream (the kernels dfss_attention launches)
+    # ---- dense baselines on the same box and shard: unfused cuBLAS (the paper's "full
+    # attention", scale folded into Q) and fused SDPA (flash / cuDNN)
     scale = 1.0 / math.sqrt(d)
-    holder = {}
-    tc16 = ((cfg["dtype"] != "float32" and n % 128 == 0) or (cfg.get("math") == "tf32" and n % 256 == 0)) and d == 64
-    # ^ a fused kernel runs (16-bit 2:4 / 1:2, or tf32 1:2)
-
-    staged_tc = tc16 and cfg["mode"] == "2:4"  # the staged tcgen05 kernels are 2:4-only
-
-    def k_sddmm():
-        holder["c"], _ = dfss.sddmm_prune(q, k, mode, scale, with_row_max=staged_tc)
-
-    def k_softmax():
-        holder["p"] = dfss.softmax_rows(holder["c"], check=False)
-
-    def k_spmm():
-        dfss.spmm(holder["p"], v)
-
-    def k_spmm_softmax():
-        dfss.spmm_softmax(holder["c"], v)
-
-    if info or not tc16:
-        k_sddmm(); k_softmax(); k_spmm()
-    torch.cuda.synchronize()
-    hbm_peak, tf_peak, peak_src = peaks()
-    kt_info = {}
-    if tc16:
-        # the step is ONE kernel (dfss_flash_kernel): its time is the step time
-        kt = {"flash": ms_per_step}
-        for name, fn in (("sddmm_rowmax", k_sddmm), ("spmm_softmax", k_spmm_softmax), ("softmax_rows", k_softmax),
-                         ("spmm", k_spmm)):
-            if not (info and staged_tc):
-                break
-            kt_info[name] = float(np.mean(time_steps(fn, max(3, args.steps), 2, flush)))
-        flops = 3.0 * n * n * d  # QK^T (2n^2d) + kept-half PV (n^2d), SURVEY §8(d)
-        achieved = flops * bh / (ms_per_step * 1e-3) / 1e12
-        traffic = None
-        prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(prof):
-            try:
-                t = json.load(open(prof)).get(cfg_name, {}).get("flash")
-                traffic = None if t is None else int(t)
-            except Exception:
-                traffic = None
-        roof = {"kernel": "dfss_flash2_kernel" if n % 256 == 0 else "dfss_flash_kernel", "bound": "tensor",
-                "achieved": round(achieved, 1), "peak": tf_peak,
-                "unit": "TFLOP/s", "frac": round(achieved / tf_peak, 4), "traffic": traffic,
-                "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_src})",
-                "algorithmic_flops_per_launch": flops * bh,
-                "algorithmic_hbm_bytes_per_launch": 4 * n * d * 2 * bh,
-                "note": "fused kernel, no n^2 HBM traffic (traffic = ncu dram bytes per launch, Q/K/V/O only); "
-                        "tensor work 2n^2d (S) + sparse PV at the 2:4 rate; the bound in practice is instruction "
-                        "issue in the prune + exp epilogue (~29 issued instructions per 4-score group, issue "
-                        "active ~71%, ALU pipe ~67%; profiles/r01j_ncu_summary.md, DESIGN.md 4.1)"}
-        ab = {"flash": 4 * n * d * 2}
-        dom = "flash"
-    else:
-        stages = (("sddmm", k_sddmm), ("softmax", k_softmax), ("spmm", k_spmm))
-        kt = {}
-        for name, fn in stages:
-            kt[name] = float(np.mean(time_steps(fn, max(3, args.steps), 2, flush)))
-        ab = algorithmic_bytes(cfg, False)
-        dom = max(kt, key=kt.get)
-        achieved = ab[dom] * bh / (kt[dom] * 1e-3) / 1e9
-        traffic = None
-        prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(prof):
-            try:
-                t = json.load(open(prof)).get(cfg_name, {}).get(dom)
-                traffic = None if t is None else int(t)
-            except Exception:
-                traffic = None
-        roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
-                "algorithmic_bytes_per_launch": ab[dom] * bh}
-    res["kernels_ms"] = kt
-    res["kernels_info_ms"] = kt_info
-    res["path"] = ("fused flash-DFSS: QK^T -> 2:4 prune -> exp -> tcgen05.mma.sp PV in one kernel" if tc16 else
-                   "staged: sddmm+prune -> softmax -> SpMM")
-    res["roofline"] = roof
-    if not tc16:
-        pipe_bytes = sum(ab.values()) * bh
-        res["pipeline_hbm_gbs"] = round(pipe_bytes / (ms_per_step * 1e-3) / 1e9, 1)
-        res["pipeline_roofline_frac"] = round(pipe_bytes / (ms_per_step * 1e-3) / 1e9 / hbm_peak, 4)
-    else:
-        res["pipeline_hbm_gbs"] = None
-        res["pipeline_roofline_frac"] = None
-
-    # ---- dense baselines on the same box and shard: unfused cuBLAS and fused SDPA
     qd, kd, vd = q.unsqueeze(0), k.unsqueeze(0), v.unsqueeze(0)
 
     def dense_unfused():
-        s = torch.matmul(q, k.transpose(-1, -2)) * scale
-        p = torch.softmax(s, dim=-1)
-        return torch.matmul(p, v)
+        s = torch.matmul(q * scale, k.transpose(-1, -2))
+        return torch.matmul(torch.softmax(s, dim=-1), v)
 
     def dense_sdpa():
         return torch.nn.functional.scaled_dot_product_attention(qd, kd, vd)
@@ -333,8 +320,115 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True, info=Tr
             res.setdefault("baseline_errors", {})[name] = str(ex)[:120]
     res["dense_ms"] = base
     res["speedup_vs_dense"] = {k_: (round(t / ms_per_step, 3) if t else None) for k_, t in base.items()}
+
+    # ---- staged reference-shaped kernels on the same shard (informational: sddmm_prune ->
+    # softmax_rows -> spmm, the three-kernel path the paper describes)
+    if info and path == "fused-16bit" and cfg["mode"] == "2:4":
+        holder = {}
+
+        def k_sddmm():
+            holder["c"], _ = dfss.sddmm_prune(q, k, mode, scale, with_row_max=True)
+
+        def k_spmm_softmax():
+            dfss.spmm_softmax(holder["c"], v)
+
+        k_sddmm()
+        res["staged_kernels_ms"] = {
+            "sddmm_rowmax": float(np.mean(time_steps(k_sddmm, max(3, args.steps), 2, flush))),
+            "spmm_softmax": float(np.mean(time_steps(k_spmm_softmax, max(3, args.steps), 2, flush)))}
     del workspace, flush_buf
     return res, (q, k, v, out, lo, hi)
+
+
+def parity_spot_check(cfg_name, q, k, v, out, lo, hi, total_bh):
+    """Oracle check of heads from the first, middle and last persistent-CTA rounds of the timed
+    output (the two first, one middle and the two last heads of this shard); SURVEY §8(c)
+    tolerances: 1e-5 for exact FP32, 2e-2 for 16-bit and tf32 (on tf32-truncated operands)."""
+    from oracle import oracle_c
+
+    cfg = CONFIGS[cfg_name]
+    bh = hi - lo
+    if bh == 0:
+        return {"heads": [], "ok": True}
+    idx = sorted({0, min(1, bh - 1), bh // 2, max(bh - 2, 0), bh - 1})
+    x = [t[idx].double().cpu().numpy() for t in (q, k, v)]
+    if cfg.get("math") == "tf32":
+        x = [(a.astype(np.float32).view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32).astype(np.float64)
+             for a in x]
+    want = oracle_c.attention_batched(x[0], x[1], x[2], cfg["mode"], nthreads=min(8, len(idx)))
+    got = out[idx].double().cpu().numpy()
+    tol = 1e-5 if cfg["dtype"] == "float32" and cfg.get("math") != "tf32" else 2e-2
+    err = np.abs(got - want)
+    ok = bool((err <= tol + tol * np.abs(want)).all())
+    return {"heads": [lo + i for i in idx], "of": total_bh, "tol": tol, "ok": ok, "max_abs_err": float(err.max())}
+
+
+def e2e_measure(args, cfg, q, k, v, device, ws, total_bh):
+    """Same metric through the public host-buffer API (dfss_attention_host, synchronous like the
+    reference's calls) with pinned host buffers: every step copies Q/K/V host->device, runs the
+    kernel and copies O back, pipelined over 4 batch x heads pieces on three streams.  Max over
+    ranks when N > 1."""
+    import paper_2203_00091_b200 as dfss
+
+    mode = dfss.SparsityMode.parse(cfg["mode"])
+    hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
+    hout = torch.empty(q.shape, dtype=q.dtype).pin_memory()
+    math_mode = cfg.get("math", "auto")
+
+    def step():
+        if q.shape[0]:
+            dfss.dfss_attention_host(hq, hk, hv, mode, math_mode=math_mode, out=hout, chunks=4, device=device)
+
+    if ws > 1:
+        torch.distributed.barrier()
+    ms = float(np.mean(time_steps(step, max(3, args.steps), 2)))
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=device)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    n, d = cfg["seq"], cfg["d"]
+    eb = q.element_size()
+    return {"ms_per_step": ms, "value": 4.0 * n * n * d * total_bh / (ms * 1e-3) / 1e12, "unit": UNIT,
+            "h2d_bytes_per_step": 3 * int(q.shape[0]) * n * d * eb, "d2h_bytes_per_step": int(q.shape[0]) * n * d * eb,
+            "api": "dfss_attention_host (pinned host tensors in and out, synchronous)"}
+
+
+def cpu_reference(cfg, budget_s: float, threads: int, dense: bool = False):
+    """The reference's CPU algorithm (C restatement of nmattn.nm_attention, or of full_attention
+    with dense=True; float64, the numba kernels' operation order) on a bounded sample of the
+    workload's heads, all host threads."""
+    from oracle import oracle_c
+
+    n, d = cfg["seq"], cfg["d"]
+    total_bh = cfg["batch"] * cfg["heads"]
+    qkv = make_inputs(cfg, 0, 1, "cpu")
+    x = [t.double().numpy() for t in qkv]
+    t0 = time.perf_counter()
+    oracle_c.attention_batched(x[0], x[1], x[2], cfg["mode"], nthreads=1, dense=dense)
+    per_head = time.perf_counter() - t0
+    heads = int(max(threads, min(total_bh, budget_s * threads / max(per_head, 1e-6))))
+    heads = max(1, min(total_bh, heads - heads % threads if heads >= threads else heads))
+    qkv = make_inputs(cfg, 0, heads, "cpu")
+    x = [t.double().numpy() for t in qkv]
+    t0 = time.perf_counter()
+    oracle_c.attention_batched(x[0], x[1], x[2], cfg["mode"], nthreads=threads, dense=dense)
+    el = time.perf_counter() - t0
+    what = "full_attention (dense fp64)" if dense else "nm_attention"
+    return {"value": 4.0 * n * n * d * heads / el / 1e12, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{heads} of {total_bh} (batch x head) slices, float64 C restatement of nmattn.{what} "
+                      f"(oracle/dfss_oracle.c, bitwise the numba reference on tests/golden), {el:.2f} s wall, "
+                      f"{per_head * 1e3:.1f} ms/head single-core",
+            "seconds": el, "heads": heads, "ms_per_head_1core": per_head * 1e3}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def block_mask_measure(device, steps=5):
@@ -369,65 +463,30 @@ def block_mask_measure(device, steps=5):
     return res
 
 
-def e2e_measure(args, cfg, q, k, v, device):
-    """Same metric through the public host-buffer API (dfss_attention_host) with pinned host
-    buffers: every step copies Q/K/V host->device, runs the fused kernel and copies O back,
-    pipelined over 4 batch x heads pieces on three streams (both PCIe directions busy;
-    tools/time_host_api.py: 1.70 ms at c2 vs 1.82 ms for the serial copies)."""
-    import paper_2203_00091_b200 as dfss
-
-    mode = dfss.SparsityMode.parse(cfg["mode"])
-    hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
-    hout = torch.empty(q.shape, dtype=q.dtype).pin_memory()
-    math_mode = cfg.get("math", "auto")
-
-    def step():
-        dfss.dfss_attention_host(hq, hk, hv, mode, math_mode=math_mode, out=hout, chunks=4, device=device)
-
-    ts = time_steps(step, max(3, args.steps), 2)
-    ms = float(np.mean(ts))
-    n, d = cfg["seq"], cfg["d"]
-    bh = q.shape[0]
-    eb = q.element_size()
-    return {"ms_per_step": ms, "value": 4.0 * n * n * d * bh / (ms * 1e-3) / 1e12, "unit": UNIT,
-            "h2d_bytes_per_step": 3 * bh * n * d * eb, "d2h_bytes_per_step": bh * n * d * eb}
-
-
-def cpu_reference(cfg, budget_s: float, threads: int):
-    """The oracle port of the reference nm_attention (C, float64, same op order as the numba kernels),
-    on a bounded sample of the workload's heads, all host threads."""
-    from oracle import oracle_c
-
-    n, d = cfg["seq"], cfg["d"]
-    total_bh = cfg["batch"] * cfg["heads"]
-    # estimate per-head cost with one head, then size the sample to ~budget_s
-    qkv = make_inputs(cfg, 0, 1, "cpu")
-    x = [t.double().numpy() for t in qkv]
-    t0 = time.perf_counter()
-    oracle_c.attention_batched(x[0], x[1], x[2], cfg["mode"], nthreads=1)
-    per_head = time.perf_counter() - t0
-    heads = int(max(threads, min(total_bh, budget_s * threads / max(per_head, 1e-6))))
-    heads = max(1, min(total_bh, heads - heads % threads if heads >= threads else heads))
-    qkv = make_inputs(cfg, 0, heads, "cpu")
-    x = [t.double().numpy() for t in qkv]
-    t0 = time.perf_counter()
-    oracle_c.attention_batched(x[0], x[1], x[2], cfg["mode"], nthreads=threads)
-    el = time.perf_counter() - t0
-    value = 4.0 * n * n * d * heads / el / 1e12
-    return {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{heads} of {total_bh} (batch x head) slices, float64 C restatement of nmattn.nm_attention "
-                      f"(oracle/dfss_oracle.c), {el:.2f} s wall, {per_head * 1e3:.1f} ms/head single-core",
-            "seconds": el, "heads": heads}
-
-
-def cpu_model():
-    try:
-        for line in open("/proc/cpuinfo"):
-            if line.startswith("model name"):
-                return line.split(":", 1)[1].strip()
-    except OSError:
-        pass
-    return "unknown"
+def reference_arm(args, ws, rank, threads):
+    """--impl reference: the reference's CPU algorithm on the host cores, rank 0 only."""
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    steps = []
+    budget = max(2.0, min(20.0, 150.0 / (args.steps + args.warmup)))
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference(cfg, budget, threads)
+        if i >= args.warmup:
+            steps.append(r)
+    dense = cpu_reference(cfg, min(budget, 10.0), threads, dense=True)
+    val = float(np.median([s["value"] for s in steps]))
+    secs = float(np.median([s["seconds"] for s in steps]))
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(args.config, args.gpus, args.scaling, steps[-1]["heads"]),
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": steps[-1]["sample"], "cpu_model": cpu_model()},
+            "cpu_full_attention": {"value": dense["value"], "unit": UNIT, "cores": threads, "sample": dense["sample"]},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
 
 
 def main():
@@ -437,6 +496,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["dfss", "reference"], default="dfss")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--no-sweep", action="store_true", help="skip the configs[4] sequence sweep")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for the CPU baseline")
     ap.add_argument("--no-extra", action="store_true", help="skip sweep / e2e / cpu baseline (profiling runs)")
@@ -446,28 +506,8 @@ def main():
     ws, rank, local = dist_env()
     cfg = CONFIGS[args.config]
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-
     if args.impl == "reference":
-        if rank != 0:
-            return 0
-        steps = []
-        budget = max(2.0, min(20.0, 150.0 / (args.steps + args.warmup)))
-        for i in range(args.warmup + args.steps):
-            r = cpu_reference(cfg, budget, threads)
-            if i >= args.warmup:
-                steps.append(r)
-        val = float(np.median([s["value"] for s in steps]))
-        secs = float(np.median([s["seconds"] for s in steps]))
-        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": args.config + ": " + cfg["desc"], "batch": cfg["batch"], "heads": cfg["heads"],
-                           "seq_len": cfg["seq"], "head_dim": cfg["d"], "mode": cfg["mode"]},
-                "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
-                                 "sample": steps[-1]["sample"], "cpu_model": cpu_model()},
-                "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
-        return 0
+        return reference_arm(args, ws, rank, threads)
 
     if ws > 1:
         torch.cuda.set_device(local)
@@ -476,56 +516,63 @@ def main():
         torch.cuda.set_device(0)
     device = torch.device("cuda", torch.cuda.current_device())
 
-    res, (q, k, v, out, lo, hi) = run_dfss(args, args.config, ws, rank, local, device)
-    launches_per_step = len(res["kernels_ms"])  # kernels dfss_nm_attention launches per step (1 when fused)
+    res, (q, k, v, out, lo, hi) = run_dfss(args, args.config, ws, rank, local, device, scaling=args.scaling)
+    total_bh = job_heads(cfg, ws, args.scaling)
 
-    # end-to-end parity gather: NCCL all_gather of the output shards (outside the timed region)
+    # end-to-end parity gather: NCCL all_gather of the output shards (outside the timed region);
+    # shards are padded to the largest one (strong scaling may split unevenly)
     parity = None
     if ws > 1:
-        total_bh = cfg["batch"] * cfg["heads"] * ws
-        gathered = torch.empty((total_bh,) + tuple(out.shape[1:]), dtype=out.dtype, device=device)
-        torch.distributed.all_gather_into_tensor(gathered, out.contiguous())
-        parity = {"gathered_heads": int(total_bh), "checksum": float(gathered.float().abs().sum()),
-                  "shards_equal_local": bool(torch.equal(gathered[lo:hi], out))}
+        width = max(b - a for a, b in (shard(total_bh, ws, r) for r in range(ws)))
+        pad = torch.zeros((width,) + tuple(out.shape[1:]), dtype=out.dtype, device=device)
+        pad[: hi - lo] = out
+        gathered = torch.empty((width * ws,) + tuple(out.shape[1:]), dtype=out.dtype, device=device)
+        torch.distributed.all_gather_into_tensor(gathered, pad)
+        parts = [gathered[r * width: r * width + (shard(total_bh, ws, r)[1] - shard(total_bh, ws, r)[0])]
+                 for r in range(ws)]
+        full = torch.cat(parts)
+        parity = {"gathered_heads": int(full.shape[0]), "checksum": float(full.float().abs().sum()),
+                  "shards_equal_local": bool(torch.equal(full[lo:hi], out))}
 
     extra = {}
+    if not args.no_extra:
+        extra["e2e"] = e2e_measure(args, cfg, q, k, v, device, ws, total_bh)
     if rank == 0 and not args.no_extra:
-        # oracle spot check of two heads of the timed output (SURVEY §8(c) tolerances)
-        from oracle import oracle_c
-
-        hq, hk, hv, ho = (x[:2].double().cpu().numpy() for x in (q, k, v, out))
-        want = oracle_c.attention_batched(hq, hk, hv, cfg["mode"], nthreads=2)
-        tol = 1e-5 if cfg["dtype"] == "float32" else 2e-2
-        ok = bool((np.abs(ho - want) <= tol + tol * np.abs(want)).all())
-        extra["parity_spot_check"] = {"heads": 2, "tol": tol, "ok": ok,
-                                      "max_abs_err": float(np.abs(ho - want).max())}
+        extra["parity_spot_check"] = parity_spot_check(args.config, q, k, v, out, lo, hi, total_bh)
+        budget = args.cpu_budget if ws == 1 else min(args.cpu_budget, 8.0)
+        cb = cpu_reference(cfg, budget, threads)
+        cb["cpu_model"] = cpu_model()
+        extra["cpu_baseline"] = cb
+        cd = cpu_reference(cfg, min(budget, 8.0), threads, dense=True)
+        extra["cpu_full_attention"] = {"value": cd["value"], "unit": UNIT, "cores": threads, "sample": cd["sample"]}
         if ws == 1:
-            extra["e2e"] = e2e_measure(args, cfg, q, k, v, device)
-            cb = cpu_reference(cfg, args.cpu_budget, threads)
-            cb["cpu_model"] = cpu_model()
-            extra["cpu_baseline"] = cb
-            sweep = {}
-            for name in ("c1", "c3", "c4"):
+            others = {}
+            for name in ("c1", "c2", "c3", "c4"):
                 if name == args.config:
                     continue
                 try:
-                    r2, _ = run_dfss(argparse.Namespace(steps=max(3, args.steps // 2), warmup=3), name, 1, 0, 0,
-                                     device)
-                    sweep[name] = {"ms_per_step": round(r2["ms_per_step"], 4), "tflops": round(r2["value"], 2),
-                                   "speedup_vs_dense": r2["speedup_vs_dense"], "dense_ms": r2["dense_ms"],
-                                   "kernels_ms": r2["kernels_ms"], "kernels_info_ms": r2["kernels_info_ms"],
-                                   "path": r2["path"], "roofline": r2["roofline"],
-                                   "pipeline_roofline_frac": r2["pipeline_roofline_frac"]}
+                    r2, (q2, k2, v2, o2, lo2, hi2) = run_dfss(argparse.Namespace(steps=max(3, args.steps // 2),
+                                                                                 warmup=3), name, 1, 0, 0, device)
+                    others[name] = {"ms_per_step": round(r2["ms_per_step"], 4), "tflops": round(r2["value"], 2),
+                                    "speedup_vs_dense": r2["speedup_vs_dense"], "dense_ms": r2["dense_ms"],
+                                    "path": r2["path"], "gpu_launches_per_step": r2["launches_per_step"],
+                                    "roofline": r2["roofline"],
+                                    "parity_spot_check": parity_spot_check(name, q2, k2, v2, o2, lo2, hi2, hi2 - lo2)}
+                    if "staged_kernels_ms" in r2:
+                        others[name]["staged_kernels_ms"] = r2["staged_kernels_ms"]
+                    del q2, k2, v2, o2
                 except Exception as ex:
-                    sweep[name] = {"error": str(ex)[:200]}
-            extra["other_configs"] = sweep
+                    others[name] = {"error": str(ex)[:200]}
+            extra["other_configs"] = others
             if not args.no_sweep:
                 sw = {}
-                for name in sorted((c for c in CONFIGS if c.startswith("c5_")), key=lambda c: (c.split("_")[1], int(c.split("_")[2]))):
+                for name in sorted((c for c in CONFIGS if c.startswith("c5_")),
+                                   key=lambda c: (c.split("_")[1], int(c.split("_")[2]))):
                     try:
                         r2, _ = run_dfss(argparse.Namespace(steps=5, warmup=3), name, 1, 0, 0, device, info=False)
                         sw[name] = {"ms": round(r2["ms_per_step"], 4), "tflops": round(r2["value"], 1),
-                                    "speedup_vs_dense": r2["speedup_vs_dense"], "path": r2["path"].split(":")[0]}
+                                    "speedup_vs_dense": r2["speedup_vs_dense"], "path": r2["path"],
+                                    "frac": r2["roofline"]["frac"], "bound": r2["roofline"]["bound"]}
                     except Exception as ex:
                         sw[name] = {"error": str(ex)[:200]}
                 extra["sweep"] = sw
@@ -538,23 +585,20 @@ def main():
         line = {
             "metric": METRIC, "value": round(res["value"], 3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(res["ms_per_step"], 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
-            "dtype": {"float32": "f32", "bfloat16": "bf16", "float16": "f16"}[cfg["dtype"]],
+            "scaling": args.scaling, "vs_baseline": None, "dtype": DTYPE_TAG[cfg["dtype"]],
             "data": "synthetic N(0,1) Q/K/V, seeded per (seed, global head)",
-            "config": {"workload": args.config + ": " + cfg["desc"], "batch": cfg["batch"], "heads": cfg["heads"],
-                       "seq_len": cfg["seq"], "head_dim": cfg["d"], "mode": cfg["mode"],
-                       "global_batch": cfg["batch"] * ws, "parallelism": f"bh-shard{ws}", "heads_per_rank": res["bh_local"],
-                       "l2": "flushed between timed steps (256 MiB write, outside the step events)"},
-            "roofline": res["roofline"], "path": res["path"], "kernels_ms": res["kernels_ms"],
-            "kernels_info_ms": res["kernels_info_ms"],
-            "pipeline_hbm_gbs": res["pipeline_hbm_gbs"], "pipeline_roofline_frac": res["pipeline_roofline_frac"],
+            "config": config_block(args.config, ws, args.scaling, res["bh_local"]),
+            "roofline": res["roofline"], "path": res["path"],
             "dense_ms": res["dense_ms"], "speedup_vs_dense": res["speedup_vs_dense"],
-            "gpu_launches": launches_per_step * args.steps, "clocks": res["clocks"],
+            "gpu_launches": res["launches_per_step"] * args.steps, "clocks": res["clocks"],
         }
+        if "staged_kernels_ms" in res:
+            line["staged_kernels_ms"] = res["staged_kernels_ms"]
         if "e2e" in extra:
             e = extra.pop("e2e")
             line["e2e"] = {"value": round(e["value"], 3), "unit": e["unit"], "h2d_bytes_per_step": e["h2d_bytes_per_step"],
-                           "d2h_bytes_per_step": e["d2h_bytes_per_step"], "ms_per_step": round(e["ms_per_step"], 4)}
+                           "d2h_bytes_per_step": e["d2h_bytes_per_step"], "ms_per_step": round(e["ms_per_step"], 4),
+                           "api": e["api"]}
         if "cpu_baseline" in extra:
             line["cpu_baseline"] = extra.pop("cpu_baseline")
         if parity:

@@ -66,12 +66,23 @@ def test_bh_sharding_and_gather_match_single_process():
 
 
 def test_shard_bounds_cover_exactly():
-    for total, ws in [(12, 8), (384, 8), (96, 3), (5, 2)]:
+    for total, ws in [(12, 8), (384, 8), (96, 3), (5, 2), (3, 8)]:
         seen = []
         for r in range(ws):
             lo, hi = bench.shard(total, ws, r)
             seen.extend(range(lo, hi))
         assert seen == list(range(total))
+    # floor + remainder: c1 on 8 ranks 2,2,2,2,1,1,1,1; c4 12 per rank
+    assert [bench.shard(12, 8, r)[1] - bench.shard(12, 8, r)[0] for r in range(8)] == [2, 2, 2, 2, 1, 1, 1, 1]
+    assert {bench.shard(96, 8, r)[1] - bench.shard(96, 8, r)[0] for r in range(8)} == {12}
+
+
+def test_weak_and_strong_job_sizes_and_config_keys():
+    c4 = bench.CONFIGS["c4"]
+    assert bench.job_heads(c4, 8, "weak") == 8 * 96 and bench.job_heads(c4, 8, "strong") == 96
+    a = bench.config_block("c2", 4, "strong", 96)
+    b = bench.config_block("c2", 4, "strong", 12)
+    assert a.keys() == b.keys() and a["global_heads"] == 384 and a["parallelism"] == "bh-shard4"
 
 
 def test_inputs_seeded_per_global_head():

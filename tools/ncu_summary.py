@@ -5,7 +5,8 @@
 Reads gpurun_out/launches_<tag>_<cfg>.csv (gpu__time_duration launch lists) and
 gpurun_out/prof_<tag>_<cfg>_<kernel>.ncu-rep (--set full), writes
 profiles/<tag>_ncu_summary.md, copies the launch lists to profiles/, and
-updates profiles/ncu_traffic.json (dram bytes per launch, read by bench.py).
+updates profiles/ncu_kernel_stats.json (dram bytes and issued warp instructions per launch,
+read by bench.py for the roofline traffic and the issue-rate floor).
 """
 
 from __future__ import annotations
@@ -36,6 +37,7 @@ METRICS = {
     "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
     "launch__registers_per_thread": "regs",
     "smsp__inst_executed.sum": "warp_insts",
+    "smsp__inst_issued.sum": "warp_issued",
     "sm__cycles_elapsed.avg.per_second": "sm_clock",
 }
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1e-9, "us": 1e-6,
@@ -78,7 +80,7 @@ def main(tag: str) -> None:
     lines = [f"# ncu summary `{tag}`", "",
              "Captured with `tools/profile.sh` / `tools/prof_one.sh` under gpurun on one B200 "
              "(`--clock-control none`; launch lists are cold-cache and serialised, compare shares).", ""]
-    traffic_path = os.path.join(PROF, "ncu_traffic.json")
+    traffic_path = os.path.join(PROF, "ncu_kernel_stats.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     for path in sorted(glob.glob(os.path.join(OUT, f"launches_{tag}_*.csv"))):
         cfg = path.rsplit("_", 1)[1].replace(".csv", "")
@@ -105,7 +107,8 @@ def main(tag: str) -> None:
         suffix = base.split("_")[-1]
         key = (suffix if suffix.startswith("flash") and suffix != "flash" else "flash" if "flash" in kname
                else "sddmm" if "sddmm" in kname else "softmax" if "softmax" in kname else "spmm")
-        traffic.setdefault(cfg, {})[key] = int(dram)
+        traffic.setdefault(cfg, {})[key] = {"traffic": int(dram), "capture": tag,
+                                            "warp_instructions": m.get("warp_issued", m.get("warp_insts", 0))}
         lines += [f"## `{kname}` — {cfg} (`{base}.ncu-rep`)", "",
                   f"- duration {m.get('duration', 0) * 1e6:.1f} µs at SM clock {m.get('sm_clock', 0) / 1e9:.2f} GHz",
                   f"- DRAM traffic {dram / 1e9:.3f} GB (read {m.get('dram_read', 0) / 1e9:.3f}, "

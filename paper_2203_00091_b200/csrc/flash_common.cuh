@@ -70,15 +70,27 @@ struct FlashDump {
   uint32_t* meta = nullptr;
 };
 
-// one 32-column chunk of one row: registers in (k0, k2, k1, k3) order per group of 4 (the
-// permuted K tensor map) back to key order, times the exact power-of-two scale 1/sqrt(64)
+// one 32-column chunk of one row, times the exact power-of-two scale 1/sqrt(64), in key order.
+// PERMUTED: registers hold each group of 4 in (k0, k2, k1, k3) order (the tf32 kernel's
+// permuted K tensor map); otherwise in key order (the 16-bit kernels).
+template <bool PERMUTED>
 __device__ __forceinline__ void dump_chunk_scores(float* dst, const uint32_t (&s)[32], float scale) {
   float4* d4 = reinterpret_cast<float4*>(dst);
+  constexpr int i1 = PERMUTED ? 2 : 1, i2 = PERMUTED ? 1 : 2;
 #pragma unroll
   for (int g = 0; g < 8; ++g)
-    d4[g] = make_float4(__uint_as_float(s[4 * g]) * scale, __uint_as_float(s[4 * g + 2]) * scale,
-                        __uint_as_float(s[4 * g + 1]) * scale, __uint_as_float(s[4 * g + 3]) * scale);
+    d4[g] = make_float4(__uint_as_float(s[4 * g]) * scale, __uint_as_float(s[4 * g + i1]) * scale,
+                        __uint_as_float(s[4 * g + i2]) * scale, __uint_as_float(s[4 * g + 3]) * scale);
 }
+
+// Register budget of the warp-specialised fused kernels (640 threads = 96 registers each at
+// launch): the role warpgroup (warps 16-19: TMA, MMA issuers) drops to 32 registers and the
+// four softmax warpgroups take the freed 8192 -- 112 each -- so the prune / exp epilogue
+// keeps two 32-column chunks in flight without spilling.  Warpgroup-uniform, and the two
+// branches must not re-join (ptxas needs one register budget per code region): each one
+// finishes the CTA itself.
+__device__ __forceinline__ void regs_role() { asm volatile("setmaxnreg.dec.sync.aligned.u32 32;\n" ::: "memory"); }
+__device__ __forceinline__ void regs_softmax() { asm volatile("setmaxnreg.inc.sync.aligned.u32 112;\n" ::: "memory"); }
 
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");

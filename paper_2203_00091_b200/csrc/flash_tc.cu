@@ -83,9 +83,16 @@ constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kSumLimit = 256.0f;  // a quarter-tile partial sum above 2^8 triggers a shift update
 }  // namespace
 
-// One quarter-tile of one row: 8 groups of 4 scores s[] in (v0, v2, v1, v3) register order.
-// Prunes 2:4 (reference rule), exponentiates the kept half against the shift `mlog`
-// (= m * c), packs P, builds the metadata word W (group g at bits 4g) and the partial sum.
+// One quarter-tile of one row: 8 groups of 4 scores s[] in key order.  Prunes 2:4 (reference
+// rule), exponentiates the kept half against the shift `mlog` (= m * c), packs P, builds the
+// metadata word W (group g at bits 4g) and the partial sum.
+//
+// Instruction budget per group (the kernel is bound by the ALU pipe, 2 clk per warp
+// instruction per sub-partition, like the FMA pipe): 4 FMNMX + 2 FSETP + 2 predicated FSEL on
+// the ALU; FADD x2 + IMAD.HI x2 (pair winners' sign bits) + IMAD (nibble) + FFMA2 + FADD2 on
+// the FMA pipe; 2 MUFU.EX2; F2FP.  Key-order registers make the kept pair land in the
+// registers of (v0, v1) -- an aligned pair for FFMA2 -- and each of lo / hi is one FSEL
+// predicated on "that register's own value is not the kept one" (keep01 keeps v0 / v1).
 //
 // PAIRS (mode 1:2 on 16-bit data): keep the larger of each pair, element 1 iff v1 > v0
 // (codec.py:114-117) -- on the tensor core this is the 2:4 pattern with one survivor per
@@ -99,15 +106,14 @@ __device__ __forceinline__ void prune_exp_tile(const uint32_t (&s)[32], float c,
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
     const float v0 = __uint_as_float(s[4 * g + 0]);
-    const float v2 = __uint_as_float(s[4 * g + 1]);
-    const float v1 = __uint_as_float(s[4 * g + 2]);
+    const float v1 = __uint_as_float(s[4 * g + 1]);
+    const float v2 = __uint_as_float(s[4 * g + 2]);
     const float v3 = __uint_as_float(s[4 * g + 3]);
     // winner index of each pair from the sign of the difference (ties -> +0 -> lower index).
     // tcgen05.mma writes every zero score as +0 (tools/negzero_probe.cu; covered by
     // test_flash_tie_lattice_and_zero_queries), so (-0) - (+0) cannot occur and the
     // differences need no canonicalisation.
-    float d01, d23;
-    sub2(v0, v2, v1, v3, d01, d23);
+    const float d01 = v0 - v1, d23 = v2 - v3;
     // sign bits: IMAD.HI on the FMA pipe for 2:4 (the ALU pipe is the busy one there), SHF on
     // the otherwise idle ALU pipe for 1:2 (there the FMA pipe and MUFU are the busy ones)
     const uint32_t a = PAIRS ? __float_as_uint(d01) >> 31 : sign_bit(d01, two);
@@ -212,7 +218,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int t = 0; t < ntiles; ++t) {
           tc::mbar_wait_sleep(&k_empty[ks], kph ^ 1);
           tc::mbar_arrive_expect_tx(&k_full[ks], K_BYTES);
-          tc::tma_load_5d(smem + SMEM_K + ks * K_BYTES, &tm_k, &k_full[ks], 0, 0, 0, t * (BN / 4), b);
+          tc::tma_load_3d(smem + SMEM_K + ks * K_BYTES, &tm_k, &k_full[ks], 0, t * BN, b);
           if (++ks == KST) { ks = 0; kph ^= 1; }
         }
       }
@@ -345,7 +351,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
           if constexpr (DUMP)
-            dump_chunk_scores(dump.s + ((int64_t)b * n + (ib * HALVES + h) * BM + r) * n + t * BN + quarter * 32, s,
+            dump_chunk_scores<false>(dump.s + ((int64_t)b * n + (ib * HALVES + h) * BM + r) * n + t * BN + quarter * 32, s,
                               scale);
           uint32_t pk[8], W;
           float lt0, lt1;
@@ -360,7 +366,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (cmask) masked_chunk(pk, W, lt0, lt1); else prune_exp_tile<T, PAIRS>(s, c, mlog[h], two, pk, W, lt0, lt1);
           } else {
             if (cmask) masked_chunk(pk, W, lt0, lt1); else prune_exp_tile<T, PAIRS>(s, c, mlog[h], two, pk, W, lt0, lt1);
-            if (bar_any(qbar, 128, !(lt0 + lt1 <= kSumLimit))) {
+            if (bar_any(qbar, 128, !(lt0 + lt1 <= kSumLimit) || W == ~0u)) {  // W: see the two-set kernel
               // ---- slow path (whole quad): raise the shift to the row maximum, rescale O_h and the sums.
               // Every PV into O_h issued so far has retired: with PST == HALVES the P-stage wait
               // above was for this half's previous tile; otherwise wait for the step before.
@@ -602,6 +608,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) FTRACE(15, 0, 1, 0);  // setup done
 
+  if (warp >= SM_WARPS) {
+  regs_role();
   if (warp == W_QK) {
     // ------------------------------------------------------------ TMA producer: Q (both halves), K (keys permuted), V
     if (lane == 0) {
@@ -621,7 +629,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (MASKED && !(((lw0 | lw1) >> (t & 31)) & 1u)) continue;
           wait_role(&k_empty[ks], kph ^ 1);
           tc::mbar_arrive_expect_tx(&k_full[ks], K_BYTES);
-          tc::tma_load_5d(smem + S2_K + ks * K_BYTES, &tm_k, &k_full[ks], 0, 0, 0, t * (BN / 4), b);
+          tc::tma_load_3d(smem + S2_K + ks * K_BYTES, &tm_k, &k_full[ks], 0, t * BN, b);
           FTRACE(8, it, t, 0);
           if (++ks == K2ST) { ks = 0; kph ^= 1; }
           wait_role(&v_empty[vs], vph ^ 1);
@@ -738,7 +746,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc::mma_commit_w(&o_full[h]);
       }
     }
-  } else if (warp < SM_WARPS) {
+  }
+  // end of the role warpgroup (no code after the branches: ptxas needs one register budget
+  // per region, so each branch finishes the CTA itself)
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == W_PV) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc<512>(tmem_base);
+  }
+  } else {
+    regs_softmax();
     // ------------------------------------------------------------ softmax / prune / epilogue sets
     const int h = warp >> 3;              // half owned by this set
     const int pr = (warp >> 2) & 1;       // column pair: quarters 2pr, 2pr + 1
@@ -848,7 +866,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tc::tmem_ld_wait(s);
             if (tw) FTRACE(11 + 2 * ch, it, t, h);
             if constexpr (DUMP)
-              dump_chunk_scores(dump.s + ((int64_t)b * n + (ib * 2 + h) * BM + r) * n + t * BN + 64 * pr + 32 * ch, s,
+              dump_chunk_scores<false>(dump.s + ((int64_t)b * n + (ib * 2 + h) * BM + r) * n + t * BN + 64 * pr + 32 * ch, s,
                                 scale);
             prune_exp_tile<T, PAIRS>(s, c, mlog, two, pk[ch], W[ch], a0, a1);
             // masked chunk (structurally absent): computed like the others -- straight-line code
@@ -863,7 +881,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int pass = 0;; ++pass) {
           if (MASKED && anym) compute(std::true_type{});
           else compute(std::false_type{});
-          if (pass > 0 || first || !bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit))) break;
+          // (W[0] & W[1]) == ~0 never holds (no nibble is 0xF); it makes the vote consume the
+          // metadata so ptxas builds W before the branch instead of keeping every group's
+          // keep predicates / operands alive across it (which spilled to local memory)
+          if (pass > 0 || first || !bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit) || (W[0] & W[1]) == ~0u)) break;
           // ---- slow path (both warps of the pair): raise the shift to the row maximum,
           // rescale O_h and the sums once every PV into O_h so far (this half's tile t-1) retired.
           // (pv_done[h] completes once per tile of this half and cannot run ahead of this set,
@@ -921,14 +942,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       cw = cwn;
     }
     if (pend) epilogue();
+    if (threadIdx.x == 0) FTRACE(15, 1, 0, 0);  // CTA end
+    tc::tc_fence_before();
+    __syncthreads();
   }
-  tc::tc_fence_before();
-  __syncthreads();
-  if (warp == W_PV) {
-    tc::tc_fence_after();
-    tc::tmem_dealloc<512>(tmem_base);
-  }
-  if (threadIdx.x == 0) FTRACE(15, 1, 0, 0);  // CTA end
 }
 
 #ifndef DFSS_FLASH_DUMP_TU  // defined once, in flash_tc.cu
@@ -1011,17 +1028,11 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
   const CUtensorMapDataType dt =
       std::is_same<T, __nv_bfloat16>::value ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tq, tk, tv;
-  // K as [bh][n/4 groups][j2][j1][d] with key = 4g + 2 j1 + j2 and j1 iterated before j2:
-  // the smem rows of a tile come out in key order (k0, k2, k1, k3) per group of 4.
-  const uint64_t row = HD * 2;
-  const uint64_t kdims[5] = {(uint64_t)HD, 2, 2, (uint64_t)n / 4, (uint64_t)bh};
-  const uint64_t kstr[4] = {2 * row, row, 4 * row, (uint64_t)n * row};
-  const uint32_t kbox[5] = {(uint32_t)HD, 2, 2, BN / 4, 1};
   // n % 256 == 0: the two-set kernel (256-row items, independent softmax sets per half);
   // otherwise 128-row items with all 16 softmax warps on one half
   const bool two_set = n % (2 * BM) == 0 && (!MASKED || flash_mask_two_set_ok(n));
   if (!encode_tmap_3d(&tq, dt, 2, (void*)q, HD, n, bh, HD, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !encode_tmap(&tk, dt, 5, (void*)k, kdims, kstr, kbox, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !encode_tmap_3d(&tk, dt, 2, (void*)k, HD, n, bh, HD, BN, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !encode_tmap_3d(&tv, dt, 2, (void*)v, HD, n, bh, HD, BN, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   const int halves = two_set ? 2 : 1;

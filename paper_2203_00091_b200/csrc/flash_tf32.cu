@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tc::tmem_ld_32x32b_x32(scol + 32 * ch, s);
             tc::tmem_ld_wait(s);
             if constexpr (DUMP)
-              dump_chunk_scores(dump.s + ((int64_t)b * n + (ib * 2 + h) * BM + r) * n + t * BN + 64 * pr + 32 * ch, s,
+              dump_chunk_scores<true>(dump.s + ((int64_t)b * n + (ib * 2 + h) * BM + r) * n + t * BN + 64 * pr + 32 * ch, s,
                                 scale);
             prune12_chunk(s, c, mlog, p[ch], W[ch][0], W[ch][1], a0, a1);
             if (MV && cm[ch]) {  // masked chunk: structurally absent

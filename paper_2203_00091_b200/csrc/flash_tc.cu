@@ -824,6 +824,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       return __ldg(tmask.cbits + (int64_t)strip * tmask.cbw + lane);
     };
     uint32_t cw = cword(pos_at(0));
+    const uint32_t word_sel = (lane & 8) ? 0x3276u : 0x5410u;
     for (int kk_ = 0, pos = pos_at(0); pos < items; pos = pos_at(++kk_), ++it) {
         const int item = item_of(pos);
         uint32_t lw0 = 0, lw1 = 0;
@@ -912,12 +913,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (tw) FTRACE(1, it, t, h);
         // P (8 columns of 16-bit pairs at 32q + 16) and the metadata word (column 32q) of each
         // chunk into this warp's own, already read S columns; rows r and r^8 trade metadata
-        // halves (include/dfss.h)
+        // halves (include/dfss.h): one PRMT with a lane-dependent selector
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
           const uint32_t partner = __shfl_xor_sync(0xffffffffu, W[ch], 8);
-          const uint32_t word =
-              (lane & 8) ? ((partner >> 16) | (W[ch] & 0xFFFF0000u)) : ((W[ch] & 0xFFFFu) | (partner << 16));
+          const uint32_t word = __byte_perm(W[ch], partner, word_sel);
           tc::tmem_st_32x32b_x8(scol + 32 * ch + 16, pk[ch]);
           tc::tmem_st_32x32b_x1(scol + 32 * ch, word);
           if constexpr (DUMP)

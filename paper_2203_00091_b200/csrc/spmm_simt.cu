@@ -8,6 +8,7 @@
 // broadcast by shuffles, lanes own output columns lane + 32*t.
 // This is the exact-FP32 path (c1 at 1e-5) and the fallback for shapes the
 // tcgen05.mma.sp kernel does not tile.
+#include <type_traits>
 #include <cstdlib>
 
 #include "dfss_common.cuh"
@@ -176,23 +177,28 @@ __global__ void __launch_bounds__(256) spmm_simt_softmax_d64_kernel(const float*
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int j0 = 0; j0 < nzc; j0 += 32) {  // same trip count in both halves (converged shuffles)
+    // one batch = 32 nonzeros, 16 per half-warp; same trip count in both halves (converged
+    // shuffles).  Full batches run unpredicated (all 16 V-row loads in flight); only the row's
+    // last partial batch predicates its slots -- slots past the row end are skipped, not
+    // weighted 0 (an Inf in an unrelated V row must not leak in as 0 * Inf).
+    auto batch = [&](int j0, auto tail) {
+      constexpr bool TAIL = decltype(tail)::value;
       const int j = j0 + 16 * part + hl;
       float pv = 0.f;
       int col = 0;
-      if (j < nzc) {
+      if (!TAIL || j < nzc) {
         const int g = (GS == 4) ? (j >> 1) : j;
         int shift;
         const uint32_t nib = (mb[geo.word_of(r, g, shift)] >> shift) & 0xFu;
         col = (GS == 4) ? 4 * g + (int)((j & 1) ? ((nib >> 2) & 3u) : (nib & 3u)) : 2 * g + (nib == 0xEu ? 1 : 0);
         pv = exp2f(fmaf(prow[j], kLog2e, -mlb));
       }
-      const int cnt = nzc - (j0 + 16 * part);  // slots past the row end are skipped, not weighted 0
+      const int cnt = nzc - (j0 + 16 * part);
 #pragma unroll
       for (int l = 0; l < 16; ++l) {
         const float pl = __shfl_sync(0xffffffffu, pv, l, 16);
         const int cl = __shfl_sync(0xffffffffu, col, l, 16);
-        if (l < cnt) {
+        if (!TAIL || l < cnt) {
           const float4 x = vb[(int64_t)cl * 16 + hl];
           acc.x = fmaf(pl, x.x, acc.x);
           acc.y = fmaf(pl, x.y, acc.y);
@@ -200,7 +206,10 @@ __global__ void __launch_bounds__(256) spmm_simt_softmax_d64_kernel(const float*
           acc.w = fmaf(pl, x.w, acc.w);
         }
       }
-    }
+    };
+    const int nfull = nzc & ~31;
+    for (int j0 = 0; j0 < nfull; j0 += 32) batch(j0, std::false_type{});
+    if (nfull < nzc) batch(nfull, std::true_type{});
     acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
     acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
     acc.z += __shfl_xor_sync(0xffffffffu, acc.z, 16);

@@ -126,7 +126,8 @@ int64_t dfss_nm_attention_workspace_bytes_for(int mode, int dtype, int math, int
   const bool mask_ok = !masked || dfss::tc_flash_mask_supported(tile_rows, tile_cols);
   if (math == DFSS_MATH_AUTO && dtype != DFSS_F32 && dfss::tc_flash_supported(mode, dtype, n, d) && mask_ok &&
       dfss_has_tcgen05())
-    return masked ? dfss::flash_mask_workspace_bytes(n) : 0;  // fused: no intermediate in HBM (mask bitmaps only)
+    // fused: no n x n intermediate in HBM -- mask bitmaps, or the split last round's partial O
+    return masked ? dfss::flash_mask_workspace_bytes(n) : dfss::flash_split_workspace_bytes(bh, n);
   if (math == DFSS_MATH_TF32 && dtype == DFSS_F32 && dfss::tc_flash_tf32_supported(mode, n, d) &&
       (!masked || (mask_ok && dfss::flash_mask_two_set_ok(n))) && dfss_has_tcgen05())
     return dfss::flash_tf32_workspace_bytes(bh, n, masked);  // V^T (K-major tf32 B) + mask bitmaps

@@ -205,6 +205,8 @@ cudaError_t launch_flash_tc(const void* q, const void* k, const void* v, void* o
                             void* workspace, cudaStream_t s);
 // workspace of launch_flash_tc with a tile mask (liveness bitmaps); unmasked needs none
 int64_t flash_mask_workspace_bytes(int n);
+// unmasked fused 16-bit path: partial results of the split last round (flash_tc.cu SplitPlan)
+int64_t flash_split_workspace_bytes(int64_t bh, int n);
 // block-mask step skipping in the two-set fused kernels (flash_tc.cu): n % 256 == 0, n <= 32768
 bool flash_mask_two_set_ok(int n);
 int flash_mask_smem_bytes(int n);

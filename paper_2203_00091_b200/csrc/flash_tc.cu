@@ -45,6 +45,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <type_traits>
 
 #include "flash_common.cuh"
@@ -82,6 +83,22 @@ constexpr int TM_E = TM_O + 2 * HD;  // PST x 4 metadata columns
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kSumLimit = 256.0f;  // a quarter-tile partial sum above 2^8 triggers a shift update
 }  // namespace
+
+// Split of the last round (two-set kernel, unmasked): `items` equal items on G persistent CTAs
+// leave items % G of them for a last round in which the other CTAs idle (c2: 768 items on 148
+// SMs = 5.19 rounds, 14 % of the kernel).  Those `rem` items are cut along the keys into
+// `parts` contiguous tile ranges, one per CTA; parts 1.. leave their unnormalised O, shift and
+// row sum in the workspace behind a flag holding the launch's token (so no memset is needed:
+// a reused workspace holds older tokens) and part 0 merges them:
+// O = sum_p 2^(m_p - M) O_p / sum_p 2^(m_p - M) l_p, M = max_p m_p.
+struct SplitPlan {
+  int rounds = 0;   // whole rounds: unit k < rounds of CTA b is item k * G + b
+  int rem = 0;      // items of the last round
+  int parts = 1;    // key ranges per last-round item (1: no split)
+  unsigned long long token = 0;   // per launch: a part's flag holds it once its data is written
+  float* part_ws = nullptr;       // [rem][2 halves][8 warps][parts][34][32 lanes]
+  unsigned long long* counters = nullptr;  // flags [rem][2 halves][8 warps][parts]
+};
 
 // One quarter-tile of one row: 8 groups of 4 scores s[] in key order.  Prunes 2:4 (reference
 // rule), exponentiates the kept half against the shift `mlog` (= m * c), packs P, builds the
@@ -144,7 +161,7 @@ template <typename T, int HALVES, bool PAIRS, bool MASKED, bool DUMP>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     dfss_flash_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_v, T* __restrict__ out, float scale, int bh, int n,
-                      uint32_t two, FlashDump dump, TileMask tmask) {
+                      uint32_t two, FlashDump dump, TileMask tmask, SplitPlan /*two-set kernel only*/) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + SMEM_BAR);
@@ -488,17 +505,86 @@ __device__ unsigned long long* g_flash_trace = nullptr;
     if (trace && (it_) < 2 && (t_) < 64)                                                           \
       trace[((((slot) * 2 + (it_)) * 64 + (t_)) * 2 + (h_))] = clock64();                          \
   } while (0)
+// per-CTA unit timeline: [CTA < 148][unit < 16][event < 8] after the CTA-0 trace
+#define UTRACE(k_, ev_)                                                                                  \
+  do {                                                                                                   \
+    if (g_flash_trace && blockIdx.x < 148 && (k_) < 16)                                                  \
+      g_flash_trace[16 * 2 * 64 * 2 + ((blockIdx.x * 16 + (k_)) * 8 + (ev_))] = clock64();               \
+  } while (0)
 #else
 #define FTRACE(slot, it_, t_, h_) \
   do {                            \
   } while (0)
+#define UTRACE(k_, ev_) \
+  do {                  \
+  } while (0)
 #endif
+
+// One warp's part of a split last-round item (SplitPlan): parts 1.. leave their 32 rows x 32
+// columns of unnormalised O, the rows' shift (log2 units) and sum in the workspace and publish
+// them with a release store of the launch token; part 0 keeps its own in registers, waits for
+// the other parts' tokens (one lane per part, acquire loads) and merges.  Part 0 of an item
+// is the CTA with the lowest id; all parts hold (nearly) the same number of tiles.
+template <typename T>
+__device__ __forceinline__ void split_part_epilogue(const SplitPlan& sp, int ui, int h, int w, int part, uint32_t lane,
+                                                    const uint32_t (&o)[32], float mlog, float lsum, T* dst) {
+  const int64_t slot = ((int64_t)(ui * 2 + h) * 8 + w) * sp.parts;
+  unsigned long long* flags = sp.counters + slot;
+  if (part > 0) {
+    float* mine = sp.part_ws + (slot + part) * 34 * 32 + lane;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) __stcg(mine + j * 32, __uint_as_float(o[j]));
+    __stcg(mine + 32 * 32, mlog);
+    __stcg(mine + 33 * 32, lsum);
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flags + part), "l"(sp.token) : "memory");
+    }
+    return;
+  }
+  // part 0: wait for parts 1 .. parts-1 (lane p polls part p)
+  for (;;) {
+    bool ok = true;
+    if (lane > 0 && (int)lane < sp.parts) {
+      unsigned long long f;
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(flags + lane) : "memory");
+      ok = f == sp.token;
+    }
+    if (__all_sync(0xffffffffu, ok)) break;
+    __nanosleep(64);
+  }
+  __threadfence();
+  float m = mlog;
+  for (int p = 1; p < sp.parts; ++p) m = fmaxf(m, __ldcg(sp.part_ws + ((slot + p) * 34 + 32) * 32 + lane));
+  const float f0 = exp2f(mlog - m);
+  float acc[32], l = f0 * lsum;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] = f0 * __uint_as_float(o[j]);
+  for (int p = 1; p < sp.parts; ++p) {
+    const float* q = sp.part_ws + (slot + p) * 34 * 32 + lane;
+    float x[34];
+#pragma unroll
+    for (int j = 0; j < 34; ++j) x[j] = __ldcg(q + j * 32);
+    const float f = exp2f(x[32] - m);
+    l = fmaf(f, x[33], l);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = fmaf(f, x[j], acc[j]);
+  }
+  const float inv = 1.0f / l;
+  uint32_t pko[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) pko[j] = fpack2<T>(acc[2 * j] * inv, acc[2 * j + 1] * inv);
+  uint4* orow = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) orow[j] = make_uint4(pko[4 * j], pko[4 * j + 1], pko[4 * j + 2], pko[4 * j + 3]);
+}
 
 template <typename T, bool PAIRS, bool MASKED, bool DUMP>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     dfss_flash2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, T* __restrict__ out, float scale, int bh, int n,
-                       uint32_t two, FlashDump dump, TileMask tmask) {
+                       uint32_t two, FlashDump dump, TileMask tmask, SplitPlan sp) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + S2_BAR);
@@ -563,6 +649,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int info = s_order[p / bh], r0 = (info >> 8) & 255, m = info >> 16, o = p - r0 * bh;
     return (o / m) * iblocks + (s_order[r0 + o % m] & 255);
   };
+  // k-th unit of this CTA: an item, its tile range [t0, t1) and its part of a split last-round
+  // item (-1: the whole item); false past the CTA's last unit
+  auto unit_at = [&](int k, int& item, int& t0, int& t1, int& part) -> bool {
+    t0 = 0;
+    t1 = ntiles;
+    part = -1;
+    if (MASKED || sp.parts <= 1 || k < sp.rounds) {
+      const int pos = pos_at(k);
+      item = pos < items ? item_of(pos) : 0;
+      return pos < items;
+    }
+    if (k > sp.rounds || (int)blockIdx.x >= sp.rem * sp.parts) return false;
+    item = sp.rounds * (int)gridDim.x + (int)blockIdx.x / sp.parts;
+    part = (int)blockIdx.x % sp.parts;
+    t0 = part * ntiles / sp.parts;
+    t1 = (part + 1) * ntiles / sp.parts;
+    return true;
+  };
   // step-liveness words of an item's two halves for tiles [32 (t / 32), +32), refreshed every
   // 32 tiles; bit_u reads one as a warp vote so branches on it stay uniform in the converged
   // role warps
@@ -615,16 +719,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (lane == 0) {
       int ks = 0, vs = 0, it = 0;
       uint32_t kph = 0, vph = 0;
-      for (int kk_ = 0, pos = pos_at(0); pos < items; pos = pos_at(++kk_), ++it) {
-        const int item = item_of(pos);
+      int item, t0, t1, part;
+      for (int kk_ = 0; unit_at(kk_, item, t0, t1, part); ++kk_, ++it) {
         uint32_t lw0 = 0, lw1 = 0;
         const int b = item / iblocks, ib = item % iblocks;
         const int qs = it & 1;
+        UTRACE(kk_, 0);
         wait_role(&q_empty[qs], ((it >> 1) & 1) ^ 1);
+        UTRACE(kk_, 1);
         tc::mbar_arrive_expect_tx(&q_full[qs], 2 * Q_BYTES);
         tc::tma_load_3d(smem + S2_Q + (2 * qs) * Q_BYTES, &tm_q, &q_full[qs], 0, ib * 2 * BM, b);
         tc::tma_load_3d(smem + S2_Q + (2 * qs + 1) * Q_BYTES, &tm_q, &q_full[qs], 0, ib * 2 * BM + BM, b);
-        for (int t = 0; t < ntiles; ++t) {
+        for (int t = t0; t < t1; ++t) {
           live_words(ib, t, lw0, lw1);
           if (MASKED && !(((lw0 | lw1) >> (t & 31)) & 1u)) continue;
           wait_role(&k_empty[ks], kph ^ 1);
@@ -647,13 +753,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       constexpr uint32_t idesc_s = tc::instr_desc(fmt, BM, BN, false, false, false);
       int ks = 0, it = 0, sb = 0;
       uint32_t kph = 0, sph = 0;
-      for (int kk_ = 0, pos = pos_at(0); pos < items; pos = pos_at(++kk_), ++it) {
-        const int item = item_of(pos);
+      int item, t0, t1, part;
+      for (int kk_ = 0; unit_at(kk_, item, t0, t1, part); ++kk_, ++it) {
         uint32_t lw0 = 0, lw1 = 0;
         const int qs = it & 1;
         const int ib = item % iblocks;
         wait_role(&q_full[qs], (it >> 1) & 1);
-        for (int t = 0; t < ntiles; ++t) {
+        for (int t = t0; t < t1; ++t) {
           live_words(ib, t, lw0, lw1);
           const bool lv[2] = {bit_u(lw0, t), bit_u(lw1, t)};
           if (MASKED && !lv[0] && !lv[1]) continue;
@@ -693,8 +799,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       constexpr uint32_t idesc_pv = tc::instr_desc(fmt, BM, HD, false, true, true);
       int vs = 0, it = 0;
       uint32_t vph = 0, gcount = 0, pbits = 0;  // live steps so far (both halves); p_full phase per slot
-      for (int kk_ = 0, pos = pos_at(0); pos < items; pos = pos_at(++kk_), ++it) {
-        const int item = item_of(pos);
+      int item, t0, t1, part;
+      for (int kk_ = 0; unit_at(kk_, item, t0, t1, part); ++kk_, ++it) {
         uint32_t lw0 = 0, lw1 = 0;
         const int ib = item % iblocks;
         // O_h free (previous item drained) is awaited only before the first PV MMA of the item --
@@ -707,7 +813,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           o_free = true;
         };
         bool first = true;  // first live step of this half-item initialises O_h
-        for (int t = 0; t < ntiles; ++t) {
+        for (int t = t0; t < t1; ++t) {
           live_words(ib, t, lw0, lw1);
           const bool l0 = bit_u(lw0, t), l1 = bit_u(lw1, t);
           if (MASKED && !l0 && !l1) continue;  // tile not loaded
@@ -792,12 +898,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     };
     // ---- epilogue of a finished item: O_h / row sum; this warp writes columns [32 pr, +32) of its rows
     bool pend = false;
-    int pend_b = 0, pend_ib = 0, pend_it = 0;
-    float pend_l = 0.f;
+    int pend_b = 0, pend_ib = 0, pend_it = 0, pend_item = 0, pend_part = -1;
+    float pend_l = 0.f, pend_m = 0.f;
     auto epilogue = [&]() {
       rsum[pr * BM + r] = pend_l;
       tc::named_bar_sync(pbar, 64);
-      const float inv = 1.0f / (rsum[r] + rsum[BM + r]);
+      const float lsum = rsum[r] + rsum[BM + r];
+      const float inv = 1.0f / lsum;
       tc::named_bar_sync(pbar, 64);
       tc::mbar_wait(&o_full[h], pend_it & 1);
       tc::tc_fence_after();
@@ -807,11 +914,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&o_empty[h]);
+      const int64_t row = (int64_t)pend_b * n + (pend_ib * 2 + h) * BM + r;
+      if (!MASKED && pend_part >= 0) {
+        pend = false;
+        split_part_epilogue<T>(sp, pend_item - sp.rounds * (int)gridDim.x, h, (int)(warp & 7), pend_part, lane, o,
+                               pend_m, lsum, out + row * HD + 32 * pr);
+        return;
+      }
       uint32_t pko[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j)
         pko[j] = fpack2<T>(__uint_as_float(o[2 * j]) * inv, __uint_as_float(o[2 * j + 1]) * inv);
-      const int64_t row = (int64_t)pend_b * n + (pend_ib * 2 + h) * BM + r;
       uint4* orow = reinterpret_cast<uint4*>(out + row * HD + 32 * pr);
 #pragma unroll
       for (int j = 0; j < 4; ++j) orow[j] = make_uint4(pko[4 * j], pko[4 * j + 1], pko[4 * j + 2], pko[4 * j + 3]);
@@ -825,14 +938,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     };
     uint32_t cw = cword(pos_at(0));
     const uint32_t word_sel = (lane & 8) ? 0x3276u : 0x5410u;
-    for (int kk_ = 0, pos = pos_at(0); pos < items; pos = pos_at(++kk_), ++it) {
-        const int item = item_of(pos);
-        uint32_t lw0 = 0, lw1 = 0;
+    int item, t0, t1, part;
+    for (int kk_ = 0; unit_at(kk_, item, t0, t1, part); ++kk_, ++it) {
+      uint32_t lw0 = 0, lw1 = 0;
       const int b = item / iblocks, ib = item % iblocks;
       const uint32_t cwn = cword(pos_at(kk_ + 1));
       float mlog = 0.f, l0 = 0.f, l1 = 0.f;
       bool first = true;  // first live step of this half-item: establishes the shift
-      for (int t = 0; t < ntiles; ++t) {
+      for (int t = t0; t < t1; ++t) {
         live_words(ib, t, lw0, lw1);
         const bool lv0 = bit_u(lw0, t), lv1 = bit_u(lw1, t);
         const uint32_t g = gcount + (h ? (uint32_t)lv0 : 0u);  // global live step
@@ -844,6 +957,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc::mbar_wait(&s_full[h * S2RING + slot], (sfbits >> slot) & 1);  // k-th use of (h, slot): parity k & 1
         sfbits ^= 1u << slot;
         if (tw) FTRACE(0, it, t, h);
+        if (tw && h == 0 && t == t0) UTRACE(kk_, 2);
         tc::tc_fence_after();
         bool anym = false;  // a chunk of this warp masked (uniform): the masked compute variant
         if (MASKED) {
@@ -931,6 +1045,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         first = false;
         if (pend) epilogue();  // previous item's output (first live step only)
       }
+      if (tw && h == 0) UTRACE(kk_, 3);
       // the epilogue of this item runs after step 0 of the next one (below), so the wait for
       // the item's last PV overlaps that step instead of idling the set at every item boundary
       if (pend) epilogue();  // the previous item's, if this item had no live step for this set
@@ -939,9 +1054,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       pend_ib = ib;
       pend_it = it;
       pend_l = l0 + l1;
+      pend_m = mlog;
+      pend_item = item;
+      pend_part = part;
       cw = cwn;
     }
+    if (tw && h == 0) UTRACE(15, 4);
     if (pend) epilogue();
+    if (tw && h == 0) UTRACE(15, 5);
     if (threadIdx.x == 0) FTRACE(15, 1, 0, 0);  // CTA end
     tc::tc_fence_before();
     __syncthreads();
@@ -1022,6 +1142,46 @@ bool tc_flash_supported(int gs, int dtype, int n, int d) {
 
 #endif  // DFSS_FLASH_DUMP_TU
 
+unsigned long long next_split_token();
+
+// Last-round split of the two-set kernel for bh heads of n keys on `sms` persistent CTAs
+// (SplitPlan); workspace bytes in *bytes (0: no split).
+static SplitPlan split_plan(int64_t bh, int n, int sms, int64_t* bytes) {
+  SplitPlan sp;
+  *bytes = 0;
+  if (n % (2 * BM) != 0 || bh <= 0) return sp;
+  const int64_t items = bh * (n / (2 * BM));
+  const int64_t g = items < sms ? items : sms;
+  const int64_t rem = items % g;
+  const int ntiles = n / BN;
+  // >= 4 tiles per part: a part's epilogue (publish / merge through L2) costs about one tile
+  // of work, so 1-tile parts (c2: 28 items x 4 parts) measured slower than no split
+  const int64_t parts = rem ? std::min<int64_t>(ntiles / 4, g / rem) : 1;
+  if (parts < 2 || items / g > (1 << 20)) return sp;
+  sp.rounds = (int)(items / g);
+  sp.rem = (int)rem;
+  sp.parts = (int)parts;
+  const int64_t part_bytes = (rem * 2 * 8 * parts * 34 * 32 * 4 + 255) / 256 * 256;
+  *bytes = part_bytes + (rem * 2 * 8 * parts * 8 + 255) / 256 * 256;
+  return sp;
+}
+
+#ifndef DFSS_FLASH_DUMP_TU
+// one token per launch of any instantiation (the counters of a reused workspace may hold the
+// previous launch's token; a per-instantiation count would repeat across instantiations)
+unsigned long long next_split_token() {
+  static std::atomic<unsigned long long> launches{0};
+  return (++launches) & ((1ull << 56) - 1);
+}
+
+// workspace of the unmasked fused 16-bit path: the last-round split's partial results (SplitPlan)
+int64_t flash_split_workspace_bytes(int64_t bh, int n) {
+  int64_t bytes = 0;
+  split_plan(bh, n, device_sms(current_device()), &bytes);
+  return bytes;
+}
+#endif
+
 template <typename T, bool PAIRS, bool MASKED, bool DUMP>
 static cudaError_t flash_launch_typed(const void* q, const void* k, const void* v, void* out, float scale, int64_t bh,
                                       int n, TileMask tmask, void* workspace, FlashDump dump, cudaStream_t s) {
@@ -1041,6 +1201,17 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
   if (smem_total > 227 * 1024) return cudaErrorNotSupported;
   if (MASKED && two_set) prepare_mask_bits(tmask, n, workspace, s);
   const int dev = current_device();
+  SplitPlan sp;
+  if (two_set && !MASKED && workspace) {
+    int64_t split_bytes = 0;
+    sp = split_plan(bh, n, device_sms(dev), &split_bytes);
+    if (split_bytes) {
+      sp.token = next_split_token();
+      sp.part_ws = (float*)workspace;
+      sp.counters = (unsigned long long*)((char*)workspace + split_bytes -
+                                          ((int64_t)sp.rem * 2 * 8 * sp.parts * 8 + 255) / 256 * 256);
+    }
+  }
   static std::atomic<uint64_t> attr1{0}, attr2{0};
   cudaError_t e = set_max_smem_once((const void*)kern, two_set ? attr2 : attr1, dev);
   if (e != cudaSuccess) return e;
@@ -1051,14 +1222,14 @@ static cudaError_t flash_launch_typed(const void* q, const void* k, const void* 
   // bring-up timeline (tools/trace_flash.py): DFSS_FLASH_TRACE=<file> in trace builds only
   static const char* trace_file = getenv("DFSS_FLASH_TRACE");
   unsigned long long* trace = nullptr;
-  const size_t trace_n = 16 * 2 * 64 * 2;
+  const size_t trace_n = 16 * 2 * 64 * 2 + 148 * 16 * 8;
   if (trace_file && two_set) {
     cudaMalloc(&trace, trace_n * 8);
     cudaMemset(trace, 0, trace_n * 8);
     cudaMemcpyToSymbol(g_flash_trace, &trace, sizeof(trace));
   }
 #endif
-  kern<<<grid, NUM_THREADS, smem_total, s>>>(tq, tk, tv, (T*)out, scale, (int)bh, n, 2u, dump, tmask);
+  kern<<<grid, NUM_THREADS, smem_total, s>>>(tq, tk, tv, (T*)out, scale, (int)bh, n, 2u, dump, tmask, sp);
 #ifdef DFSS_FLASH_TRACE_BUILD
   if (trace) {
     cudaStreamSynchronize(s);

@@ -46,16 +46,29 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _flags_stamp(obj: str) -> str:
+    return obj + ".flags"
+
+
 def _compile(src: str, force: bool) -> str:
     obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
-    if force or _stale(obj, [src] + _headers()):
-        # DFSS_NVCC_EXTRA: extra nvcc flags for bring-up builds (e.g. -DDFSS_FLASH_TRACE_BUILD)
-        cmd = [nvcc(), *NVCC_FLAGS, *os.environ.get("DFSS_NVCC_EXTRA", "").split(), "-c", src, "-o", obj]
+    # DFSS_NVCC_EXTRA: extra nvcc flags for bring-up builds (e.g. -DDFSS_FLASH_TRACE_BUILD)
+    cmd = [nvcc(), *NVCC_FLAGS, *os.environ.get("DFSS_NVCC_EXTRA", "").split(), "-c", src, "-o", obj]
+    # the object records the exact command it was built with: a flag change (a trace build
+    # switched on or off) rebuilds it even when no source is newer
+    stamp = " ".join(cmd)
+    try:
+        same_flags = open(_flags_stamp(obj)).read() == stamp
+    except OSError:
+        same_flags = False
+    if force or not same_flags or _stale(obj, [src] + _headers()):
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{res.stdout}\n{res.stderr}")
         if res.stderr.strip():
             sys.stderr.write(res.stderr)
+        with open(_flags_stamp(obj), "w") as f:
+            f.write(stamp)
     return obj
 
 

@@ -22,7 +22,7 @@ spmm_gather and gemm_abt return bitwise the numba results and the softmaxes diff
 exp (<= 1 ulp).
 
 To plug it in, copy this file to ``nmattn/_kernels_cuda.py`` and add ``"cuda"`` to
-``backend._VALID`` (INTEGRATION.md §2 shows the three-line diff); ``paper_2203_00091_b200`` must be
+``backend._VALID`` (INTEGRATION.md §1 shows the one-line diff); ``paper_2203_00091_b200`` must be
 importable and a B200 present.  There is no CPU fallback: without the library or a device every
 call raises.
 """

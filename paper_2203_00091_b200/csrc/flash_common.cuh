@@ -60,7 +60,11 @@ __device__ __forceinline__ bool bar_any(uint32_t id, uint32_t count, bool pred) 
 }
 
 // role-warp wait: try_wait with a suspend-time hint (the waiting warp yields its issue slots)
+#ifdef DFSS_EXP_ROLE_SPIN  // timing experiment: role warps spin on try_wait without a suspend hint
+__device__ __forceinline__ void wait_role(uint64_t* bar, uint32_t parity) { tc::mbar_wait(bar, parity); }
+#else
 __device__ __forceinline__ void wait_role(uint64_t* bar, uint32_t parity) { tc::mbar_wait_sleep(bar, parity); }
+#endif
 
 // Parity dump of the fused kernels (DUMP instantiations only, dfss_nm_attention_dump): the
 // post-scale fp32 scores every prune compared, [bh, n, n] in true key order, and the metadata

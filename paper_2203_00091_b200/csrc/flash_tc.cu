@@ -117,9 +117,21 @@ struct SplitPlan {
 template <typename T, bool PAIRS>
 __device__ __forceinline__ void prune_exp_tile(const uint32_t (&s)[32], float c, float mlog, uint32_t two,
                                                uint32_t (&pk)[8], uint32_t& W, float& lt0, float& lt1) {
+#ifdef DFSS_EXP_NO_PRUNE  // timing experiment: no selection, no exp (results invalid)
+  W = 0x44444444u ^ (s[0] & 0x11111111u);
+  lt0 = __uint_as_float(s[1]) * 0.f;
+  lt1 = 0.f;
+#pragma unroll
+  for (int g = 0; g < 8; ++g) pk[g] = s[4 * g] ^ s[4 * g + 2];
+  return;
+#endif
   W = 0x88888888u;
   lt0 = 0.f;
   lt1 = 0.f;
+  // 2:4 metadata in float arithmetic on the otherwise idle FMA-lite pipe: nibble - 8 of groups
+  // 0-3 / 4-7 accumulated exactly as integers into 2^23 + 0x8888 (ulp 1), low halves merged by
+  // one PRMT at the end (tools/epi_probe.cu: -12 % against sign bits by IMAD.HI + SEL chains)
+  float wf[2] = {8388608.f + 34952.f, 8388608.f + 34952.f};
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
     const float v0 = __uint_as_float(s[4 * g + 0]);
@@ -131,24 +143,29 @@ __device__ __forceinline__ void prune_exp_tile(const uint32_t (&s)[32], float c,
     // test_flash_tie_lattice_and_zero_queries), so (-0) - (+0) cannot occur and the
     // differences need no canonicalisation.
     const float d01 = v0 - v1, d23 = v2 - v3;
-    // sign bits: IMAD.HI on the FMA pipe for 2:4 (the ALU pipe is the busy one there), SHF on
-    // the otherwise idle ALU pipe for 1:2 (there the FMA pipe and MUFU are the busy ones)
-    const uint32_t a = PAIRS ? __float_as_uint(d01) >> 31 : sign_bit(d01, two);
-    const uint32_t b = PAIRS ? __float_as_uint(d23) >> 31 : sign_bit(d23, two);
     const float w01 = fmaxf(v0, v1), w23 = fmaxf(v2, v3);
     float lo = w01, hi = w23;
-    // nibble - 8: 0x4 -> -4, 0xE -> 6, mixed 8 + a + 4b -> a + 4b
-    int nib = (int)(a + 4u * b);
-    if (!PAIRS) {
+    if (PAIRS) {
+      // sign bits on the otherwise idle ALU pipe (1:2 is FMA / MUFU-bound); nibble 8 + a + 4b
+      const uint32_t a = __float_as_uint(d01) >> 31, b = __float_as_uint(d23) >> 31;
+      W += (a + 4u * b) * (1u << (4 * g));
+    } else {
       const float l01 = fminf(v0, v1), l23 = fminf(v2, v3);
       const bool keep01 = l01 >= w23;  // lower-index loser vs higher-index winner
       const bool keep23 = l23 > w01;   // higher-index loser must strictly beat the winner
       lo = keep01 ? v0 : (keep23 ? v2 : w01);
       hi = keep01 ? v1 : (keep23 ? v3 : w23);
-      nib = keep23 ? 6 : nib;
-      nib = keep01 ? -4 : nib;
+      // a = [v1 > v0], b = [v3 > v2] as exact 0 / 1 floats: sat(d * -2^127 * 2^127) is 1 for
+      // every d < 0 down to the smallest subnormal and 0 for d >= 0 (ties: d = +0 -> lower index)
+      const float fa = __saturatef(__fmul_rn(d01, -1.7014118e38f) * 1.7014118e38f);
+      const float fb = __saturatef(__fmul_rn(d23, -1.7014118e38f) * 1.7014118e38f);
+      // nibble - 8: 0x4 -> -4, 0xE -> 6, mixed 8 + a + 4b -> a + 4b
+      float n = fmaf(fb, 4.f, fa);
+      n = keep23 ? 6.f : n;
+      n = keep01 ? -4.f : n;
+      wf[g >> 2] = fmaf(n, (float)(1 << (4 * (g & 3))), wf[g >> 2]);
+      if (g == 7) W = __byte_perm(__float_as_uint(wf[0]), __float_as_uint(wf[1]), 0x5410);
     }
-    W += (uint32_t)nib * (1u << (4 * g));
     float x0, x1;
     fma2s(lo, hi, c, -mlog, x0, x1);
     const float p0 = fex2(x0), p1 = fex2(x1);
@@ -778,7 +795,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int kk = 0; kk < HD / 16; ++kk) {
               const uint64_t ad = tc::smem_desc(q_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
               const uint64_t bd = tc::smem_desc(k_addr + kk * 32, 16, 1024, tc::kSwizzle128B);
+#ifndef DFSS_EXP_NO_MMA
               tc::mma_f16_ss_w(tmem_base + sb * BN, ad, bd, idesc_s, kk > 0 ? 1u : 0u);
+#endif
             }
             tc::mma_commit_w(&s_full[h * S2RING + sb]);
             if (lane == 0) FTRACE(5, it, t, h);
@@ -838,8 +857,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const uint64_t bd = tc::smem_desc(v_addr + q * 32 * 128, V_BYTES, 1024, tc::kSwizzle128B);
+#ifndef DFSS_EXP_NO_MMA
             tc::mma_sp_f16_ts_w(tmem_base + T2_O + h * HD, s_col + 32 * q + 16, bd, s_col + 32 * q, idesc_pv,
                                 (!first || q > 0) ? 1u : 0u);
+#endif
           }
           first = false;
           tc::mma_commit_w(&s_free[slot]);
@@ -954,7 +975,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ++hcount;
         const uint32_t slot = g % S2RING;
         scol = lane_base + slot * BN + 64 * pr;
+#ifndef DFSS_EXP_NO_SWAIT
         tc::mbar_wait(&s_full[h * S2RING + slot], (sfbits >> slot) & 1);  // k-th use of (h, slot): parity k & 1
+#endif
         sfbits ^= 1u << slot;
         if (tw) FTRACE(0, it, t, h);
         if (tw && h == 0 && t == t0) UTRACE(kk_, 2);
@@ -999,7 +1022,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // (W[0] & W[1]) == ~0 never holds (no nibble is 0xF); it makes the vote consume the
           // metadata so ptxas builds W before the branch instead of keeping every group's
           // keep predicates / operands alive across it (which spilled to local memory)
+#ifdef DFSS_EXP_NO_VOTE
+          if (pass > 0 || first || !((W[0] & W[1]) == ~0u && lt0 + lt1 > 1e30f)) break;
+#else
           if (pass > 0 || first || !bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit) || (W[0] & W[1]) == ~0u)) break;
+#endif
           // ---- slow path (both warps of the pair): raise the shift to the row maximum,
           // rescale O_h and the sums once every PV into O_h so far (this half's tile t-1) retired.
           // (pv_done[h] completes once per tile of this half and cannot run ahead of this set,

@@ -17,6 +17,8 @@ import os as _os
 MODE = _os.environ.get("DFSS_MODE", "2:4")
 for name, (b, h, n, dt) in {"c2": (32, 12, 512, torch.bfloat16), "c3": (16, 16, 1024, torch.float16),
                              "c4": (8, 12, 4096, torch.bfloat16)}.items():
+    if _os.environ.get("CONFIGS") and name not in _os.environ["CONFIGS"].split(","):
+        continue
     q, k, v = (torch.randn(b, h, n, 64, device="cuda", dtype=dt) for _ in range(3))
     out = torch.empty_like(q)
     ws = torch.empty(dfss.workspace_bytes(MODE, dt, b * h, n, 64), dtype=torch.uint8, device="cuda")

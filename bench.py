@@ -121,48 +121,102 @@ def config_block(cfg_name: str, ws: int, scaling: str, heads_per_rank) -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled every 50 ms during the timed region,
+    through NVML in-process (the library nvidia-smi reads; a process spawned per sample would
+    land in the timed region), on the device torch runs on (matched by UUID).  Falls back to
+    one `nvidia-smi -lms 200` process when pynvml is missing."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
-    def __init__(self, index: int):
-        self.index = index
-        self.samples = []
+    def __init__(self, device: torch.device):
+        self.device = device
+        self.samples = []  # (sm_mhz, sm_max_mhz, watts, reason bits)
         self._stop = threading.Event()
         self._t = None
+        self._nv = None
+        self._h = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            uuid = str(torch.cuda.get_device_properties(device).uuid)
+            for i in range(pynvml.nvmlDeviceGetCount()):
+                h = pynvml.nvmlDeviceGetHandleByIndex(i)
+                u = pynvml.nvmlDeviceGetUUID(h)
+                u = u.decode() if isinstance(u, bytes) else u
+                if u.replace("GPU-", "") == uuid.replace("GPU-", ""):
+                    self._nv, self._h = pynvml, h
+                    break
+        except Exception:
+            self._nv = None
 
     def _run(self):
+        nv, h = self._nv, self._h
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                     nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM),
+                                     nv.nvmlDeviceGetPowerUsage(h) / 1000.0,
+                                     int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))))
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.05)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        else:
+            self._p = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE, text=True)
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         if self._t:
-            self._t.join(timeout=6)
+            self._t.join(timeout=2)
+        elif getattr(self, "_p", None):
+            self._p.terminate()
+            for line in self._p.communicate(timeout=5)[0].splitlines():
+                f = [x.strip() for x in line.split(",")]
+                try:
+                    self.samples.append((float(f[0]), float(f[1]), float(f[2]), int(f[3], 16)))
+                except (ValueError, IndexError):
+                    pass
 
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower().startswith("active")})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        bits = 0
+        for smp in self.samples:
+            bits |= smp[3]
+        return {"sm_mhz": float(np.median([smp[0] for smp in self.samples])),
+                "sm_max_mhz": float(max(smp[1] for smp in self.samples)),
+                "power_w": round(float(np.median([smp[2] for smp in self.samples])), 1),
+                "reasons": sorted(k for k, b in self.REASONS.items() if bits & b),
+                "samples": len(self.samples), "source": "nvml" if self._nv is not None else "nvidia-smi -lms 200"}
+
+
+def soak(fn, seconds: float | None = None):
+    """Run fn back to back for `seconds` (DFSS_BENCH_SOAK_S, default 1.5): a 1 kW B200 reaches its
+    sustained (power-capped) clock within about a second of full load, and every arm -- DFSS and
+    the dense comparators -- is timed in that same state (tools/time_soak.py: both settle at
+    the sw_power_cap clock, SDPA lower than DFSS)."""
+    seconds = float(os.environ.get("DFSS_BENCH_SOAK_S", "1.5")) if seconds is None else seconds
+    t_end = time.perf_counter() + seconds
+    while time.perf_counter() < t_end:
+        for _ in range(20):
+            fn()
+        torch.cuda.synchronize()
+
+
+def soaked_steps(fn, steps, warmup, flush, device):
+    """soak, then time_steps, under one clock sampler: (per-step ms, clocks)."""
+    with ClockSampler(device) as clk:
+        soak(fn)
+        times = time_steps(fn, steps, warmup, flush)
+    return times, clk.summary()
 
 
 def time_steps(fn, steps, warmup, flush=None):
@@ -274,17 +328,8 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True, info=Tr
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
-    smi_index = int(cvd.split(",")[local]) if cvd and cvd.split(",")[local].strip().isdigit() else local
-    with ClockSampler(smi_index) as clk:
-        # soak: keep the GPU busy on the same step for >= 1.5 s so the sampler sees the
-        # clocks under this load, then the K timed steps (same sampler window)
-        t_end = time.perf_counter() + float(os.environ.get("DFSS_BENCH_SOAK_S", "1.5"))
-        while time.perf_counter() < t_end:
-            for _ in range(20):
-                step()
-            torch.cuda.synchronize()
-        times = time_steps(step, args.steps, args.warmup, flush)
+    # soak (sustained-load clocks, see soak()), then the K timed steps, one sampler window
+    times, clocks = soaked_steps(step, args.steps, args.warmup, flush, device)
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
@@ -293,7 +338,7 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True, info=Tr
         torch.distributed.all_reduce(total_ms, op=torch.distributed.ReduceOp.MAX)
     ms_per_step = float(total_ms.item()) / args.steps
     value = 4.0 * n * n * d * total_bh / (ms_per_step * 1e-3) / 1e12  # all ranks' heads / max-rank time
-    res = {"ms_per_step": ms_per_step, "value": value, "clocks": clk.summary(), "bh_local": bh, "path": path,
+    res = {"ms_per_step": ms_per_step, "value": value, "clocks": clocks, "bh_local": bh, "path": path,
            "launches_per_step": LAUNCHES[path] if bh else 0, "lo": lo, "hi": hi}
     if not report_extra:
         return res, (q, k, v, out, lo, hi)
@@ -311,14 +356,16 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True, info=Tr
     def dense_sdpa():
         return torch.nn.functional.scaled_dot_product_attention(qd, kd, vd)
 
-    base = {}
+    base, base_clk = {}, {}
     for name, fn in (("cublas_unfused", dense_unfused), ("sdpa", dense_sdpa)):
-        try:
-            base[name] = float(np.mean(time_steps(fn, max(3, args.steps), 2, flush)))
+        try:  # same protocol as the DFSS step: soaked to the sustained clock, L2 flushed per step
+            tt, base_clk[name] = soaked_steps(fn, max(3, args.steps), 2, flush, device)
+            base[name] = float(np.mean(tt))
         except Exception as ex:  # e.g. OOM for huge unfused scores
             base[name] = None
             res.setdefault("baseline_errors", {})[name] = str(ex)[:120]
     res["dense_ms"] = base
+    res["dense_clocks"] = base_clk
     res["speedup_vs_dense"] = {k_: (round(t / ms_per_step, 3) if t else None) for k_, t in base.items()}
 
     # ---- staged reference-shaped kernels on the same shard (informational: sddmm_prune ->
@@ -449,7 +496,7 @@ def block_mask_measure(device, steps=5):
                      device=device)
     flush_buf = torch.empty(256 * 2**20, dtype=torch.uint8, device=device)
     flush = lambda: flush_buf.fill_(1)  # noqa: E731
-    t = lambda fn: float(np.mean(time_steps(fn, steps, 3, flush)))  # noqa: E731
+    t = lambda fn: float(np.mean(soaked_steps(fn, steps, 3, flush, device)[0]))  # noqa: E731
     res = {"workload": "c4 shape, 2:4 bf16, block-causal 128x128 BlockMask on 32x64 tiles",
            "live_step_fraction": round(float(keep[::4, ::2].mean()), 4),
            "dfss_unmasked_ms": round(t(lambda: dfss.dfss_attention(q, k, v, "2:4", out=out)), 4),
@@ -555,6 +602,7 @@ def main():
                                                                                  warmup=3), name, 1, 0, 0, device)
                     others[name] = {"ms_per_step": round(r2["ms_per_step"], 4), "tflops": round(r2["value"], 2),
                                     "speedup_vs_dense": r2["speedup_vs_dense"], "dense_ms": r2["dense_ms"],
+                                    "clocks": r2["clocks"], "dense_clocks": r2.get("dense_clocks"),
                                     "path": r2["path"], "gpu_launches_per_step": r2["launches_per_step"],
                                     "roofline": r2["roofline"],
                                     "parity_spot_check": parity_spot_check(name, q2, k2, v2, o2, lo2, hi2, hi2 - lo2)}
@@ -591,6 +639,7 @@ def main():
             "roofline": res["roofline"], "path": res["path"],
             "dense_ms": res["dense_ms"], "speedup_vs_dense": res["speedup_vs_dense"],
             "gpu_launches": res["launches_per_step"] * args.steps, "clocks": res["clocks"],
+            "dense_clocks": res.get("dense_clocks"),
         }
         if "staged_kernels_ms" in res:
             line["staged_kernels_ms"] = res["staged_kernels_ms"]

@@ -22,6 +22,12 @@ __device__ __forceinline__ uint32_t lop_or_orn(float a, float b, float c) {  // 
   return __float_as_uint(a) | ~__float_as_uint(b) | __float_as_uint(c);
 }
 
+__device__ __forceinline__ void mul2(float a0, float a1, float b0, float b1, float& d0, float& d1) {
+  asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
 __device__ __forceinline__ float fset_gt(float a, float b) {  // 1.0f if a > b else 0.0f
   float r;
   asm("set.gt.f32.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
@@ -44,6 +50,29 @@ __device__ __forceinline__ void prune(const uint32_t (&s)[32], float c, float ml
 #pragma unroll
   for (int gg = 0; gg < 8; ++gg) {
     const int g = (MODE == 2) ? 7 - gg : gg;  // funnel shifts build W from the top nibble down
+    if (MODE == 15) {
+      // registers hold (v0, v2, v1, v3): differences are one FADD2, the flag multiply one FMUL2
+      const float v0 = __uint_as_float(s[4 * g + 0]), v2 = __uint_as_float(s[4 * g + 1]);
+      const float v1 = __uint_as_float(s[4 * g + 2]), v3 = __uint_as_float(s[4 * g + 3]);
+      float d01, d23, m01, m23;
+      sub2(v0, v2, v1, v3, d01, d23);
+      mul2(d01, d23, -1.7014118e38f, -1.7014118e38f, m01, m23);
+      const float fa = __saturatef(m01 * 1.7014118e38f), fb = __saturatef(m23 * 1.7014118e38f);
+      const float w01 = fmaxf(v0, v1), w23 = fmaxf(v2, v3), l01 = fminf(v0, v1), l23 = fminf(v2, v3);
+      const bool keep01 = l01 >= w23, keep23 = l23 > w01;
+      const float lo = keep01 ? v0 : (keep23 ? v2 : w01);
+      const float hi = keep01 ? v1 : (keep23 ? v3 : w23);
+      float n = fmaf(fb, 4.f, fa);
+      n = keep23 ? 6.f : n;
+      n = keep01 ? -4.f : n;
+      wf[g >> 2] = fmaf(n, (float)(1 << (4 * (g & 3))), wf[g >> 2]);
+      if (g == 7) W = __byte_perm(__float_as_uint(wf[0]), __float_as_uint(wf[1]), 0x5410);
+      const float x0 = fmaf(lo, c, -mlog), x1 = fmaf(hi, c, -mlog);
+      const float p0 = fex2(x0), p1 = fex2(x1);
+      pk[g] = fpack2<T>(p0, p1);
+      add2(lt0, lt1, p0, p1, lt0, lt1);
+      continue;
+    }
     const float v0 = __uint_as_float(s[4 * g + 0]);
     const float v1 = __uint_as_float(s[4 * g + 1]);
     const float v2 = __uint_as_float(s[4 * g + 2]);
@@ -176,7 +205,10 @@ __global__ void __launch_bounds__(512, 1) k(int iters, long long* cyc, float c, 
 template <int MODE>
 __global__ void meta_k(const float* s_in, uint32_t* w_out) {
   uint32_t s[32];
-  for (int j = 0; j < 32; ++j) s[j] = __float_as_uint(s_in[threadIdx.x * 32 + j]);
+  for (int j = 0; j < 32; ++j) {
+    const int jj = MODE == 15 ? (j & ~3) | ((j & 3) == 1 ? 2 : (j & 3) == 2 ? 1 : (j & 3)) : j;
+    s[j] = __float_as_uint(s_in[threadIdx.x * 32 + jj]);
+  }
   uint32_t pk[8], W;
   float a, b;
   prune<MODE>(s, 1.f, 0.f, 2u, pk, W, a, b);
@@ -195,7 +227,7 @@ int main() {
                          "mixed nibble only (IMAD.HI)", "mixed nibble only (SHF)", "keep SELs only",
                          "sign bits only (IMAD.HI)", "float flags (FMUL.SAT) + FSEL", "FSET flags, float nibble (lite)",
                          "FSET a/b, FSEL keeps, float nibble", "FMUL.SAT a/b, FSEL keeps, float nibble",
-                         "1-FMUL.SAT a/b (unsafe), FSEL keeps, fl. nib"};
+                         "1-FMUL.SAT a/b (unsafe), FSEL keeps, fl. nib", "permuted regs: FADD2 + FMUL2 flags"};
   auto run = [&](auto kern, int mode) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int iters = 4096;
@@ -219,7 +251,7 @@ int main() {
     cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
     printf("%-46s %s %.0f cycles per (1 warp x 8 chunks) / SMSP\n", "production, 4 warps x 8 chunks", cudaGetErrorString(e), (double)h / 4096);
   }
-  run(k<0>, 0); run(k<1>, 1); run(k<2>, 2); run(k<3>, 3); run(k<5>, 5); run(k<6>, 6); run(k<7>, 7); run(k<8>, 8); run(k<9>, 9); run(k<10>, 10); run(k<11>, 11); run(k<12>, 12); run(k<13>, 13); run(k<14>, 14);
+  run(k<0>, 0); run(k<1>, 1); run(k<2>, 2); run(k<3>, 3); run(k<5>, 5); run(k<6>, 6); run(k<7>, 7); run(k<8>, 8); run(k<9>, 9); run(k<10>, 10); run(k<11>, 11); run(k<12>, 12); run(k<13>, 13); run(k<14>, 14); run(k<15>, 15);
   // metadata equality of the funnel-shift form
   float* ds; uint32_t *w0, *w2;
   cudaMalloc(&ds, 512 * 32 * 4); cudaMalloc(&w0, 512 * 4); cudaMalloc(&w2, 512 * 4);
@@ -240,5 +272,6 @@ int main() {
   check(meta_k<11>, "FSET float nibble");
   check(meta_k<12>, "FSET + FSEL float nibble");
   check(meta_k<13>, "FMUL.SAT float nibble");
+  check(meta_k<15>, "permuted FADD2/FMUL2 float nibble");
   return 0;
 }

@@ -10,4 +10,4 @@ timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_
 fi
 timeout -s KILL 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_${TAG}.json 2> gpurun_out/bench_${TAG}.err; echo "bench rc=$?" >> gpurun_out/bench_${TAG}.err
 bash tools/prof_flash.sh ${TAG} > /dev/null 2>&1
-tail -3 gpurun_out/pytest_${TAG}.log gpurun_out/smoke_${TAG}.log gpurun_out/bench_${TAG}.err
+tail -n 3 gpurun_out/pytest_${TAG}.log gpurun_out/smoke_${TAG}.log gpurun_out/bench_${TAG}.err

@@ -11,6 +11,7 @@ from __future__ import annotations
 import concurrent.futures as cf
 import glob
 import os
+import re
 import shutil
 import subprocess
 import sys
@@ -39,6 +40,24 @@ def _headers() -> list[str]:
     return glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
 
 
+def _includes(src: str, seen: set | None = None) -> list[str]:
+    """Files `src` pulls in with #include "..." (recursively, relative to its directory): an
+    object is stale when any of them changed -- flash_tc_dump.cu includes flash_tc.cu."""
+    seen = set() if seen is None else seen
+    out = []
+    try:
+        text = open(src).read()
+    except OSError:
+        return out
+    for m in re.finditer(r'^\s*#\s*include\s+"([^"]+)"', text, re.M):
+        f = os.path.normpath(os.path.join(os.path.dirname(src), m.group(1)))
+        if f not in seen and os.path.exists(f):
+            seen.add(f)
+            out.append(f)
+            out += _includes(f, seen)
+    return out
+
+
 def _stale(target: str, deps: list[str]) -> bool:
     if not os.path.exists(target):
         return True
@@ -61,7 +80,7 @@ def _compile(src: str, force: bool) -> str:
         same_flags = open(_flags_stamp(obj)).read() == stamp
     except OSError:
         same_flags = False
-    if force or not same_flags or _stale(obj, [src] + _headers()):
+    if force or not same_flags or _stale(obj, [src] + _headers() + _includes(src)):
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{res.stdout}\n{res.stderr}")

@@ -917,16 +917,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc::named_bar_sync(pbar, 64);
       return m * c;
     };
-    // ---- epilogue of a finished item: O_h / row sum; this warp writes columns [32 pr, +32) of its rows
+    auto chunk0_max = [&]() {
+      uint32_t s0[32];
+      tc::tmem_ld_32x32b_x32(scol - 64 * pr, s0);
+      tc::tmem_ld_wait(s0);
+      float mc = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) mc = fmaxf(mc, fmaxf(__uint_as_float(s0[j]), __uint_as_float(s0[j + 1])));
+      return mc * c;
+    };
+    // ---- epilogue of a finished item: O_h / row sum; this warp writes columns [32 pr, +32) of its rows.
+    // The row sums of the two warps of a pair are combined when the item ends (lsum, below);
+    // O_h is drained, normalised and stored during the next item's first live step, after its
+    // compute but BEFORE its P is published: that item's first PV overwrites O_h, so it (and with
+    // it the S ring) is never held up waiting for this epilogue (it was when the epilogue ran after
+    // the publication: ~2500 clk per item boundary, tools/trace_items.py).
     bool pend = false;
     int pend_b = 0, pend_ib = 0, pend_it = 0, pend_item = 0, pend_part = -1;
-    float pend_l = 0.f, pend_m = 0.f;
+    float pend_lsum = 0.f, pend_m = 0.f;
     auto epilogue = [&]() {
-      rsum[pr * BM + r] = pend_l;
-      tc::named_bar_sync(pbar, 64);
-      const float lsum = rsum[r] + rsum[BM + r];
-      const float inv = 1.0f / lsum;
-      tc::named_bar_sync(pbar, 64);
       tc::mbar_wait(&o_full[h], pend_it & 1);
       tc::tc_fence_after();
       uint32_t o[32];
@@ -936,12 +945,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&o_empty[h]);
       const int64_t row = (int64_t)pend_b * n + (pend_ib * 2 + h) * BM + r;
+      pend = false;
       if (!MASKED && pend_part >= 0) {
-        pend = false;
         split_part_epilogue<T>(sp, pend_item - sp.rounds * (int)gridDim.x, h, (int)(warp & 7), pend_part, lane, o,
-                               pend_m, lsum, out + row * HD + 32 * pr);
+                               pend_m, pend_lsum, out + row * HD + 32 * pr);
         return;
       }
+      const float inv = 1.0f / pend_lsum;
       uint32_t pko[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j)
@@ -949,7 +959,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint4* orow = reinterpret_cast<uint4*>(out + row * HD + 32 * pr);
 #pragma unroll
       for (int j = 0; j < 4; ++j) orow[j] = make_uint4(pko[4 * j], pko[4 * j + 1], pko[4 * j + 2], pko[4 * j + 3]);
-      pend = false;
     };
     // chunk-keep word `lane` of this warp's 32-row strip (cbits), next item's prefetched
     auto cword = [&](int pos_) -> uint32_t {
@@ -990,7 +999,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           cm[1] = !(w & 2u);
           anym = __any_sync(0xffffffffu, (~w & 3u) != 0);
         }
-        if (first) mlog = row_max();  // the shift starts at the row maximum of the item's first live tile
+        // the shift starts at the row maximum of the item's first live tile -- unmasked: of its
+        // first 32 columns only, read by both warps of the pair alike (no exchange, no barrier);
+        // a step whose sums then exceed the limit recomputes with the exact maximum (below)
+        if (first) mlog = MASKED ? row_max() : chunk0_max();
         uint32_t pk[2][8], W[2];
         float lt0 = 0.f, lt1 = 0.f;
         auto compute = [&](auto masked_variant) {
@@ -1025,8 +1037,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #ifdef DFSS_EXP_NO_VOTE
           if (pass > 0 || first || !((W[0] & W[1]) == ~0u && lt0 + lt1 > 1e30f)) break;
 #else
-          if (pass > 0 || first || !bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit) || (W[0] & W[1]) == ~0u)) break;
+          if (pass > 0 || (MASKED && first) || !bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit) || (W[0] & W[1]) == ~0u)) break;
 #endif
+          if (!MASKED && first) {  // estimated shift too low: exact row maximum, nothing accumulated yet
+            mlog = fmaxf(mlog, row_max());
+            continue;
+          }
           // ---- slow path (both warps of the pair): raise the shift to the row maximum,
           // rescale O_h and the sums once every PV into O_h so far (this half's tile t-1) retired.
           // (pv_done[h] completes once per tile of this half and cannot run ahead of this set,
@@ -1052,6 +1068,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         add2(l0, l1, lt0, lt1, l0, l1);
         if (tw) FTRACE(1, it, t, h);
+        // previous item's output, before this item's first P goes out (masked kernels: after it --
+        // their extra live state would spill around the epilogue here)
+        if (!MASKED && pend) epilogue();
         // P (8 columns of 16-bit pairs at 32q + 16) and the metadata word (column 32q) of each
         // chunk into this warp's own, already read S columns; rows r and r^8 trade metadata
         // halves (include/dfss.h): one PRMT with a lane-dependent selector
@@ -1070,17 +1089,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) tc::mbar_arrive(&p_full[h * S2RING + slot]);
         if (tw) FTRACE(2, it, t, h);
         first = false;
-        if (pend) epilogue();  // previous item's output (first live step only)
+        if (MASKED && pend) epilogue();
       }
       if (tw && h == 0) UTRACE(kk_, 3);
-      // the epilogue of this item runs after step 0 of the next one (below), so the wait for
-      // the item's last PV overlaps that step instead of idling the set at every item boundary
+      // the epilogue of this item runs in step 0 of the next one (above), so the wait for the
+      // item's last PV overlaps that step's compute instead of idling the set at the boundary
       if (pend) epilogue();  // the previous item's, if this item had no live step for this set
+      rsum[pr * BM + r] = l0 + l1;  // row sum over both warps of the pair
+      tc::named_bar_sync(pbar, 64);
+      pend_lsum = rsum[r] + rsum[BM + r];
+      tc::named_bar_sync(pbar, 64);
       pend = true;
       pend_b = b;
       pend_ib = ib;
       pend_it = it;
-      pend_l = l0 + l1;
       pend_m = mlog;
       pend_item = item;
       pend_part = part;

@@ -29,9 +29,15 @@ if os.environ.get("DFSS_FLASH_TRACE") is None:
             for h in range(2):
                 ev = {NAMES[s]: tr[s, it, t, h] - t0 for s in NAMES if tr[s, it, t, h] > 0}
                 print(f"item {it} t {t} h {h}: " + "  ".join(f"{k} {v}" for k, v in sorted(ev.items(), key=lambda x: x[1])))
-    base = u[u > 0].min()
+    base = u[0, 0, 0]
     for b in (0, 1, 147):
-        print(f"cta {b}: " + " | ".join(f"u{k} {[int(x - base) if x > 0 else -1 for x in u[b, k, :4]]}" for k in range(7)))
+        for k in range(1, 6):
+            e = u[b, k]
+            if e[5] > 0:
+                print(f"cta {b} unit {k} epilogue: o_full wait {e[4] - e[5]}  LDTM O {e[6] - e[4]}  normalise+store {e[7] - e[6]}"
+                      f"  | previous item's O_0 complete (PV issuer) at {u[b, k - 1, 1] - e[5]} rel. to epilogue start")
+    for b in (0, 1, 147):
+        print(f"cta {b}: " + " | ".join(f"u{k} {[int(x - base) if x > 0 else -1 for x in u[b, k, :8]]}" for k in range(7)))
     sys.exit(0)
 import torch  # noqa: E402
 

@@ -85,7 +85,41 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, 
   meta_b[(int64_t)((colh + cc * 32) >> 5) * 128 + row_blk] = word;
 }
 
+// 1:2 (codec.py:114-117: element 1 of a pair survives iff v1 > v0): the chunk's 16 pairs keep 16
+// values -- the same 16 per 32 columns as 2:4, so staging and the TMA store are unchanged -- and
+// their 16 nibbles (0x4 / 0xE) fill two meta_hw words (meta chunks of 8 pairs = 16 columns).
 template <typename T, bool DBG, bool RMAX>
+__device__ __forceinline__ void epi_chunk12(const uint32_t (&r)[32], float scale, int colh, int cc, int unit0,
+                                            uint8_t* stg, uint32_t lane, uint32_t* meta_b, int row_blk, float* dbg,
+                                            int64_t dbg_row, int m, float& mx) {
+  uint32_t packed[8];
+  uint32_t W[2] = {0u, 0u};
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {  // g: pairs 2g, 2g + 1
+    const float v0 = scale_canon(__uint_as_float(r[4 * g + 0]), scale);
+    const float v1 = scale_canon(__uint_as_float(r[4 * g + 1]), scale);
+    const float v2 = scale_canon(__uint_as_float(r[4 * g + 2]), scale);
+    const float v3 = scale_canon(__uint_as_float(r[4 * g + 3]), scale);
+    if (DBG) *reinterpret_cast<float4*>(dbg + dbg_row * m + colh + cc * 32 + 4 * g) = make_float4(v0, v1, v2, v3);
+    float k0, k1;
+    const uint32_t n0 = select12(v0, v1, k0), n1 = select12(v2, v3, k1);
+    if (RMAX) mx = fmaxf(mx, fmaxf(k0, k1));
+    packed[g] = pack2<T>(k0, k1);
+    W[g >> 2] += (n0 | (n1 << 4)) << (8 * (g & 3));
+  }
+  const int u0 = unit0, sw = lane & 7;
+  *reinterpret_cast<uint4*>(stg + lane * 128 + ((u0 ^ sw) << 4)) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+  *reinterpret_cast<uint4*>(stg + lane * 128 + (((u0 + 1) ^ sw) << 4)) =
+      make_uint4(packed[4], packed[5], packed[6], packed[7]);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t partner = __shfl_xor_sync(0xffffffffu, W[h], 8);
+    const uint32_t word = (lane & 8) ? ((partner >> 16) | (W[h] & 0xFFFF0000u)) : ((W[h] & 0xFFFFu) | (partner << 16));
+    meta_b[(int64_t)(((colh + cc * 32) >> 4) + h) * 128 + row_blk] = word;
+  }
+}
+
+template <typename T, int GS, bool DBG, bool RMAX>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     sddmm24_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_nz, uint32_t* __restrict__ meta, float scale, int bh,
@@ -194,7 +228,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int ew = warp - 4;
     const int quad = warp & 3;
     const int half = ew >> 2;
-    const int chunks = m / 32;  // meta chunks of 8 groups per row block
+    const int chunks = m / (8 * GS);  // meta chunks of 8 groups per row block
     uint8_t* stg_base = smem + SMEM_STG + ew * 2 * STG_BYTES;
     int acc = 0, sb = 0;
     uint32_t aph = 0;
@@ -218,18 +252,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int64_t drow = (int64_t)b * n + grow;
           uint32_t ra[32], rb[32];
           // chunk cc+1 is in flight while cc is pruned
+          auto chunk = [&](const uint32_t (&rr)[32], int cc) {
+            if constexpr (GS == 4)
+              epi_chunk<T, DBG, RMAX>(rr, scale, colh, cc, 2 * cc, stg, lane, meta_b, row_blk, dbg, drow, m, mx, two);
+            else
+              epi_chunk12<T, DBG, RMAX>(rr, scale, colh, cc, 2 * cc, stg, lane, meta_b, row_blk, dbg, drow, m, mx);
+          };
           tc::tmem_ld_32x32b_x32(tbase, ra);
           tc::tmem_ld_wait(ra);
           tc::tmem_ld_32x32b_x32(tbase + 32, rb);
-          epi_chunk<T, DBG, RMAX>(ra, scale, colh, 0, 0, stg, lane, meta_b, row_blk, dbg, drow, m, mx, two);
+          chunk(ra, 0);
           tc::tmem_ld_wait(rb);
           tc::tmem_ld_32x32b_x32(tbase + 64, ra);
-          epi_chunk<T, DBG, RMAX>(rb, scale, colh, 1, 2, stg, lane, meta_b, row_blk, dbg, drow, m, mx, two);
+          chunk(rb, 1);
           tc::tmem_ld_wait(ra);
           tc::tmem_ld_32x32b_x32(tbase + 96, rb);
-          epi_chunk<T, DBG, RMAX>(ra, scale, colh, 2, 4, stg, lane, meta_b, row_blk, dbg, drow, m, mx, two);
+          chunk(ra, 2);
           tc::tmem_ld_wait(rb);
-          epi_chunk<T, DBG, RMAX>(rb, scale, colh, 3, 6, stg, lane, meta_b, row_blk, dbg, drow, m, mx, two);
+          chunk(rb, 3);
         }
         tc::tc_fence_before();
         __syncwarp();
@@ -264,7 +304,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // ---------------------------------------------------------------- host side
 
 bool tc_sddmm_supported(int gs, int in_dtype, int nz_dtype, int n, int m, int d) {
-  return gs == 4 && (in_dtype == DFSS_BF16 || in_dtype == DFSS_F16) && nz_dtype == in_dtype && d == HD &&
+  return (gs == 4 || gs == 2) && (in_dtype == DFSS_BF16 || in_dtype == DFSS_F16) && nz_dtype == in_dtype && d == HD &&
          n % BM == 0 && m % 128 == 0 && n > 0 && m > 0;
 }
 
@@ -279,7 +319,7 @@ static int num_sms() {
   return cached;
 }
 
-template <typename T>
+template <typename T, int GS>
 static cudaError_t launch_typed(const void* q, const void* k, void* nz, uint32_t* meta, float scale, int64_t bh, int n,
                                 int m, float* dbg, float* rowmax, cudaStream_t s) {
   const CUtensorMapDataType dt =
@@ -289,8 +329,8 @@ static cudaError_t launch_typed(const void* q, const void* k, void* nz, uint32_t
       !encode_tmap_3d(&tk, dt, 2, (void*)k, HD, m, bh, HD, BN, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !encode_tmap_3d(&tn, dt, 2, nz, m / 2, n, bh, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
-  auto kern = dbg ? (rowmax ? sddmm24_tc_kernel<T, true, true> : sddmm24_tc_kernel<T, true, false>)
-                 : (rowmax ? sddmm24_tc_kernel<T, false, true> : sddmm24_tc_kernel<T, false, false>);
+  auto kern = dbg ? (rowmax ? sddmm24_tc_kernel<T, GS, true, true> : sddmm24_tc_kernel<T, GS, true, false>)
+                 : (rowmax ? sddmm24_tc_kernel<T, GS, false, true> : sddmm24_tc_kernel<T, GS, false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
   if (e != cudaSuccess) return e;
   const int items = (int)bh * (n / BM);
@@ -303,8 +343,12 @@ cudaError_t launch_sddmm_tc(const void* q, const void* k, void* nz, uint32_t* me
                             int64_t bh, int n, int m, int d, float* dbg, float* rowmax, cudaStream_t s) {
   if (!tc_sddmm_supported(gs, in_dtype, in_dtype, n, m, d)) return cudaErrorNotSupported;
   if (bh == 0) return cudaSuccess;
-  if (in_dtype == DFSS_BF16) return launch_typed<__nv_bfloat16>(q, k, nz, meta, scale, bh, n, m, dbg, rowmax, s);
-  return launch_typed<__half>(q, k, nz, meta, scale, bh, n, m, dbg, rowmax, s);
+  if (gs == 2) {
+    if (in_dtype == DFSS_BF16) return launch_typed<__nv_bfloat16, 2>(q, k, nz, meta, scale, bh, n, m, dbg, rowmax, s);
+    return launch_typed<__half, 2>(q, k, nz, meta, scale, bh, n, m, dbg, rowmax, s);
+  }
+  if (in_dtype == DFSS_BF16) return launch_typed<__nv_bfloat16, 4>(q, k, nz, meta, scale, bh, n, m, dbg, rowmax, s);
+  return launch_typed<__half, 4>(q, k, nz, meta, scale, bh, n, m, dbg, rowmax, s);
 }
 
 }  // namespace dfss

@@ -10,6 +10,8 @@
 // raise the reference's ValueError (sparse_ops.py:27-32) after the fact.
 #include <math_constants.h>
 
+#include <type_traits>
+
 #include "dfss_common.cuh"
 
 namespace dfss {
@@ -136,6 +138,145 @@ __global__ void __launch_bounds__(256) softmax_rows_kernel(const TIn* __restrict
   }
 }
 
+// Fast path: 16-bit in and out (same type), no tile mask, rows of NV * 256 nonzeros.  The row
+// stays in registers PACKED (NV x 16 B per lane: 32 registers at 2048 nonzeros, so 3 CTAs of 8
+// warps fit per SM and keep ~128 KB of loads in flight), the maximum is taken on packed pairs
+// (exact in 16 bit), exp is recomputed in the normalising pass instead of cached as fp32 (MUFU has
+// the headroom: 2 ex2 per element stay under the HBM time), and NaN detection costs nothing in
+// the common case: a NaN input makes the row sum NaN, and only then is the row re-scanned to tell
+// a NaN input (reference: ValueError) from an inf (reference: NaN output, no error).
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// the normalising pass recomputes exp: volatile, so the compiler cannot keep the first pass's
+// values alive across the row-sum reduction instead (64 live floats: spills)
+__device__ __forceinline__ float ex2_again(float f, float c, float nb) {  // exp2(f * c + nb)
+  float y;
+  asm volatile("{\n\t.reg .f32 t;\n\tfma.rn.f32 t, %1, %2, %3;\n\tex2.approx.ftz.f32 %0, t;\n\t}"
+               : "=f"(y) : "f"(f), "f"(c), "f"(nb));
+  return y;
+}
+
+template <typename T, int NV, int RW>
+__global__ void __launch_bounds__(256, 3) softmax_rows16_kernel(const T* __restrict__ in, T* __restrict__ out,
+                                                                int64_t total_rows, int cols,
+                                                                int32_t* __restrict__ err) {
+  using T2 = typename std::conditional<std::is_same<T, __half>::value, __half2, __nv_bfloat162>::type;
+  constexpr float kLog2e = 1.4426950408889634f;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  auto f_lo = [](uint32_t u) -> float {
+    if constexpr (std::is_same<T, __half>::value) return __half2float(__ushort_as_half((unsigned short)(u & 0xffffu)));
+    else return __uint_as_float(u << 16);
+  };
+  auto f_hi = [](uint32_t u) -> float {
+    if constexpr (std::is_same<T, __half>::value) return __half2float(__ushort_as_half((unsigned short)(u >> 16)));
+    else return __uint_as_float(u & 0xffff0000u);
+  };
+  // RW rows per warp at a time (short rows: more loads in flight per warp)
+  for (int64_t rg0 = warp * RW; rg0 < total_rows; rg0 += nwarps * RW) {
+    uint4 pk[RW][NV];
+#pragma unroll
+    for (int q = 0; q < RW; ++q) {
+      const uint4* x = reinterpret_cast<const uint4*>(in + (rg0 + q) * cols);
+#pragma unroll
+      for (int t = 0; t < NV; ++t) pk[q][t] = (rg0 + q < total_rows) ? __ldcs(x + lane + 32 * t) : make_uint4(0, 0, 0, 0);
+    }
+    float mb[RW], inv[RW];
+#pragma unroll
+    for (int q = 0; q < RW; ++q) {
+      // max on packed pairs
+      uint32_t m2u = pk[q][0].x;
+#pragma unroll
+      for (int t = 0; t < NV; ++t) {
+        const uint32_t w[4] = {pk[q][t].x, pk[q][t].y, pk[q][t].z, pk[q][t].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          T2 a = *reinterpret_cast<const T2*>(&m2u), c = *reinterpret_cast<const T2*>(&w[i]);
+          a = __hmax2(a, c);
+          m2u = *reinterpret_cast<uint32_t*>(&a);
+        }
+      }
+      float mx = fmaxf(f_lo(m2u), f_hi(m2u));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mb[q] = mx * kLog2e;
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int t = 0; t < NV; ++t) {
+        const uint32_t w[4] = {pk[q][t].x, pk[q][t].y, pk[q][t].z, pk[q][t].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          s0 += ex2_approx(fmaf(f_lo(w[i]), kLog2e, -mb[q]));
+          s1 += ex2_approx(fmaf(f_hi(w[i]), kLog2e, -mb[q]));
+        }
+      }
+      float sum = s0 + s1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (isnan(sum)) {  // rare: a NaN input (flag it) or an inf (reference: NaN output, no error)
+        bool nan_seen = false;
+#pragma unroll
+        for (int t = 0; t < NV; ++t) {
+          const uint32_t w[4] = {pk[q][t].x, pk[q][t].y, pk[q][t].z, pk[q][t].w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) nan_seen |= isnan(f_lo(w[i])) || isnan(f_hi(w[i]));
+        }
+        if (__any_sync(0xffffffffu, nan_seen) && lane == 0 && err && rg0 + q < total_rows)
+          atomicMin(err + 1, (int32_t)(rg0 + q + 1));
+      }
+      inv[q] = 1.0f / sum;
+    }
+#pragma unroll
+    for (int q = 0; q < RW; ++q) {
+      if (rg0 + q >= total_rows) break;
+      uint4* y = reinterpret_cast<uint4*>(out + (rg0 + q) * cols);
+#pragma unroll
+      for (int t = 0; t < NV; ++t) {
+        const uint32_t w[4] = {pk[q][t].x, pk[q][t].y, pk[q][t].z, pk[q][t].w};
+        uint32_t o4[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float a = ex2_again(f_lo(w[i]), kLog2e, -mb[q]) * inv[q];
+          const float c = ex2_again(f_hi(w[i]), kLog2e, -mb[q]) * inv[q];
+          T2 p2;
+          if constexpr (std::is_same<T, __half>::value) p2 = __floats2half2_rn(a, c);
+          else p2 = __floats2bfloat162_rn(a, c);
+          o4[i] = *reinterpret_cast<uint32_t*>(&p2);
+        }
+        __stcs(y + lane + 32 * t, make_uint4(o4[0], o4[1], o4[2], o4[3]));
+      }
+    }
+  }
+}
+
+template <typename T>
+static bool softmax16_fast(const void* in, void* out, int64_t bh, int rows, int cols, int32_t* err, cudaStream_t s,
+                           cudaError_t* e) {
+  if (cols % 256 || cols > 2048 || ((uintptr_t)in | (uintptr_t)out) % 16) return false;
+  const int64_t total = bh * rows;
+  auto go = [&](auto kern, int rw) {
+    int64_t blocks = (total + 8 * rw - 1) / (8 * rw);
+    if (blocks > 148 * 3 * 4) blocks = 148 * 3 * 4;
+    kern<<<(int)blocks, 256, 0, s>>>((const T*)in, (T*)out, total, cols, err);
+  };
+  switch (cols / 256) {
+    case 1: go(softmax_rows16_kernel<T, 1, 4>, 4); break;
+    case 2: go(softmax_rows16_kernel<T, 2, 2>, 2); break;
+    case 3: go(softmax_rows16_kernel<T, 3, 1>, 1); break;
+    case 4: go(softmax_rows16_kernel<T, 4, 1>, 1); break;
+    case 5: go(softmax_rows16_kernel<T, 5, 1>, 1); break;
+    case 6: go(softmax_rows16_kernel<T, 6, 1>, 1); break;
+    case 7: go(softmax_rows16_kernel<T, 7, 1>, 1); break;
+    default: go(softmax_rows16_kernel<T, 8, 1>, 1); break;
+  }
+  *e = cudaGetLastError();
+  return true;
+}
+
 template <typename TIn, typename TOut, int VEC>
 static cudaError_t softmax_vec(const void* in, void* out, int64_t bh, int rows, int cols, const uint8_t* keep,
                                int tr, int tc, int32_t* err, cudaStream_t s) {
@@ -163,6 +304,10 @@ static cudaError_t softmax_vec(const void* in, void* out, int64_t bh, int rows, 
 template <typename TIn, typename TOut>
 static cudaError_t softmax_typed(const void* in, void* out, int64_t bh, int rows, int cols, const uint8_t* keep,
                                  int tr, int tc, int32_t* err, cudaStream_t s) {
+  if constexpr (std::is_same<TIn, TOut>::value && !std::is_same<TIn, float>::value) {
+    cudaError_t e;
+    if (!keep && softmax16_fast<TIn>(in, out, bh, rows, cols, err, s, &e)) return e;
+  }
   constexpr int V = 16 / (sizeof(TIn) > sizeof(TOut) ? sizeof(TIn) : sizeof(TOut));
   const bool aligned = (cols % V == 0) && ((uintptr_t)in % 16 == 0) && ((uintptr_t)out % 16 == 0);
   if (aligned) return softmax_vec<TIn, TOut, V>(in, out, bh, rows, cols, keep, tr, tc, err, s);

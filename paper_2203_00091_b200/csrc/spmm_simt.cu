@@ -92,10 +92,102 @@ __global__ void __launch_bounds__(256) spmm_simt_kernel(const TP* __restrict__ p
   }
 }
 
+// Tiled generic variant (d == 64, n_k % 128 == 0): a CTA owns 32 rows of one (batch, head) and
+// streams V through shared memory (converted to fp32) in 128-key tiles, so every V row is read
+// from L2 once per CTA instead of once per nonzero -- the warp-per-row kernel above re-reads a
+// 128-byte V row per nonzero and is L2-bound at long rows (c4 1:2: 48 ms).  The nonzeros of a
+// row inside a 128-key tile are the contiguous range [k0 / 2, k0 / 2 + 64) for either mode.
+// Absent nonzeros (BlockMask) point at an all-zero V row and weigh 0: skipped, as the reference
+// skips them (_kernels_numba.py:98) -- no 0 * Inf.  Accumulation stays in ascending order.
+template <typename TP, typename TV, typename TO, int GS>
+__global__ void __launch_bounds__(256) spmm_tiled_kernel(const TP* __restrict__ p, const uint32_t* __restrict__ meta,
+                                                         const TV* __restrict__ v, TO* __restrict__ out, int rows,
+                                                         int n_k, const uint8_t* __restrict__ keep, int tile_rows,
+                                                         int tile_cols, MetaGeom geo) {
+  constexpr int RB = 32, KT = 128, NZT = KT / 2;
+  constexpr int VE = 16 / sizeof(TV);  // V elements per 16-byte load
+  __shared__ __align__(16) float Vs[KT + 1][64];
+  __shared__ float Ps[RB][NZT + 1];
+  __shared__ uint8_t Cs[RB][NZT];
+  const int b = blockIdx.y, row0 = blockIdx.x * RB;
+  const int nzc = n_k / 2;
+  const int grid_cols = keep ? (n_k + tile_cols - 1) / tile_cols : 0;
+  const TP* pb = p + ((int64_t)b * rows) * nzc;
+  const uint32_t* mb = meta + (int64_t)b * geo.words_per_bh();
+  const uint4* vb = reinterpret_cast<const uint4*>(v + (int64_t)b * n_k * 64);
+  if (threadIdx.x < 64) Vs[KT][threadIdx.x] = 0.f;
+  const int orow = threadIdx.x >> 3, cb = threadIdx.x & 7;  // output row, 8-column block
+  float acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  for (int k0 = 0; k0 < n_k; k0 += KT) {
+#pragma unroll
+    for (int i = 0; i < (KT * 64 / VE) / 256; ++i) {
+      const int idx = threadIdx.x + 256 * i;  // 16-byte unit of the [128][64] tile
+      const uint4 u = vb[(int64_t)k0 * (64 / VE) + idx];
+      const TV* e = reinterpret_cast<const TV*>(&u);
+      float* dst = &Vs[0][0] + idx * VE;
+#pragma unroll
+      for (int j = 0; j < VE; ++j) dst[j] = DT<TV>::to_f(e[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < (RB * NZT) / 256; ++i) {
+      const int idx = threadIdx.x + 256 * i;
+      const int rr = idx / NZT, jl = idx % NZT;
+      const int r = row0 + rr, j = k0 / 2 + jl;
+      float w = 0.f;
+      int col = KT;  // the zero row: rows past the end, absent nonzeros
+      if (r < rows) {
+        const int g = (GS == 4) ? (j >> 1) : j;
+        int shift;
+        const uint32_t nib = (mb[geo.word_of(r, g, shift)] >> shift) & 0xFu;
+        const int c = (GS == 4) ? 4 * g + (int)((j & 1) ? ((nib >> 2) & 3u) : (nib & 3u)) : 2 * g + (nib == 0xEu ? 1 : 0);
+        if (!keep || keep[(int64_t)(r / tile_rows) * grid_cols + c / tile_cols]) {
+          w = DT<TP>::to_f(pb[(int64_t)r * nzc + j]);
+          col = c - k0;
+        }
+      }
+      Ps[rr][jl] = w;
+      Cs[rr][jl] = (uint8_t)col;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int jl = 0; jl < NZT; ++jl) {
+      const float w = Ps[orow][jl];
+      const float4* vr = reinterpret_cast<const float4*>(&Vs[Cs[orow][jl]][8 * cb]);
+      const float4 x0 = vr[0], x1 = vr[1];
+      acc[0] = fmaf(w, x0.x, acc[0]);
+      acc[1] = fmaf(w, x0.y, acc[1]);
+      acc[2] = fmaf(w, x0.z, acc[2]);
+      acc[3] = fmaf(w, x0.w, acc[3]);
+      acc[4] = fmaf(w, x1.x, acc[4]);
+      acc[5] = fmaf(w, x1.y, acc[5]);
+      acc[6] = fmaf(w, x1.z, acc[6]);
+      acc[7] = fmaf(w, x1.w, acc[7]);
+    }
+    __syncthreads();
+  }
+  const int r = row0 + orow;
+  if (r < rows) {
+    TO* o = out + ((int64_t)b * rows + r) * 64 + 8 * cb;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = DT<TO>::from_f(acc[i]);
+  }
+}
+
 template <typename TP, typename TV, typename TO, int GS>
 static cudaError_t spmm_simt_gs(const void* p, const uint32_t* meta, const void* v, void* out, int64_t bh, int rows,
                                 int n_k, int d, const uint8_t* keep, int tr, int tc, cudaStream_t s) {
   MetaGeom geo(rows, n_k / GS);
+  if (d == 64 && n_k % 128 == 0 && n_k >= 512 && ((uintptr_t)v & 15) == 0) {
+    for (int64_t b0 = 0; b0 < bh; b0 += 65535) {  // bh on gridDim.y (<= 65535): slices
+      const int64_t nb = bh - b0 < 65535 ? bh - b0 : 65535;
+      spmm_tiled_kernel<TP, TV, TO, GS><<<dim3((unsigned)((rows + 31) / 32), (unsigned)nb), 256, 0, s>>>(
+          (const TP*)p + b0 * rows * (n_k / 2), meta + b0 * geo.words_per_bh(), (const TV*)v + b0 * n_k * 64,
+          (TO*)out + b0 * rows * 64, rows, n_k, keep, tr, tc, geo);
+    }
+    return cudaGetLastError();
+  }
   const int64_t total = bh * rows;
   int64_t blocks = (total + 7) / 8;
   if (blocks > 148 * 64) blocks = 148 * 64;

@@ -78,7 +78,21 @@ __device__ __forceinline__ uint32_t pack2f<__half>(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&p);
 }
 
-template <typename T, typename TO, bool SOFTMAX>
+// 1:2 metadata (include/dfss.h: one nibble 0x4 / 0xE per pair, meta chunks of 8 pairs) as the
+// tcgen05 2:4 pattern "one survivor per pair" (nibble 8 + a + 4b: elements a and 2 + b of each
+// group of 4): the 1:2 nonzeros already ARE that pattern's stored values in order, so only the
+// metadata is rewritten -- the word of TMEM lane L (m2, k1, m0) for the 32-key chunk kk is built
+// from the 1:2 words of chunk 2 kk + k1 at lanes 16 m2 + m0 (pairs 0-3) and 16 m2 + 8 + m0
+// (pairs 4-7), bit 3 of a 1:2 nibble being "element 1 kept".
+__device__ __forceinline__ uint32_t meta12_to_24(uint32_t w0, uint32_t w1) {
+  const uint32_t x0 = (w0 >> 3) & 0x11111111u, x1 = (w1 >> 3) & 0x11111111u;
+  // byte k of v = the 2:4 nibble of source pairs (2k, 2k + 1) of the word
+  const uint32_t v0 = (x0 & 0x01010101u) | ((x0 & 0x10101010u) >> 2) | 0x08080808u;
+  const uint32_t v1 = (x1 & 0x01010101u) | ((x1 & 0x10101010u) >> 2) | 0x08080808u;
+  return (v0 & 0x000F000Fu) | ((v0 & 0x0F000F00u) >> 4) | ((v1 & 0x000F000Fu) << 8) | ((v1 & 0x0F000F00u) << 4);
+}
+
+template <typename T, typename TO, bool SOFTMAX, int GS>
 __global__ void __launch_bounds__(SOFTMAX ? 640 : 384, 1)
     spmm24_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_v,
                      const uint32_t* __restrict__ meta, TO* __restrict__ out, int bh, int rows, int n_k,
@@ -101,7 +115,7 @@ __global__ void __launch_bounds__(SOFTMAX ? 640 : 384, 1)
   const int rblocks = rows / BM;
   const int items = bh * rblocks;
   const int kblocks = n_k / BKL;
-  const int chunks = n_k / 32;
+  const int chunks = n_k / (8 * GS);  // meta_hw chunks per row block
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tm_p);
@@ -181,11 +195,30 @@ __global__ void __launch_bounds__(SOFTMAX ? 640 : 384, 1)
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       const int b = item / rblocks, rb = item % rblocks;
       const uint32_t* mrow = meta + ((int64_t)b * rblocks + rb) * chunks * 128 + quad * 32 + lane;
+      // 1:2: this lane's source words are at lanes 16 m2 + m0 and + 8 of chunk 2 kk + k1
+      const int L = quad * 32 + (int)lane;
+      const uint32_t* mrow12 = meta + ((int64_t)b * rblocks + rb) * chunks * 128 + 16 * (L >> 4) + (L & 7);
+      const int k1 = (L >> 3) & 1;
       for (int kb = 0; kb < kblocks; ++kb) {
-        const uint32_t w0 = __ldg(mrow + (int64_t)(kb * 4 + 0) * 128);
-        const uint32_t w1 = __ldg(mrow + (int64_t)(kb * 4 + 1) * 128);
-        const uint32_t w2 = __ldg(mrow + (int64_t)(kb * 4 + 2) * 128);
-        const uint32_t w3 = __ldg(mrow + (int64_t)(kb * 4 + 3) * 128);
+        uint32_t w0, w1, w2, w3;
+        if constexpr (GS == 4) {
+          w0 = __ldg(mrow + (int64_t)(kb * 4 + 0) * 128);
+          w1 = __ldg(mrow + (int64_t)(kb * 4 + 1) * 128);
+          w2 = __ldg(mrow + (int64_t)(kb * 4 + 2) * 128);
+          w3 = __ldg(mrow + (int64_t)(kb * 4 + 3) * 128);
+        } else {
+          uint32_t src[8];
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t* c = mrow12 + (int64_t)(kb * 8 + 2 * kk + k1) * 128;
+            src[2 * kk] = __ldg(c);
+            src[2 * kk + 1] = __ldg(c + 8);
+          }
+          w0 = meta12_to_24(src[0], src[1]);
+          w1 = meta12_to_24(src[2], src[3]);
+          w2 = meta12_to_24(src[4], src[5]);
+          w3 = meta12_to_24(src[6], src[7]);
+        }
         tc::mbar_wait(&empty[s], ph ^ 1);
         tc::tc_fence_after();
         tc::tmem_st_32x32b_x4(tmem_base + ((uint32_t)(quad * 32) << 16) + E_COL0 + s * 4, w0, w1, w2, w3);
@@ -298,7 +331,7 @@ __global__ void __launch_bounds__(SOFTMAX ? 640 : 384, 1)
 }
 
 bool tc_spmm_supported(int gs, int p_dtype, int v_dtype, int out_dtype, int rows, int n_k, int d) {
-  return gs == 4 && (p_dtype == DFSS_BF16 || p_dtype == DFSS_F16) && v_dtype == p_dtype &&
+  return (gs == 4 || gs == 2) && (p_dtype == DFSS_BF16 || p_dtype == DFSS_F16) && v_dtype == p_dtype &&
          (out_dtype == p_dtype || out_dtype == DFSS_F32) && d == HD && rows % BM == 0 && n_k % BKL == 0 && rows > 0;
 }
 
@@ -313,7 +346,7 @@ static int num_sms_spmm() {
   return cached;
 }
 
-template <typename T, typename TO>
+template <typename T, typename TO, int GS>
 static cudaError_t spmm_launch_typed(const void* p, const uint32_t* meta, const void* v, void* out, int64_t bh, int rows,
                                      int n_k, const float* rowmax, cudaStream_t s) {
   const CUtensorMapDataType dt =
@@ -325,12 +358,12 @@ static cudaError_t spmm_launch_typed(const void* p, const uint32_t* meta, const 
   const int items = (int)bh * (rows / BM);
   const int grid = items < num_sms_spmm() ? items : num_sms_spmm();
   if (rowmax) {
-    auto kern = spmm24_tc_kernel<T, TO, true>;
+    auto kern = spmm24_tc_kernel<T, TO, true, GS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
     if (e != cudaSuccess) return e;
     kern<<<grid, 640, SMEM_TOTAL, s>>>(tp, tv, meta, (TO*)out, (int)bh, rows, n_k, rowmax);
   } else {
-    auto kern = spmm24_tc_kernel<T, TO, false>;
+    auto kern = spmm24_tc_kernel<T, TO, false, GS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
     if (e != cudaSuccess) return e;
     kern<<<grid, 384, SMEM_TOTAL, s>>>(tp, tv, meta, (TO*)out, (int)bh, rows, n_k, nullptr);
@@ -342,12 +375,16 @@ cudaError_t launch_spmm_tc(const void* p, const uint32_t* meta, const void* v, v
                            int out_dtype, int64_t bh, int rows, int n_k, int d, const float* rowmax, cudaStream_t s) {
   if (!tc_spmm_supported(gs, dtype, dtype, out_dtype, rows, n_k, d)) return cudaErrorNotSupported;
   if (bh == 0) return cudaSuccess;
-  if (dtype == DFSS_BF16)
-    return out_dtype == DFSS_F32
-               ? spmm_launch_typed<__nv_bfloat16, float>(p, meta, v, out, bh, rows, n_k, rowmax, s)
-               : spmm_launch_typed<__nv_bfloat16, __nv_bfloat16>(p, meta, v, out, bh, rows, n_k, rowmax, s);
-  return out_dtype == DFSS_F32 ? spmm_launch_typed<__half, float>(p, meta, v, out, bh, rows, n_k, rowmax, s)
-                               : spmm_launch_typed<__half, __half>(p, meta, v, out, bh, rows, n_k, rowmax, s);
+  auto go = [&](auto gs_tag) {
+    constexpr int G = decltype(gs_tag)::value;
+    if (dtype == DFSS_BF16)
+      return out_dtype == DFSS_F32
+                 ? spmm_launch_typed<__nv_bfloat16, float, G>(p, meta, v, out, bh, rows, n_k, rowmax, s)
+                 : spmm_launch_typed<__nv_bfloat16, __nv_bfloat16, G>(p, meta, v, out, bh, rows, n_k, rowmax, s);
+    return out_dtype == DFSS_F32 ? spmm_launch_typed<__half, float, G>(p, meta, v, out, bh, rows, n_k, rowmax, s)
+                                 : spmm_launch_typed<__half, __half, G>(p, meta, v, out, bh, rows, n_k, rowmax, s);
+  };
+  return gs == 2 ? go(std::integral_constant<int, 2>{}) : go(std::integral_constant<int, 4>{});
 }
 
 }  // namespace dfss

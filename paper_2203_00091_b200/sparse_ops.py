@@ -110,7 +110,7 @@ def spmm_softmax(a: CompressedSparse, v, out_dtype: torch.dtype | None = None) -
     """``spmm(softmax_rows(a), v)`` in one kernel: the row softmax is applied to each staged
     P tile in shared memory (exp(s - row max)) and the output rows are divided by the row
     sums -- no HBM round trip for the probabilities.  Needs ``a`` from
-    ``sddmm_prune(..., with_row_max=True)`` (tcgen05 path: 2:4, 16-bit, d = 64)."""
+    ``sddmm_prune(..., with_row_max=True)`` (tcgen05 path: 2:4 or 1:2, 16-bit, d = 64)."""
     if a.row_max is None:
         raise ValueError("spmm_softmax needs the row maxima: call sddmm_prune(..., with_row_max=True)")
     if a.layout is not Layout.LOGICAL or a.block_mask is not None:

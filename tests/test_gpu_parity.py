@@ -385,18 +385,25 @@ def test_flash_sequence_lengths(n):
     _flash_vs_oracle(q, k, v, f"n={n}")
 
 
+@pytest.mark.parametrize("mode", ["2:4", "1:2"])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
-def test_fused_softmax_spmm_matches_staged_and_oracle(dtype):
-    """spmm_softmax(sddmm_prune(with_row_max)) == spmm(softmax_rows(.)) == reference nm_attention."""
+def test_fused_softmax_spmm_matches_staged_and_oracle(dtype, mode):
+    """spmm_softmax(sddmm_prune(with_row_max)) == spmm(softmax_rows(.)) == reference nm_attention
+    (1:2 runs the tcgen05 kernels too: one survivor per pair as the 2:4 pattern 8 + a + 4b)."""
     (q, k, v), (q64, k64, v64) = seeded_qkv((2, 2, 640, 64), dtype, seed=4)
     dbg = torch.empty((2, 2, 640, 640), dtype=torch.float32, device="cuda")
-    c, _ = dfss.sddmm_prune(q, k, "2:4", 0.125, with_row_max=True, scores_out=dbg)
+    c, _ = dfss.sddmm_prune(q, k, mode, 0.125, with_row_max=True, scores_out=dbg)
+    meta = logical_meta(c)
+    for b in range(2):
+        for h in range(2):
+            _, want_meta, _ = oracle_on_scores(_np(dbg[b, h]), mode)
+            assert np.array_equal(meta[b, h], want_meta), (mode, b, h)
     # the recorded row maximum is the exact fp32 max of the row's scores (always a kept value)
     assert torch.equal(c.row_max.amax(-1), dbg.amax(-1))
     fused = _np(dfss.spmm_softmax(c, v).data)
     staged = _np(dfss.spmm(dfss.softmax_rows(c), v).data)
     assert_close(fused, staged, 2e-2, 2e-2, "fused vs staged")
-    want = oracle_attention(q64, k64, v64, "2:4")
+    want = oracle_attention(q64, k64, v64, mode)
     assert_close(fused, want, 2e-2, 2e-2, "fused vs oracle")
 
 

@@ -63,7 +63,11 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, 
                                           uint8_t* stg, uint32_t lane, uint32_t* meta_b, int row_blk, float* dbg,
                                           int64_t dbg_row, int m, float& mx, uint32_t two) {
   uint32_t packed[8];
-  uint32_t W = 0;
+  // the select24 rule with the metadata in float arithmetic on the FMA-lite pipe (as in the
+  // fused kernel, flash_tc.cu prune_exp_tile): exact 0 / 1 pair-winner flags from saturated
+  // multiplies of v0 - v1, v2 - v3 (canonical zeros: a tie gives +0 -> 0), nibble - 8 accumulated
+  // as integers into 2^23 + 0x8888 floats, one PRMT -- no IMAD.HI / SEL chains on the busy pipes
+  float wf[2] = {8388608.f + 34952.f, 8388608.f + 34952.f};
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
     const float v0 = scale_canon(__uint_as_float(r[4 * g + 0]), scale);
@@ -71,11 +75,22 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, 
     const float v2 = scale_canon(__uint_as_float(r[4 * g + 2]), scale);
     const float v3 = scale_canon(__uint_as_float(r[4 * g + 3]), scale);
     if (DBG) *reinterpret_cast<float4*>(dbg + dbg_row * m + colh + cc * 32 + 4 * g) = make_float4(v0, v1, v2, v3);
-    float lo, hi;
-    const uint32_t nib = RMAX ? select24_max(v0, v1, v2, v3, lo, hi, mx, two) : select24(v0, v1, v2, v3, lo, hi, two);
+    const float w01 = fmaxf(v0, v1), l01 = fminf(v0, v1);
+    const float w23 = fmaxf(v2, v3), l23 = fminf(v2, v3);
+    if (RMAX) mx = fmaxf(mx, fmaxf(w01, w23));
+    const bool keep01 = l01 >= w23, keep23 = l23 > w01;
+    const float lo = keep01 ? v0 : (keep23 ? v2 : w01);
+    const float hi = keep01 ? v1 : (keep23 ? v3 : w23);
+    const float fa = __saturatef(__fmul_rn(v0 - v1, -1.7014118e38f) * 1.7014118e38f);
+    const float fb = __saturatef(__fmul_rn(v2 - v3, -1.7014118e38f) * 1.7014118e38f);
+    float nf = fmaf(fb, 4.f, fa);
+    nf = keep23 ? 6.f : nf;
+    nf = keep01 ? -4.f : nf;
+    wf[g >> 2] = fmaf(nf, (float)(1 << (4 * (g & 3))), wf[g >> 2]);
     packed[g] = pack2<T>(lo, hi);
-    W += nib * (1u << (4 * g));  // IMAD on the FMA pipe, not shift+or on the ALU pipe
   }
+  const uint32_t W = __byte_perm(__float_as_uint(wf[0]), __float_as_uint(wf[1]), 0x5410);
+  (void)two;
   const int u0 = unit0, sw = lane & 7;
   *reinterpret_cast<uint4*>(stg + lane * 128 + ((u0 ^ sw) << 4)) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
   *reinterpret_cast<uint4*>(stg + lane * 128 + (((u0 + 1) ^ sw) << 4)) =

@@ -82,6 +82,7 @@ constexpr int TM_O = 2 * BN;     // O_h at TM_O + 64 h
 constexpr int TM_E = TM_O + 2 * HD;  // PST x 4 metadata columns
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kSumLimit = 256.0f;  // a quarter-tile partial sum above 2^8 triggers a shift update
+constexpr float kSumFloor = 1.0f / 65536.0f;  // an item's first step summing below 2^-16: start shift too high
 }  // namespace
 
 // Split of the last round (two-set kernel, unmasked): `items` equal items on G persistent CTAs
@@ -967,13 +968,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       return __ldg(tmask.cbits + (int64_t)strip * tmask.cbw + lane);
     };
     uint32_t cw = cword(pos_at(0));
+    float carry_mlog = -INFINITY;  // the shift this row ended the set's previous item with
     const uint32_t word_sel = (lane & 8) ? 0x3276u : 0x5410u;
     int item, t0, t1, part;
     for (int kk_ = 0; unit_at(kk_, item, t0, t1, part); ++kk_, ++it) {
       uint32_t lw0 = 0, lw1 = 0;
       const int b = item / iblocks, ib = item % iblocks;
       const uint32_t cwn = cword(pos_at(kk_ + 1));
-      float mlog = 0.f, l0 = 0.f, l1 = 0.f;
+      float mlog = carry_mlog, l0 = 0.f, l1 = 0.f;
       bool first = true;  // first live step of this half-item: establishes the shift
       for (int t = t0; t < t1; ++t) {
         live_words(ib, t, lw0, lw1);
@@ -999,10 +1001,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           cm[1] = !(w & 2u);
           anym = __any_sync(0xffffffffu, (~w & 3u) != 0);
         }
-        // the shift starts at the row maximum of the item's first live tile -- unmasked: of its
-        // first 32 columns only, read by both warps of the pair alike (no exchange, no barrier);
-        // a step whose sums then exceed the limit recomputes with the exact maximum (below)
-        if (first) mlog = MASKED ? row_max() : chunk0_max();
+        // the shift starts at the row maximum of the item's first live tile -- unmasked: the
+        // shift the row of this set's previous item ended with (attention rows of one launch
+        // share their scale; no TMEM pass, no barrier), or the max of the first 32 columns for
+        // the first item, read by both warps of the pair alike; a first step whose sums leave
+        // [2^-16, 2^8] recomputes with the exact maximum (below)
+        if (first) mlog = MASKED ? row_max() : (carry_mlog == -INFINITY ? chunk0_max() : carry_mlog);
         uint32_t pk[2][8], W[2];
         float lt0 = 0.f, lt1 = 0.f;
         auto compute = [&](auto masked_variant) {
@@ -1037,10 +1041,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #ifdef DFSS_EXP_NO_VOTE
           if (pass > 0 || first || !((W[0] & W[1]) == ~0u && lt0 + lt1 > 1e30f)) break;
 #else
-          if (pass > 0 || (MASKED && first) || !bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit) || (W[0] & W[1]) == ~0u)) break;
+          if (pass > 0 || (MASKED && first) ||
+              !bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit) || (first && !(lt0 + lt1 >= kSumFloor)) ||
+                                     (W[0] & W[1]) == ~0u))
+            break;
 #endif
-          if (!MASKED && first) {  // estimated shift too low: exact row maximum, nothing accumulated yet
-            mlog = fmaxf(mlog, row_max());
+          if (!MASKED && first) {  // estimated shift off: exact row maximum, nothing accumulated yet
+            mlog = row_max();
             continue;
           }
           // ---- slow path (both warps of the pair): raise the shift to the row maximum,
@@ -1099,6 +1106,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc::named_bar_sync(pbar, 64);
       pend_lsum = rsum[r] + rsum[BM + r];
       tc::named_bar_sync(pbar, 64);
+      carry_mlog = mlog;
       pend = true;
       pend_b = b;
       pend_ib = ib;

@@ -353,6 +353,24 @@ def test_flash_large_logits(dtype):
     _flash_vs_oracle(q * 8, k, v, "large logits")
 
 
+@pytest.mark.parametrize("mode", ["2:4", "1:2"])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_flash_start_shift_carried_across_items(mode, dtype):
+    """Unmasked items start their lazy shift from the shift the row ended the CTA's previous item
+    with.  Heads whose logit scales jump by 1000x from one item to the next (so each CTA's next
+    item starts far too high or far too low) must still match the reference: the first step's
+    sums leave [2^-16, 2^8] and it recomputes with the exact row maximum."""
+    b, h, n = 2, 150, 512  # 600 items: ~4 per persistent CTA, neighbours on a CTA are 148 apart
+    (q, k, v), _ = seeded_qkv((b, h, n, 64), dtype, seed=31)
+    scale = torch.tensor([[[0.02, 1.0, 20.0][(i * 7 + j) % 3] for j in range(h)] for i in range(b)])
+    q = (q.float() * scale.view(b, h, 1, 1).cuda()).to(dtype)
+    out = _np(dfss.dfss_attention(q, k, v, mode))
+    heads = [(0, 0), (0, 1), (0, 2), (1, 74), (1, 148), (1, 149)]
+    for bi, hi in heads:
+        want = oracle_attention(*(x[bi, hi].double().cpu().numpy() for x in (q, k, v)), mode)
+        assert_close(out[bi, hi], want, 2e-2, 2e-2, f"carried shift {mode} head ({bi},{hi})")
+
+
 def test_flash_tie_lattice_and_zero_queries():
     """Integer-lattice Q/K (exact bf16, many tied scores) and all-zero queries (every score is
     a signed zero: the reference keeps the lower index of every tie, so O = mean of V rows

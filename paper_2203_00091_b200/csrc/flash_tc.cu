@@ -936,15 +936,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     bool pend = false;
     int pend_b = 0, pend_ib = 0, pend_it = 0, pend_item = 0, pend_part = -1;
     float pend_lsum = 0.f, pend_m = 0.f;
-    auto epilogue = [&]() {
+    // drain_o: O_h of the pending item into registers, O_h released (o_empty); finish_o: normalise
+    // and store.  Split so that the next item's first P can be published in between.
+    auto drain_o = [&](uint32_t (&o)[32]) {
       tc::mbar_wait(&o_full[h], pend_it & 1);
       tc::tc_fence_after();
-      uint32_t o[32];
       tc::tmem_ld_32x32b_x32(lane_base + T2_O + h * HD + 32 * pr, o);
       tc::tmem_ld_wait(o);
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&o_empty[h]);
+    };
+    auto finish_o = [&](const uint32_t (&o)[32]) {
       const int64_t row = (int64_t)pend_b * n + (pend_ib * 2 + h) * BM + r;
       pend = false;
       if (!MASKED && pend_part >= 0) {
@@ -960,6 +963,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint4* orow = reinterpret_cast<uint4*>(out + row * HD + 32 * pr);
 #pragma unroll
       for (int j = 0; j < 4; ++j) orow[j] = make_uint4(pko[4 * j], pko[4 * j + 1], pko[4 * j + 2], pko[4 * j + 3]);
+    };
+    auto epilogue = [&]() {
+      uint32_t o[32];
+      drain_o(o);
+      finish_o(o);
     };
     // chunk-keep word `lane` of this warp's 32-row strip (cbits), next item's prefetched
     auto cword = [&](int pos_) -> uint32_t {
@@ -1075,28 +1083,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         add2(l0, l1, lt0, lt1, l0, l1);
         if (tw) FTRACE(1, it, t, h);
-        // previous item's output, before this item's first P goes out (masked kernels: after it --
-        // their extra live state would spill around the epilogue here)
-        if (!MASKED && pend) epilogue();
         // P (8 columns of 16-bit pairs at 32q + 16) and the metadata word (column 32q) of each
         // chunk into this warp's own, already read S columns; rows r and r^8 trade metadata
         // halves (include/dfss.h): one PRMT with a lane-dependent selector
+        auto publish = [&]() {
 #pragma unroll
-        for (int ch = 0; ch < 2; ++ch) {
-          const uint32_t partner = __shfl_xor_sync(0xffffffffu, W[ch], 8);
-          const uint32_t word = __byte_perm(W[ch], partner, word_sel);
-          tc::tmem_st_32x32b_x8(scol + 32 * ch + 16, pk[ch]);
-          tc::tmem_st_32x32b_x1(scol + 32 * ch, word);
-          if constexpr (DUMP)
-            dump.meta[(((int64_t)b * (n / BM) + ib * 2 + h) * (n / 32) + 4 * t + 2 * pr + ch) * BM + r] = word;
+          for (int ch = 0; ch < 2; ++ch) {
+            const uint32_t partner = __shfl_xor_sync(0xffffffffu, W[ch], 8);
+            const uint32_t word = __byte_perm(W[ch], partner, word_sel);
+            tc::tmem_st_32x32b_x8(scol + 32 * ch + 16, pk[ch]);
+            tc::tmem_st_32x32b_x1(scol + 32 * ch, word);
+            if constexpr (DUMP)
+              dump.meta[(((int64_t)b * (n / BM) + ib * 2 + h) * (n / 32) + 4 * t + 2 * pr + ch) * BM + r] = word;
+          }
+          tc::tmem_st_wait();
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&p_full[h * S2RING + slot]);
+        };
+        if (!MASKED && pend) {
+          // the previous item's O_h leaves TMEM before this item's first P goes out (that P's PV
+          // overwrites O_h); normalising and storing it follows the publication (masked kernels:
+          // the whole epilogue after it -- their extra live state would spill around it here)
+          uint32_t o[32];
+          drain_o(o);
+          publish();
+          finish_o(o);
+        } else {
+          publish();
+          if (MASKED && pend) epilogue();
         }
-        tc::tmem_st_wait();
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&p_full[h * S2RING + slot]);
         if (tw) FTRACE(2, it, t, h);
         first = false;
-        if (MASKED && pend) epilogue();
       }
       if (tw && h == 0) UTRACE(kk_, 3);
       // the epilogue of this item runs in step 0 of the next one (above), so the wait for the

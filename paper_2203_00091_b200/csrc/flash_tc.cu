@@ -885,6 +885,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   } else {
     regs_softmax();
+    // the per-step barriers as 32-bit shared addresses (see tc::mbar_wait_u32)
+    // (materialised through asm so the compiler keeps them instead of re-deriving them from the
+    // generic smem pointer -- window base + alignment -- at every use)
+    uint32_t s_full32, p_full32;
+    asm volatile("mov.b32 %0, %1;" : "=r"(s_full32) : "r"(tc::smem_u32(s_full)));
+    asm volatile("mov.b32 %0, %1;" : "=r"(p_full32) : "r"(tc::smem_u32(p_full)));
     // ------------------------------------------------------------ softmax / prune / epilogue sets
     const int h = warp >> 3;              // half owned by this set
     const int pr = (warp >> 2) & 1;       // column pair: quarters 2pr, 2pr + 1
@@ -995,7 +1001,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t slot = g % S2RING;
         scol = lane_base + slot * BN + 64 * pr;
 #ifndef DFSS_EXP_NO_SWAIT
-        tc::mbar_wait(&s_full[h * S2RING + slot], (sfbits >> slot) & 1);  // k-th use of (h, slot): parity k & 1
+        tc::mbar_wait_u32(s_full32 + 8 * (h * S2RING + slot), (sfbits >> slot) & 1);  // k-th use of (h, slot): parity k & 1
 #endif
         sfbits ^= 1u << slot;
         if (tw) FTRACE(0, it, t, h);
@@ -1099,7 +1105,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc::tmem_st_wait();
           tc::tc_fence_before();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&p_full[h * S2RING + slot]);
+          if (lane == 0) tc::mbar_arrive_u32(p_full32 + 8 * (h * S2RING + slot));
         };
         if (!MASKED && pend) {
           // the previous item's O_h leaves TMEM before this item's first P goes out (that P's PV

@@ -82,7 +82,13 @@ constexpr int TM_O = 2 * BN;     // O_h at TM_O + 64 h
 constexpr int TM_E = TM_O + 2 * HD;  // PST x 4 metadata columns
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kSumLimit = 256.0f;  // a quarter-tile partial sum above 2^8 triggers a shift update
-constexpr float kSumFloor = 1.0f / 65536.0f;  // an item's first step summing below 2^-16: start shift too high
+// an item's first step summing below the floor: its start shift (carried from the previous item)
+// is too high -- recompute with the exact maximum.  fp16 P must stay out of the denormal range
+// (< 2^-14): 2^-6 keeps the significant terms normal; bf16 shares fp32's exponent range.
+template <typename T>
+__host__ __device__ constexpr float sum_floor() {
+  return std::is_same<T, __half>::value ? 1.0f / 64.0f : 1.0f / 65536.0f;
+}
 }  // namespace
 
 // Split of the last round (two-set kernel, unmasked): `items` equal items on G persistent CTAs
@@ -1056,7 +1062,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (pass > 0 || first || !((W[0] & W[1]) == ~0u && lt0 + lt1 > 1e30f)) break;
 #else
           if (pass > 0 || (MASKED && first) ||
-              !bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit) || (first && !(lt0 + lt1 >= kSumFloor)) ||
+              !bar_any(pbar, 64, !(lt0 + lt1 <= kSumLimit) || (first && !(lt0 + lt1 >= sum_floor<T>())) ||
                                      (W[0] & W[1]) == ~0u))
             break;
 #endif

@@ -353,16 +353,19 @@ def test_flash_large_logits(dtype):
     _flash_vs_oracle(q * 8, k, v, "large logits")
 
 
+@pytest.mark.parametrize("scales", [(0.02, 1.0, 20.0), (1.0, 5.0, 1.0)])
 @pytest.mark.parametrize("mode", ["2:4", "1:2"])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
-def test_flash_start_shift_carried_across_items(mode, dtype):
+def test_flash_start_shift_carried_across_items(mode, dtype, scales):
     """Unmasked items start their lazy shift from the shift the row ended the CTA's previous item
     with.  Heads whose logit scales jump by 1000x from one item to the next (so each CTA's next
     item starts far too high or far too low) must still match the reference: the first step's
     sums leave [2^-16, 2^8] and it recomputes with the exact row maximum."""
     b, h, n = 2, 150, 512  # 600 items: ~4 per persistent CTA, neighbours on a CTA are 148 apart
     (q, k, v), _ = seeded_qkv((b, h, n, 64), dtype, seed=31)
-    scale = torch.tensor([[[0.02, 1.0, 20.0][(i * 7 + j) % 3] for j in range(h)] for i in range(b)])
+    # (1, 5, 1): a start shift ~15 too high in log2 units -- fp16 P would sink into the denormal
+    # range without the fp16 sum floor (2^-6)
+    scale = torch.tensor([[scales[(i * 7 + j) % 3] for j in range(h)] for i in range(b)])
     q = (q.float() * scale.view(b, h, 1, 1).cuda()).to(dtype)
     out = _np(dfss.dfss_attention(q, k, v, mode))
     heads = [(0, 0), (0, 1), (0, 2), (1, 74), (1, 148), (1, 149)]

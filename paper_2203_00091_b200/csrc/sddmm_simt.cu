@@ -6,6 +6,8 @@
 // Same epilogue semantics as the tcgen05 kernel and as the reference
 // _sddmm_compress (_kernels_numba.py:110-185): scale, then select by signed
 // value with ties to the lower index, then write nonzeros + nibbles only.
+#include <type_traits>
+
 #include "dfss_common.cuh"
 
 namespace dfss {
@@ -16,8 +18,10 @@ constexpr int BM = 64, BN = 64, BK = 32;
 
 // grid: (ceil(m/64), 2*ceil(n/128), bh); 256 threads, each a 4x4 score block:
 // rows 4*ty .. 4*ty+3, columns 4*tx .. 4*tx+3 (one 2:4 group, two 1:2 groups).
+// (16-bit inputs: at least 2 CTAs / SM, so ptxas keeps their conversions in registers instead of
+// spilling; fp32 (the c1 exact path) keeps 64 registers / 4 CTAs: 114 registers were 10 % slower)
 template <typename TIn, typename TNz, int GS>
-__global__ void __launch_bounds__(256) sddmm_simt_kernel(const TIn* __restrict__ q, const TIn* __restrict__ k,
+__global__ void __launch_bounds__(256, std::is_same<TIn, float>::value ? 4 : 2) sddmm_simt_kernel(const TIn* __restrict__ q, const TIn* __restrict__ k,
                                                          TNz* __restrict__ nz, uint32_t* __restrict__ meta,
                                                          float scale, int n, int m, int d,
                                                          const uint8_t* __restrict__ keep, int tile_rows,

@@ -28,7 +28,7 @@ struct __align__(16) Vec {
 };
 
 template <typename TIn, typename TOut, int VEC, int NV>
-__global__ void __launch_bounds__(256) softmax_rows_kernel(const TIn* __restrict__ in, TOut* __restrict__ out,
+__global__ void __launch_bounds__(256, 2) softmax_rows_kernel(const TIn* __restrict__ in, TOut* __restrict__ out,
                                                            int64_t total_rows, int rows, int cols,
                                                            const uint8_t* __restrict__ keep, int tile_rows,
                                                            int tile_cols, int32_t* __restrict__ err) {

@@ -19,7 +19,7 @@ namespace dfss {
 // row's max and sum of exp over its nonzeros, then weights each nonzero by exp(x - max) and
 // scales the output row by 1 / sum (no mask; the exact-FP32 nm_attention path).
 template <typename TP, typename TV, typename TO, int GS, int DPER, bool SM = false>
-__global__ void __launch_bounds__(256) spmm_simt_kernel(const TP* __restrict__ p, const uint32_t* __restrict__ meta,
+__global__ void __launch_bounds__(256, 4) spmm_simt_kernel(const TP* __restrict__ p, const uint32_t* __restrict__ meta,
                                                         const TV* __restrict__ v, TO* __restrict__ out,
                                                         int64_t total_rows, int rows, int n_k, int d,
                                                         const uint8_t* __restrict__ keep, int tile_rows,

@@ -163,6 +163,8 @@ class ClockSampler:
             self._stop.wait(0.05)
 
     def __enter__(self):
+        if os.environ.get("DFSS_BENCH_NO_SAMPLER"):  # (diagnostics: timing without the sampling thread)
+            return self
         if self._nv is not None:
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
@@ -221,7 +223,12 @@ def soaked_steps(fn, steps, warmup, flush, device):
 
 def time_steps(fn, steps, warmup, flush=None):
     """Per-step CUDA events on the current stream; L2 flushed between steps outside the events."""
+    # warm-up steps exactly like the timed ones (flush included): after unflushed warm-up steps
+    # the first flushed step of the fused kernel ran ~2x the others (c2 0.107 vs 0.049 ms,
+    # tools/time_firststep.py), an artefact of the harness, not a property of the step
     for _ in range(warmup):
+        if flush is not None:
+            flush()
         fn()
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
@@ -330,6 +337,8 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True, info=Tr
     torch.cuda.synchronize()
     # soak (sustained-load clocks, see soak()), then the K timed steps, one sampler window
     times, clocks = soaked_steps(step, args.steps, args.warmup, flush, device)
+    if os.environ.get("DFSS_BENCH_STEP_TIMES"):
+        print(f"[bench] {cfg_name} step ms: " + " ".join(f"{x:.4f}" for x in times), file=sys.stderr)
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()

@@ -9,7 +9,8 @@ import paper_2203_00091_b200 as dfss
 pynvml.nvmlInit()
 hnd = pynvml.nvmlDeviceGetHandleByIndex(0)
 flush_buf = torch.empty(256 * 2**20, dtype=torch.uint8, device="cuda")
-q, k, v = (torch.randn(8, 12, 4096, 64, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+SHAPE = tuple(int(x) for x in os.environ.get("SOAK_SHAPE", "8,12,4096,64").split(","))
+q, k, v = (torch.randn(*SHAPE, device="cuda", dtype=torch.bfloat16) for _ in range(3))
 out = torch.empty_like(q)
 fns = {"dfss": lambda: dfss.dfss_attention(q, k, v, "2:4", out=out),
        "sdpa": lambda: torch.nn.functional.scaled_dot_product_attention(q, k, v)}

@@ -235,6 +235,39 @@ def test_softmax_matches_oracle_rows_sum_to_one(dtype):
             assert torch.equal(out.meta_hw, c.meta_hw)
 
 
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_softmax_16bit_fast_path_edges(dtype):
+    """The packed 16-bit softmax (rows of 256 k nonzeros <= 2048, several short rows per warp):
+    ragged row counts, every row width it serves, the oracle at 8e-3; a NaN input raises the
+    reference's ValueError, an inf input gives NaN without one (numba: exp(inf - inf))."""
+    rng = np.random.default_rng(3)
+    for rows, nz in ((7, 256), (13, 512), (5, 768), (3, 2048), (130, 256)):
+        s = (rng.standard_normal((1, rows, 2 * nz)) * 4).astype(np.float32)
+        c = dfss.compress_logical(torch.from_numpy(s).to(dtype).cuda(), M24)
+        got = _np(dfss.softmax_rows(c).nonzeros)[0]
+        want = oracle_c.softmax_nonzeros(_np(c.nonzeros[0]))
+        assert_close(got, want, 8e-3, 8e-5, f"fast softmax rows={rows} nz={nz}")
+    c = dfss.compress_logical(torch.randn(1, 4, 512, device="cuda").to(dtype), M24)
+    bad = c.nonzeros.clone()
+    bad[0, 2, 17] = float("nan")
+    with pytest.raises(ValueError, match="NaN"):
+        dfss.softmax_rows(dfss.CompressedSparse(c.rows, c.dense_cols, c.mode, bad, c.meta_hw))
+    inf = c.nonzeros.clone()
+    inf[0, 1, 5] = float("inf")
+    out = _np(dfss.softmax_rows(dfss.CompressedSparse(c.rows, c.dense_cols, c.mode, inf, c.meta_hw)).nonzeros)
+    assert np.isnan(out[0, 1]).any() and np.isfinite(out[0, 0]).all()
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_staged_12_tcgen05_attention_matches_reference(dtype):
+    """1:2 through the staged reference-shaped API on the tcgen05 kernels (16-bit, tiled shape):
+    sddmm_prune -> softmax_rows -> spmm equals the reference nm_attention at 2e-2."""
+    (q, k, v), (q64, k64, v64) = seeded_qkv((1, 3, 1024, 64), dtype, seed=8)
+    c, _ = dfss.sddmm_prune(q, k, "1:2", 0.125)
+    out = _np(dfss.spmm(dfss.softmax_rows(c), v).data)
+    assert_close(out, oracle_attention(q64, k64, v64, "1:2"), 2e-2, 2e-2, "staged 1:2 tcgen05")
+
+
 def test_softmax_rejects_nan_and_empty_rows():
     c = _row([0.0, 1.0])
     bad = dfss.CompressedSparse(c.rows, c.dense_cols, c.mode, torch.tensor([[float("nan"), 1.0]], device="cuda"),

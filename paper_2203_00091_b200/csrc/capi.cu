@@ -74,16 +74,17 @@ int dfss_sddmm_prune(const void* q, const void* k, void* nonzeros, uint32_t* met
   if (int st = check_keep(tile_keep, tile_rows, tile_cols, mode)) return st;
   if (!q || !k || !nonzeros || !meta_hw) return fail(DFSS_ERR_INVALID, "null tensor pointer");
   cudaStream_t s = (cudaStream_t)stream;
-  const bool tc_ok = !tile_keep && dfss::tc_sddmm_supported(mode, in_dtype, nz_dtype, n_q, n_k, d) &&
+  // (block masks on tcgen05 too: masked groups written absent in the epilogue; row maxima unmasked only)
+  const bool tc_ok = (!tile_keep || !row_max) && dfss::tc_sddmm_supported(mode, in_dtype, nz_dtype, n_q, n_k, d) &&
                      dfss_has_tcgen05();
   if (math == DFSS_MATH_TF32) {
     if (in_dtype != DFSS_F32 || !tc_ok) return fail(DFSS_ERR_UNSUPPORTED, "tf32 path needs fp32 inputs on a tiled shape");
     return cuda_status(dfss::launch_sddmm_tc(q, k, nonzeros, meta_hw, scale, mode, in_dtype, bh, n_q, n_k, d,
-                                             scores_dbg, row_max, s));
+                                             scores_dbg, row_max, s, tile_keep, tile_rows, tile_cols));
   }
   if (math == DFSS_MATH_AUTO && in_dtype != DFSS_F32 && tc_ok)
     return cuda_status(dfss::launch_sddmm_tc(q, k, nonzeros, meta_hw, scale, mode, in_dtype, bh, n_q, n_k, d,
-                                             scores_dbg, row_max, s));
+                                             scores_dbg, row_max, s, tile_keep, tile_rows, tile_cols));
   if (row_max) return fail(DFSS_ERR_UNSUPPORTED, "row_max is produced by the tcgen05 SDDMM only");
   return cuda_status(dfss::launch_sddmm_simt(q, k, nonzeros, meta_hw, scale, mode, in_dtype, nz_dtype, bh, n_q, n_k,
                                              d, tile_keep, tile_rows, tile_cols, scores_dbg, s));
@@ -218,6 +219,11 @@ int nm_attention_impl(const void* q, const void* k, const void* v, void* out, in
     if (st) return st;
     st = dfss_softmax_rows(nz, nz, dtype, dtype, bh, n, n / 2, tile_keep, tile_rows, tile_cols, nullptr, stream);
     if (st) return st;
+    // the masked softmax wrote exact zeros for every absent nonzero and nm_attention's V is finite
+    // (the reference's DenseMatrix rejects NaN / Inf, dense.py:34-35), so the unmasked tcgen05
+    // SpMM gives what skipping them gives
+    if (dfss::tc_spmm_supported(mode, dtype, dtype, dtype, n, n, d) && dfss_has_tcgen05())
+      return cuda_status(dfss::launch_spmm_tc(nz, meta, v, out, mode, dtype, dtype, bh, n, n, d, nullptr, s));
     return dfss_spmm(nz, meta, v, out, mode, dtype, dtype, dtype, bh, n, n, d, tile_keep, tile_rows, tile_cols,
                      nullptr, stream);
   }

@@ -189,7 +189,8 @@ cudaError_t launch_meta_logical_to_hw(const uint8_t* logical, uint32_t* hw, int 
                                       cudaStream_t s);
 // tcgen05 paths: return cudaErrorNotSupported when the shape is not covered.
 cudaError_t launch_sddmm_tc(const void* q, const void* k, void* nz, uint32_t* meta, float scale, int gs,
-                            int in_dtype, int64_t bh, int n, int m, int d, float* dbg, float* rowmax, cudaStream_t s);
+                            int in_dtype, int64_t bh, int n, int m, int d, float* dbg, float* rowmax, cudaStream_t s,
+                            const uint8_t* keep = nullptr, int tile_rows = 0, int tile_cols = 0);
 // rowmax (nullable): [bh, rows, 2] partial row maxima from the SDDMM; when given, the SpMM
 // applies softmax on the fly: P = exp(s - max) in smem, out = (P.V) / sum(P).
 cudaError_t launch_spmm_tc(const void* p, const uint32_t* meta, const void* v, void* out, int gs, int dtype,

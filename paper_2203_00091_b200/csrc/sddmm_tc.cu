@@ -55,13 +55,25 @@ __device__ __forceinline__ uint32_t pack2<__half>(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&p);
 }
 
+// BlockMask tile grid (codec.py:150-200) for the masked instantiations: a group in a masked tile
+// is structurally absent -- zero nonzeros and the padding nibble 0x4, as the FFMA kernel writes
+// it (_kernels_numba.py:110-185 skips masked tiles)
+struct TileKeepTc {
+  const uint8_t* keep = nullptr;
+  int tile_rows = 1, tile_cols = 1, grid_cols = 0;
+  __device__ __forceinline__ bool kept(int row, int col) const {
+    return keep[(row / tile_rows) * grid_cols + col / tile_cols] != 0;
+  }
+};
+
 // Prune one 32-column chunk of a row: 8 groups of 4 scores -> 16 kept 16-bit values
 // (two 16B units of the 128B-swizzled staging row) + one 32-bit nibble word that is
 // traded with row^8 into the meta_hw word of this TMEM lane (include/dfss.h).
-template <typename T, bool DBG, bool RMAX>
+template <typename T, bool DBG, bool RMAX, bool MASK>
 __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, int colh, int cc, int unit0,
                                           uint8_t* stg, uint32_t lane, uint32_t* meta_b, int row_blk, float* dbg,
-                                          int64_t dbg_row, int m, float& mx, uint32_t two) {
+                                          int64_t dbg_row, int m, float& mx, uint32_t two, const TileKeepTc& tk,
+                                          int grow) {
   uint32_t packed[8];
   // the select24 rule with the metadata in float arithmetic on the FMA-lite pipe (as in the
   // fused kernel, flash_tc.cu prune_exp_tile): exact 0 / 1 pair-winner flags from saturated
@@ -79,13 +91,17 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, 
     const float w23 = fmaxf(v2, v3), l23 = fminf(v2, v3);
     if (RMAX) mx = fmaxf(mx, fmaxf(w01, w23));
     const bool keep01 = l01 >= w23, keep23 = l23 > w01;
-    const float lo = keep01 ? v0 : (keep23 ? v2 : w01);
-    const float hi = keep01 ? v1 : (keep23 ? v3 : w23);
+    float lo = keep01 ? v0 : (keep23 ? v2 : w01);
+    float hi = keep01 ? v1 : (keep23 ? v3 : w23);
     const float fa = __saturatef(__fmul_rn(v0 - v1, -1.7014118e38f) * 1.7014118e38f);
     const float fb = __saturatef(__fmul_rn(v2 - v3, -1.7014118e38f) * 1.7014118e38f);
     float nf = fmaf(fb, 4.f, fa);
     nf = keep23 ? 6.f : nf;
     nf = keep01 ? -4.f : nf;
+    if (MASK && !tk.kept(grow, colh + cc * 32 + 4 * g)) {  // absent: zeros, padding nibble 0x4
+      lo = hi = 0.f;
+      nf = -4.f;
+    }
     wf[g >> 2] = fmaf(nf, (float)(1 << (4 * (g & 3))), wf[g >> 2]);
     packed[g] = pack2<T>(lo, hi);
   }
@@ -103,10 +119,10 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, 
 // 1:2 (codec.py:114-117: element 1 of a pair survives iff v1 > v0): the chunk's 16 pairs keep 16
 // values -- the same 16 per 32 columns as 2:4, so staging and the TMA store are unchanged -- and
 // their 16 nibbles (0x4 / 0xE) fill two meta_hw words (meta chunks of 8 pairs = 16 columns).
-template <typename T, bool DBG, bool RMAX>
+template <typename T, bool DBG, bool RMAX, bool MASK>
 __device__ __forceinline__ void epi_chunk12(const uint32_t (&r)[32], float scale, int colh, int cc, int unit0,
                                             uint8_t* stg, uint32_t lane, uint32_t* meta_b, int row_blk, float* dbg,
-                                            int64_t dbg_row, int m, float& mx) {
+                                            int64_t dbg_row, int m, float& mx, const TileKeepTc& tk, int grow) {
   uint32_t packed[8];
   uint32_t W[2] = {0u, 0u};
 #pragma unroll
@@ -117,7 +133,11 @@ __device__ __forceinline__ void epi_chunk12(const uint32_t (&r)[32], float scale
     const float v3 = scale_canon(__uint_as_float(r[4 * g + 3]), scale);
     if (DBG) *reinterpret_cast<float4*>(dbg + dbg_row * m + colh + cc * 32 + 4 * g) = make_float4(v0, v1, v2, v3);
     float k0, k1;
-    const uint32_t n0 = select12(v0, v1, k0), n1 = select12(v2, v3, k1);
+    uint32_t n0 = select12(v0, v1, k0), n1 = select12(v2, v3, k1);
+    if (MASK) {  // (tile columns are even: a pair never straddles two tiles)
+      if (!tk.kept(grow, colh + cc * 32 + 4 * g)) { n0 = 0x4u; k0 = 0.f; }
+      if (!tk.kept(grow, colh + cc * 32 + 4 * g + 2)) { n1 = 0x4u; k1 = 0.f; }
+    }
     if (RMAX) mx = fmaxf(mx, fmaxf(k0, k1));
     packed[g] = pack2<T>(k0, k1);
     W[g >> 2] += (n0 | (n1 << 4)) << (8 * (g & 3));
@@ -134,11 +154,12 @@ __device__ __forceinline__ void epi_chunk12(const uint32_t (&r)[32], float scale
   }
 }
 
-template <typename T, int GS, bool DBG, bool RMAX>
+template <typename T, int GS, bool DBG, bool RMAX, bool MASK>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     sddmm24_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_nz, uint32_t* __restrict__ meta, float scale, int bh,
-                      int n, int m, float* __restrict__ dbg, float* __restrict__ rowmax, uint32_t two) {
+                      int n, int m, float* __restrict__ dbg, float* __restrict__ rowmax, uint32_t two,
+                      TileKeepTc tk) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + SMEM_BAR);
@@ -269,9 +290,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // chunk cc+1 is in flight while cc is pruned
           auto chunk = [&](const uint32_t (&rr)[32], int cc) {
             if constexpr (GS == 4)
-              epi_chunk<T, DBG, RMAX>(rr, scale, colh, cc, 2 * cc, stg, lane, meta_b, row_blk, dbg, drow, m, mx, two);
+              epi_chunk<T, DBG, RMAX, MASK>(rr, scale, colh, cc, 2 * cc, stg, lane, meta_b, row_blk, dbg, drow, m, mx,
+                                            two, tk, grow);
             else
-              epi_chunk12<T, DBG, RMAX>(rr, scale, colh, cc, 2 * cc, stg, lane, meta_b, row_blk, dbg, drow, m, mx);
+              epi_chunk12<T, DBG, RMAX, MASK>(rr, scale, colh, cc, 2 * cc, stg, lane, meta_b, row_blk, dbg, drow, m,
+                                              mx, tk, grow);
           };
           tc::tmem_ld_32x32b_x32(tbase, ra);
           tc::tmem_ld_wait(ra);
@@ -336,34 +359,44 @@ static int num_sms() {
 
 template <typename T, int GS>
 static cudaError_t launch_typed(const void* q, const void* k, void* nz, uint32_t* meta, float scale, int64_t bh, int n,
-                                int m, float* dbg, float* rowmax, cudaStream_t s) {
+                                int m, float* dbg, float* rowmax, const TileKeepTc& tk, cudaStream_t s) {
   const CUtensorMapDataType dt =
       std::is_same<T, __nv_bfloat16>::value ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  CUtensorMap tq, tk, tn;
+  CUtensorMap tq, tkm, tn;
   if (!encode_tmap_3d(&tq, dt, 2, (void*)q, HD, n, bh, HD, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !encode_tmap_3d(&tk, dt, 2, (void*)k, HD, m, bh, HD, BN, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !encode_tmap_3d(&tkm, dt, 2, (void*)k, HD, m, bh, HD, BN, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !encode_tmap_3d(&tn, dt, 2, nz, m / 2, n, bh, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
-  auto kern = dbg ? (rowmax ? sddmm24_tc_kernel<T, GS, true, true> : sddmm24_tc_kernel<T, GS, true, false>)
-                 : (rowmax ? sddmm24_tc_kernel<T, GS, false, true> : sddmm24_tc_kernel<T, GS, false, false>);
+  auto kern = tk.keep ? (dbg ? sddmm24_tc_kernel<T, GS, true, false, true> : sddmm24_tc_kernel<T, GS, false, false, true>)
+            : dbg ? (rowmax ? sddmm24_tc_kernel<T, GS, true, true, false> : sddmm24_tc_kernel<T, GS, true, false, false>)
+                  : (rowmax ? sddmm24_tc_kernel<T, GS, false, true, false> : sddmm24_tc_kernel<T, GS, false, false, false>);
+  if (tk.keep && rowmax) return cudaErrorNotSupported;  // row maxima are unmasked-only
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
   if (e != cudaSuccess) return e;
   const int items = (int)bh * (n / BM);
   const int grid = items < num_sms() ? items : num_sms();
-  kern<<<grid, NUM_THREADS, SMEM_TOTAL, s>>>(tq, tk, tn, meta, scale, (int)bh, n, m, dbg, rowmax, 2u);
+  kern<<<grid, NUM_THREADS, SMEM_TOTAL, s>>>(tq, tkm, tn, meta, scale, (int)bh, n, m, dbg, rowmax, 2u, tk);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sddmm_tc(const void* q, const void* k, void* nz, uint32_t* meta, float scale, int gs, int in_dtype,
-                            int64_t bh, int n, int m, int d, float* dbg, float* rowmax, cudaStream_t s) {
+                            int64_t bh, int n, int m, int d, float* dbg, float* rowmax, cudaStream_t s,
+                            const uint8_t* keep, int tile_rows, int tile_cols) {
   if (!tc_sddmm_supported(gs, in_dtype, in_dtype, n, m, d)) return cudaErrorNotSupported;
   if (bh == 0) return cudaSuccess;
-  if (gs == 2) {
-    if (in_dtype == DFSS_BF16) return launch_typed<__nv_bfloat16, 2>(q, k, nz, meta, scale, bh, n, m, dbg, rowmax, s);
-    return launch_typed<__half, 2>(q, k, nz, meta, scale, bh, n, m, dbg, rowmax, s);
+  TileKeepTc tk;
+  if (keep) {
+    tk.keep = keep;
+    tk.tile_rows = tile_rows;
+    tk.tile_cols = tile_cols;
+    tk.grid_cols = (m + tile_cols - 1) / tile_cols;
   }
-  if (in_dtype == DFSS_BF16) return launch_typed<__nv_bfloat16, 4>(q, k, nz, meta, scale, bh, n, m, dbg, rowmax, s);
-  return launch_typed<__half, 4>(q, k, nz, meta, scale, bh, n, m, dbg, rowmax, s);
+  if (gs == 2) {
+    if (in_dtype == DFSS_BF16) return launch_typed<__nv_bfloat16, 2>(q, k, nz, meta, scale, bh, n, m, dbg, rowmax, tk, s);
+    return launch_typed<__half, 2>(q, k, nz, meta, scale, bh, n, m, dbg, rowmax, tk, s);
+  }
+  if (in_dtype == DFSS_BF16) return launch_typed<__nv_bfloat16, 4>(q, k, nz, meta, scale, bh, n, m, dbg, rowmax, tk, s);
+  return launch_typed<__half, 4>(q, k, nz, meta, scale, bh, n, m, dbg, rowmax, tk, s);
 }
 
 }  // namespace dfss

@@ -189,6 +189,56 @@ def test_sddmm_block_mask_matches_reference():
     assert not logical_meta(c)[~present].any()
 
 
+@pytest.mark.parametrize("mode", ["2:4", "1:2"])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_masked_sddmm_on_tcgen05_matches_reference(mode, dtype):
+    """Block-masked sddmm_prune on the tcgen05 kernel (16-bit, tiled shape): selection bit-exact on
+    the dumped scores for present groups, absent groups zero with no metadata (fused.py:73-82)."""
+    rng = np.random.default_rng(41)
+    n, m = 256, 384
+    keep = rng.random((n // 16, m // 16)) < 0.6
+    keep[:, 0] = True  # no empty row
+    mask = dfss.BlockMask(keep, tile_rows=16, tile_cols=16)
+    q = torch.from_numpy(rng.standard_normal((2, n, 64)).astype(np.float32)).to(dtype).cuda()
+    k = torch.from_numpy(rng.standard_normal((2, m, 64)).astype(np.float32)).to(dtype).cuda()
+    dbg = torch.empty((2, n, m), dtype=torch.float32, device="cuda")
+    c, _ = dfss.sddmm_prune(q, k, mode, 0.125, mask, tile_rows=16, tile_cols=16, scores_out=dbg)
+    present = mask.nonzero_keep(n, m)
+    meta = logical_meta(c)
+    for b in range(2):
+        want_nz, want_meta, _ = oracle_on_scores(_np(dbg[b]), mode)
+        gp = _group_present(present, mode)
+        assert np.array_equal(meta[b][gp], want_meta[gp])
+        assert not meta[b][~gp].any()
+        nzb = c.nonzeros[b].float().cpu().numpy()
+        assert np.array_equal(nzb[present], torch.from_numpy(want_nz[present].astype(np.float32)).to(dtype).float().numpy())
+        assert not nzb[~present].any()
+
+
+def _group_present(present_nz: np.ndarray, mode: str) -> np.ndarray:
+    """[rows, groups] presence from the [rows, nonzeros] presence (groups never straddle tiles)."""
+    per = 2 if mode == "2:4" else 1
+    return present_nz[:, ::per]
+
+
+@pytest.mark.parametrize("mode", ["2:4", "1:2"])
+def test_masked_staged_attention_on_tcgen05(mode):
+    """nm_attention with a block mask the fused kernel does not tile (16-column tiles) runs the
+    staged path -- masked tcgen05 SDDMM, masked softmax, tcgen05 SpMM over the zeroed absent
+    entries -- and matches the reference masked pipeline."""
+    rng = np.random.default_rng(5)
+    n = 512
+    keep = rng.random((n // 32, n // 16)) < 0.5
+    keep[np.arange(n // 32), np.arange(n // 32) * 2] = True
+    mask = dfss.BlockMask(keep, tile_rows=32, tile_cols=16)
+    (q, k, v), (q64, k64, v64) = seeded_qkv((1, 2, n, 64), torch.bfloat16, seed=12)
+    assert dfss.attention_path(mode, q.dtype, n, 64, block_mask=mask).startswith("staged")
+    out = _np(dfss.dfss_attention(q, k, v, mode, block_mask=mask))
+    for h in range(2):
+        assert_close(out[0, h], _masked_oracle(q64[0, h], k64[0, h], v64[0, h], mask, mode), 2e-2, 2e-2,
+                     f"masked staged {mode} head {h}")
+
+
 # ---------------------------------------------------------------- softmax
 
 

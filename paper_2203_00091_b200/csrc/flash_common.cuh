@@ -31,6 +31,21 @@ __device__ __forceinline__ void fma2s(float a0, float a1, float c, float b, floa
       : "f"(a0), "f"(a1), "f"(c), "f"(b));
 }
 
+// (a0, a1) * c + (b0, b1)
+__device__ __forceinline__ void fma2v(float a0, float a1, float c, float b0, float b1, float& d0, float& d1) {
+  asm("{\n\t.reg .b64 a, cc, bb, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 cc, {%4, %4};\n\tmov.b64 bb, {%5, %6};\n\t"
+      "fma.rn.f32x2 d, a, cc, bb;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(c), "f"(b0), "f"(b1));
+}
+// (a0, a1) * c
+__device__ __forceinline__ void mul2s(float a0, float a1, float c, float& d0, float& d1) {
+  asm("{\n\t.reg .b64 a, cc, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 cc, {%4, %4};\n\t"
+      "mul.rn.f32x2 d, a, cc;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(c));
+}
+
 __device__ __forceinline__ float fex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -62,6 +77,11 @@ __device__ __forceinline__ bool bar_any(uint32_t id, uint32_t count, bool pred) 
 // role-warp wait: try_wait with a suspend-time hint (the waiting warp yields its issue slots)
 #ifdef DFSS_EXP_ROLE_SPIN  // timing experiment: role warps spin on try_wait without a suspend hint
 __device__ __forceinline__ void wait_role(uint64_t* bar, uint32_t parity) { tc::mbar_wait(bar, parity); }
+#elif defined(DFSS_EXP_ROLE_BACKOFF)  // timing experiment: test_wait + fixed nanosleep
+__device__ __forceinline__ void wait_role(uint64_t* bar, uint32_t parity) {
+  if (tc::mbar_test(bar, parity)) return;
+  tc::mbar_wait_backoff(bar, parity, DFSS_EXP_ROLE_BACKOFF);
+}
 #else
 __device__ __forceinline__ void wait_role(uint64_t* bar, uint32_t parity) { tc::mbar_wait_sleep(bar, parity); }
 #endif

@@ -111,10 +111,11 @@ struct SplitPlan {
 // rule), exponentiates the kept half against the shift `mlog` (= m * c), packs P, builds the
 // metadata word W (group g at bits 4g) and the partial sum.
 //
-// Instruction budget per group (the kernel is bound by the ALU pipe, 2 clk per warp
-// instruction per sub-partition, like the FMA pipe): 4 FMNMX + 2 FSETP + 2 predicated FSEL on
-// the ALU; FADD x2 + IMAD.HI x2 (pair winners' sign bits) + IMAD (nibble) + FFMA2 + FADD2 on
-// the FMA pipe; 2 MUFU.EX2; F2FP.  Key-order registers make the kept pair land in the
+// Instruction budget per group (the kernel is bound by instruction issue: 23 warp instructions
+// per group, tools/sass_region.py): ALU -- 4 FMNMX, 2 FSETP, 4 FSEL (lo, hi, two nibble
+// overrides), F2FP; FMA pipe -- 2 FADD (pair differences), FMUL2 + 2 FMUL.SAT (pair-winner
+// flags), 2 FFMA (nibble), FFMA2 (exponent arguments), FADD2 (row sums); XU -- 2 MUFU.EX2.
+// Key-order registers make the kept pair land in the
 // registers of (v0, v1) -- an aligned pair for FFMA2 -- and each of lo / hi is one FSEL
 // predicated on "that register's own value is not the kept one" (keep01 keeps v0 / v1).
 //
@@ -164,8 +165,13 @@ __device__ __forceinline__ void prune_exp_tile(const uint32_t (&s)[32], float c,
       hi = keep01 ? v1 : (keep23 ? v3 : w23);
       // a = [v1 > v0], b = [v3 > v2] as exact 0 / 1 floats: sat(d * -2^127 * 2^127) is 1 for
       // every d < 0 down to the smallest subnormal and 0 for d >= 0 (ties: d = +0 -> lower index)
-      const float fa = __saturatef(__fmul_rn(d01, -1.7014118e38f) * 1.7014118e38f);
-      const float fb = __saturatef(__fmul_rn(d23, -1.7014118e38f) * 1.7014118e38f);
+      // (the first multiplies of both pairs are one FMUL2: c4 -2 %, c2 -2 %; pairing groups g and
+      // g + 4 for the nibble FFMAs as well saved another instruction per group statically but ran
+      // 1-2 % slower)
+      float t01, t23;
+      mul2s(d01, d23, -1.7014118e38f, t01, t23);
+      const float fa = __saturatef(t01 * 1.7014118e38f);
+      const float fb = __saturatef(t23 * 1.7014118e38f);
       // nibble - 8: 0x4 -> -4, 0xE -> 6, mixed 8 + a + 4b -> a + 4b
       float n = fmaf(fb, 4.f, fa);
       n = keep23 ? 6.f : n;

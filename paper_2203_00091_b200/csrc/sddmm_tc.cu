@@ -20,6 +20,7 @@
 #include <type_traits>
 
 #include "dfss_common.cuh"
+#include "flash_common.cuh"  // packed fp32 helpers (FMUL2 / FFMA2)
 #include "tc_common.cuh"
 
 namespace dfss {
@@ -93,8 +94,10 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, 
     const bool keep01 = l01 >= w23, keep23 = l23 > w01;
     float lo = keep01 ? v0 : (keep23 ? v2 : w01);
     float hi = keep01 ? v1 : (keep23 ? v3 : w23);
-    const float fa = __saturatef(__fmul_rn(v0 - v1, -1.7014118e38f) * 1.7014118e38f);
-    const float fb = __saturatef(__fmul_rn(v2 - v3, -1.7014118e38f) * 1.7014118e38f);
+    float t01, t23;
+    mul2s(v0 - v1, v2 - v3, -1.7014118e38f, t01, t23);  // both first multiplies in one FMUL2
+    const float fa = __saturatef(t01 * 1.7014118e38f);
+    const float fb = __saturatef(t23 * 1.7014118e38f);
     float nf = fmaf(fb, 4.f, fa);
     nf = keep23 ? 6.f : nf;
     nf = keep01 ? -4.f : nf;

@@ -1,4 +1,8 @@
 """Time the fused kernel with no mask, an all-kept mask, and block-causal masks."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 import paper_2203_00091_b200 as dfss

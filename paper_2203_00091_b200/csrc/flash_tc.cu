@@ -624,16 +624,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* k_empty = k_full + K2ST;      // [K2ST]
   uint64_t* v_full = k_empty + K2ST;      // [V2ST]
   uint64_t* v_empty = v_full + V2ST;      // [V2ST]
-  // [2 halves][S2RING] S of a step computed.  Per half, like p_full: when one set runs several
-  // live steps in a row (masks, an empty half) a shared slot barrier could complete two phases
-  // past a waiting set, whose parity wait would then succeed on the wrong step.
+  // [2 halves][S2RING] S of a step computed.  Per half: when one set runs several live steps in
+  // a row (masks, an empty half) a shared slot barrier could complete two phases past a waiting
+  // set, whose parity wait would then succeed on the wrong step.  (P + metadata of a step
+  // written is signalled on named barriers 9.. 14, per half, see the PV issuer.)
   uint64_t* s_full = v_empty + V2ST;
   uint64_t* s_free = s_full + 2 * S2RING; // [S2RING] PV of that step retired (buffer free)
-  // [2 halves][S2RING] P + metadata of a step written (8 warps).  Per half, not per slot only:
-  // each PV issuer may run a step ahead of the other set, and a shared slot barrier would
-  // then satisfy its wait with the other set's previous phase (parity aliasing).
-  uint64_t* p_full = s_free + S2RING;
-  uint64_t* o_full = p_full + 2 * S2RING; // [2 halves]
+  uint64_t* o_full = s_free + S2RING;     // [2 halves]
   uint64_t* o_empty = o_full + 2;         // [2 halves] (8 warps)
   uint64_t* pv_done = o_empty + 2;        // [2 halves] every PV of this half so far retired
   uint32_t* tmem_slot = (uint32_t*)(pv_done + 2);
@@ -724,7 +721,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int i = 0; i < S2RING; ++i) tc::mbar_init(&s_free[i], 1);
     for (int i = 0; i < 2 * S2RING; ++i) tc::mbar_init(&s_full[i], 1);
-    for (int i = 0; i < 2 * S2RING; ++i) tc::mbar_init(&p_full[i], 8);
     for (int i = 0; i < K2ST; ++i) {
       tc::mbar_init(&k_full[i], 1);
       tc::mbar_init(&k_empty[i], 1);
@@ -830,7 +826,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       constexpr uint32_t fmt = std::is_same<T, __nv_bfloat16>::value ? 1u : 0u;
       constexpr uint32_t idesc_pv = tc::instr_desc(fmt, BM, HD, false, true, true);
       int vs = 0, it = 0;
-      uint32_t vph = 0, gcount = 0, pbits = 0;  // live steps so far (both halves); p_full phase per slot
+      uint32_t vph = 0, gcount = 0, hc = 0;  // live steps so far (both halves / this half)
       int item, t0, t1, part;
       for (int kk_ = 0; unit_at(kk_, item, t0, t1, part); ++kk_, ++it) {
         uint32_t lw0 = 0, lw1 = 0;
@@ -861,8 +857,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           await_o_free();
           wait_role(&v_full[vs], vph);
-          wait_role(&p_full[h * S2RING + slot], (pbits >> slot) & 1);
-          pbits ^= 1u << slot;
+          // P of this half's hc-th live step published: named barrier 9 + 3h + hc % 3 over the
+          // set's 8 warps (bar.arrive) and this warp -- a hardware wait that issues nothing while
+          // it blocks (an mbarrier wait re-polled at each of the 8 arrivals: c4 -1.4 %, c2 -1 %).
+          // Three ids per half rotate; the set cannot run more than one live step ahead of this
+          // wait (its next S needs K(t+1), which the producer loads only after V(t), whose
+          // load this issuer awaits before it), so an id is never re-armed early.
+          ++hc;
+          tc::named_bar_sync(9 + 3 * h + hc % 3, 288);
           if (lane == 0) FTRACE(6, it, t, h);
           tc::tc_fence_after();
           const uint32_t v_addr = tc::smem_u32(smem + S2_V + vs * V_BYTES);
@@ -900,9 +902,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // the per-step barriers as 32-bit shared addresses (see tc::mbar_wait_u32)
     // (materialised through asm so the compiler keeps them instead of re-deriving them from the
     // generic smem pointer -- window base + alignment -- at every use)
-    uint32_t s_full32, p_full32;
+    uint32_t s_full32;
     asm volatile("mov.b32 %0, %1;" : "=r"(s_full32) : "r"(tc::smem_u32(s_full)));
-    asm volatile("mov.b32 %0, %1;" : "=r"(p_full32) : "r"(tc::smem_u32(p_full)));
     // ------------------------------------------------------------ softmax / prune / epilogue sets
     const int h = warp >> 3;              // half owned by this set
     const int pr = (warp >> 2) & 1;       // column pair: quarters 2pr, 2pr + 1
@@ -1117,7 +1118,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc::tmem_st_wait();
           tc::tc_fence_before();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive_u32(p_full32 + 8 * (h * S2RING + slot));
+          tc::named_bar_arrive(9 + 3 * h + hcount % 3, 288);  // P published (PV issuer of this half)
         };
         if (!MASKED && pend) {
           // the previous item's O_h leaves TMEM before this item's first P goes out (that P's PV

@@ -17,6 +17,8 @@
 // Work item = (bh, 128-row block); items are strided over the persistent CTAs.
 #include <stdio.h>
 
+#include <cmath>
+
 #include <type_traits>
 
 #include "dfss_common.cuh"
@@ -31,11 +33,11 @@ constexpr int BN = 256;
 constexpr int HD = 64;
 constexpr int KSTAGES = 3;
 constexpr int NACC = 2;
-constexpr int EPI_WARPS = 8;
+constexpr int EPI_WARPS = 16;  // (lane quarter, 64-column quarter) of the 128 x 256 tile
 constexpr int NUM_THREADS = (4 + EPI_WARPS) * 32;
 constexpr int Q_BYTES = BM * HD * 2;
 constexpr int K_BYTES = BN * HD * 2;
-constexpr int STG_BYTES = 32 * 128;  // 32 rows x 64 nonzeros x 2 B
+constexpr int STG_BYTES = 32 * 64;  // 32 rows x 32 nonzeros x 2 B (64B-swizzled rows)
 constexpr int SMEM_Q = 0;
 constexpr int SMEM_K = SMEM_Q + 2 * Q_BYTES;
 constexpr int SMEM_STG = SMEM_K + KSTAGES * K_BYTES;
@@ -68,9 +70,9 @@ struct TileKeepTc {
 };
 
 // Prune one 32-column chunk of a row: 8 groups of 4 scores -> 16 kept 16-bit values
-// (two 16B units of the 128B-swizzled staging row) + one 32-bit nibble word that is
+// (two 16B units of the 64B-swizzled staging row) + one 32-bit nibble word that is
 // traded with row^8 into the meta_hw word of this TMEM lane (include/dfss.h).
-template <typename T, bool DBG, bool RMAX, bool MASK>
+template <typename T, bool DBG, bool RMAX, bool MASK, bool PRE>
 __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, int colh, int cc, int unit0,
                                           uint8_t* stg, uint32_t lane, uint32_t* meta_b, int row_blk, float* dbg,
                                           int64_t dbg_row, int m, float& mx, uint32_t two, const TileKeepTc& tk,
@@ -83,19 +85,25 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, 
   float wf[2] = {8388608.f + 34952.f, 8388608.f + 34952.f};
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
-    const float v0 = scale_canon(__uint_as_float(r[4 * g + 0]), scale);
-    const float v1 = scale_canon(__uint_as_float(r[4 * g + 1]), scale);
-    const float v2 = scale_canon(__uint_as_float(r[4 * g + 2]), scale);
-    const float v3 = scale_canon(__uint_as_float(r[4 * g + 3]), scale);
+    // PRE: Q was scaled in shared memory (exact power of two), the accumulator holds the
+    // post-scale scores (tcgen05 writes zero sums as +0: already canonical)
+    const float v0 = PRE ? __uint_as_float(r[4 * g + 0]) : scale_canon(__uint_as_float(r[4 * g + 0]), scale);
+    const float v1 = PRE ? __uint_as_float(r[4 * g + 1]) : scale_canon(__uint_as_float(r[4 * g + 1]), scale);
+    const float v2 = PRE ? __uint_as_float(r[4 * g + 2]) : scale_canon(__uint_as_float(r[4 * g + 2]), scale);
+    const float v3 = PRE ? __uint_as_float(r[4 * g + 3]) : scale_canon(__uint_as_float(r[4 * g + 3]), scale);
     if (DBG) *reinterpret_cast<float4*>(dbg + dbg_row * m + colh + cc * 32 + 4 * g) = make_float4(v0, v1, v2, v3);
     const float w01 = fmaxf(v0, v1), l01 = fminf(v0, v1);
     const float w23 = fmaxf(v2, v3), l23 = fminf(v2, v3);
     if (RMAX) mx = fmaxf(mx, fmaxf(w01, w23));
     const bool keep01 = l01 >= w23, keep23 = l23 > w01;
-    float lo = keep01 ? v0 : (keep23 ? v2 : w01);
-    float hi = keep01 ? v1 : (keep23 ? v3 : w23);
     float t01, t23;
     mul2s(v0 - v1, v2 - v3, -1.7014118e38f, t01, t23);  // both first multiplies in one FMUL2
+    // kept pair: (v0, v1) unless another case applies -- one predicated select per value
+    float lo = v0, hi = v1;
+    if (!keep01) {
+      lo = keep23 ? v2 : w01;
+      hi = keep23 ? v3 : w23;
+    }
     const float fa = __saturatef(t01 * 1.7014118e38f);
     const float fb = __saturatef(t23 * 1.7014118e38f);
     float nf = fmaf(fb, 4.f, fa);
@@ -110,9 +118,11 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, 
   }
   const uint32_t W = __byte_perm(__float_as_uint(wf[0]), __float_as_uint(wf[1]), 0x5410);
   (void)two;
-  const int u0 = unit0, sw = lane & 7;
-  *reinterpret_cast<uint4*>(stg + lane * 128 + ((u0 ^ sw) << 4)) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-  *reinterpret_cast<uint4*>(stg + lane * 128 + (((u0 + 1) ^ sw) << 4)) =
+  // 64B-swizzled staging row of this lane: 16-byte unit u at (u ^ ((row >> 1) & 3)) -- the
+  // 8 lanes of a store phase hit 8 distinct 16B bank groups
+  const int u0 = unit0, sw = (lane >> 1) & 3;
+  *reinterpret_cast<uint4*>(stg + lane * 64 + ((u0 ^ sw) << 4)) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+  *reinterpret_cast<uint4*>(stg + lane * 64 + (((u0 + 1) ^ sw) << 4)) =
       make_uint4(packed[4], packed[5], packed[6], packed[7]);
   const uint32_t partner = __shfl_xor_sync(0xffffffffu, W, 8);
   const uint32_t word = (lane & 8) ? ((partner >> 16) | (W & 0xFFFF0000u)) : ((W & 0xFFFFu) | (partner << 16));
@@ -122,7 +132,7 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, 
 // 1:2 (codec.py:114-117: element 1 of a pair survives iff v1 > v0): the chunk's 16 pairs keep 16
 // values -- the same 16 per 32 columns as 2:4, so staging and the TMA store are unchanged -- and
 // their 16 nibbles (0x4 / 0xE) fill two meta_hw words (meta chunks of 8 pairs = 16 columns).
-template <typename T, bool DBG, bool RMAX, bool MASK>
+template <typename T, bool DBG, bool RMAX, bool MASK, bool PRE>
 __device__ __forceinline__ void epi_chunk12(const uint32_t (&r)[32], float scale, int colh, int cc, int unit0,
                                             uint8_t* stg, uint32_t lane, uint32_t* meta_b, int row_blk, float* dbg,
                                             int64_t dbg_row, int m, float& mx, const TileKeepTc& tk, int grow) {
@@ -130,10 +140,12 @@ __device__ __forceinline__ void epi_chunk12(const uint32_t (&r)[32], float scale
   uint32_t W[2] = {0u, 0u};
 #pragma unroll
   for (int g = 0; g < 8; ++g) {  // g: pairs 2g, 2g + 1
-    const float v0 = scale_canon(__uint_as_float(r[4 * g + 0]), scale);
-    const float v1 = scale_canon(__uint_as_float(r[4 * g + 1]), scale);
-    const float v2 = scale_canon(__uint_as_float(r[4 * g + 2]), scale);
-    const float v3 = scale_canon(__uint_as_float(r[4 * g + 3]), scale);
+    // PRE: Q was scaled in shared memory (exact power of two), the accumulator holds the
+    // post-scale scores (tcgen05 writes zero sums as +0: already canonical)
+    const float v0 = PRE ? __uint_as_float(r[4 * g + 0]) : scale_canon(__uint_as_float(r[4 * g + 0]), scale);
+    const float v1 = PRE ? __uint_as_float(r[4 * g + 1]) : scale_canon(__uint_as_float(r[4 * g + 1]), scale);
+    const float v2 = PRE ? __uint_as_float(r[4 * g + 2]) : scale_canon(__uint_as_float(r[4 * g + 2]), scale);
+    const float v3 = PRE ? __uint_as_float(r[4 * g + 3]) : scale_canon(__uint_as_float(r[4 * g + 3]), scale);
     if (DBG) *reinterpret_cast<float4*>(dbg + dbg_row * m + colh + cc * 32 + 4 * g) = make_float4(v0, v1, v2, v3);
     float k0, k1;
     uint32_t n0 = select12(v0, v1, k0), n1 = select12(v2, v3, k1);
@@ -145,9 +157,11 @@ __device__ __forceinline__ void epi_chunk12(const uint32_t (&r)[32], float scale
     packed[g] = pack2<T>(k0, k1);
     W[g >> 2] += (n0 | (n1 << 4)) << (8 * (g & 3));
   }
-  const int u0 = unit0, sw = lane & 7;
-  *reinterpret_cast<uint4*>(stg + lane * 128 + ((u0 ^ sw) << 4)) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-  *reinterpret_cast<uint4*>(stg + lane * 128 + (((u0 + 1) ^ sw) << 4)) =
+  // 64B-swizzled staging row of this lane: 16-byte unit u at (u ^ ((row >> 1) & 3)) -- the
+  // 8 lanes of a store phase hit 8 distinct 16B bank groups
+  const int u0 = unit0, sw = (lane >> 1) & 3;
+  *reinterpret_cast<uint4*>(stg + lane * 64 + ((u0 ^ sw) << 4)) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+  *reinterpret_cast<uint4*>(stg + lane * 64 + (((u0 + 1) ^ sw) << 4)) =
       make_uint4(packed[4], packed[5], packed[6], packed[7]);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -157,7 +171,7 @@ __device__ __forceinline__ void epi_chunk12(const uint32_t (&r)[32], float scale
   }
 }
 
-template <typename T, int GS, bool DBG, bool RMAX, bool MASK>
+template <typename T, int GS, bool DBG, bool RMAX, bool MASK, bool PRE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     sddmm24_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                       const __grid_constant__ CUtensorMap tm_nz, uint32_t* __restrict__ meta, float scale, int bh,
@@ -172,7 +186,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* k_empty = k_full + KSTAGES;    // [KSTAGES]
   uint64_t* t_full = k_empty + KSTAGES;    // [NACC]
   uint64_t* t_empty = t_full + NACC;       // [NACC]
-  uint32_t* tmem_slot = (uint32_t*)(t_empty + NACC);
+  uint64_t* q_ready = t_empty + NACC;     // [2] PRE: Q tile scaled in shared memory
+  uint32_t* tmem_slot = (uint32_t*)(q_ready + 2);
 
   const uint32_t warp = tc::warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -196,6 +211,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc::mbar_init(&t_full[i], 1);
       tc::mbar_init(&t_empty[i], EPI_WARPS);
     }
+    for (int i = 0; i < 2; ++i) tc::mbar_init(&q_ready[i], 1);
     tc::fence_barrier_init();
   }
   if (warp == 2) tc::tmem_alloc<512>(tmem_slot);
@@ -237,7 +253,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
         const int qs = it & 1;
         const uint32_t qph = (it >> 1) & 1;
-        tc::mbar_wait_sleep(&q_full[qs], qph);
+        tc::mbar_wait_sleep(PRE ? &q_ready[qs] : &q_full[qs], qph);
         const uint32_t q_addr = tc::smem_u32(smem + SMEM_Q + qs * Q_BYTES);
         for (int t = 0; t < ntiles; ++t) {
           const uint32_t idesc = (m - t * BN >= BN) ? idesc256 : idesc128;
@@ -260,13 +276,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc::mma_commit(&q_empty[qs]);
       }
     }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ Q scaler (PRE)
+    // the attention scale is an exact power of two and the inputs bf16 (fp32's exponent range):
+    // Q * scale is exact, so the MMA accumulates the post-scale scores directly and the epilogue
+    // drops its per-score multiply (4 of ~29 instructions per group)
+    if (PRE) {
+      const __nv_bfloat162 s2 = __float2bfloat162_rn(scale);
+      int it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
+        const int qs = it & 1;
+        tc::mbar_wait_sleep(&q_full[qs], (it >> 1) & 1);
+        uint4* qv = reinterpret_cast<uint4*>(smem + SMEM_Q + qs * Q_BYTES);
+#pragma unroll 4
+        for (int i = lane; i < Q_BYTES / 16; i += 32) {
+          uint4 u = qv[i];
+          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) h[j] = __hmul2(h[j], s2);
+          qv[i] = u;
+        }
+        tc::fence_proxy_async();  // generic-proxy writes -> the tensor core's async-proxy reads
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&q_ready[qs]);
+      }
+    }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
-    // warp (quad, half) owns TMEM lanes 32*quad.. (its 32 query rows) and accumulator
-    // columns [128*half, 128*half+128): 4 chunks of 32 columns, TMEM loads double-buffered.
+    // warp (quad, cq) owns TMEM lanes 32*quad.. (its 32 query rows) and accumulator columns
+    // [64*cq, 64*cq+64): 2 chunks of 32 columns, the second TMEM load in flight while the first
+    // is pruned.  16 epilogue warps (4 per sub-partition) hide the epilogue's latencies.
     const int ew = warp - 4;
     const int quad = warp & 3;
-    const int half = ew >> 2;
+    const int cq = ew >> 2;
     const int chunks = m / (8 * GS);  // meta chunks of 8 groups per row block
     uint8_t* stg_base = smem + SMEM_STG + ew * 2 * STG_BYTES;
     int acc = 0, sb = 0;
@@ -279,24 +321,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       float mx = -INFINITY;  // running max of this thread's row half (RMAX)
       for (int t = 0; t < ntiles; ++t) {
         const int width = min(BN, m - t * BN);
-        const bool active = half * 128 < width;
+        const bool active = cq * 64 < width;
         tc::mbar_wait(&t_full[acc], aph);
         tc::tc_fence_after();
         uint8_t* stg = stg_base + sb * STG_BYTES;
         if (active) {
           if (lane == 0) tc::bulk_wait_read<1>();  // staging buffer from two tiles ago drained
           __syncwarp();
-          const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + half * 128;
-          const int colh = t * BN + half * 128;
+          const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + cq * 64;
+          const int colh = t * BN + cq * 64;
           const int64_t drow = (int64_t)b * n + grow;
           uint32_t ra[32], rb[32];
           // chunk cc+1 is in flight while cc is pruned
           auto chunk = [&](const uint32_t (&rr)[32], int cc) {
             if constexpr (GS == 4)
-              epi_chunk<T, DBG, RMAX, MASK>(rr, scale, colh, cc, 2 * cc, stg, lane, meta_b, row_blk, dbg, drow, m, mx,
+              epi_chunk<T, DBG, RMAX, MASK, PRE>(rr, scale, colh, cc, 2 * cc, stg, lane, meta_b, row_blk, dbg, drow, m, mx,
                                             two, tk, grow);
             else
-              epi_chunk12<T, DBG, RMAX, MASK>(rr, scale, colh, cc, 2 * cc, stg, lane, meta_b, row_blk, dbg, drow, m,
+              epi_chunk12<T, DBG, RMAX, MASK, PRE>(rr, scale, colh, cc, 2 * cc, stg, lane, meta_b, row_blk, dbg, drow, m,
                                               mx, tk, grow);
           };
           tc::tmem_ld_32x32b_x32(tbase, ra);
@@ -304,13 +346,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc::tmem_ld_32x32b_x32(tbase + 32, rb);
           chunk(ra, 0);
           tc::tmem_ld_wait(rb);
-          tc::tmem_ld_32x32b_x32(tbase + 64, ra);
           chunk(rb, 1);
-          tc::tmem_ld_wait(ra);
-          tc::tmem_ld_32x32b_x32(tbase + 96, rb);
-          chunk(ra, 2);
-          tc::tmem_ld_wait(rb);
-          chunk(rb, 3);
         }
         tc::tc_fence_before();
         __syncwarp();
@@ -319,18 +355,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc::fence_proxy_async();
           __syncwarp();
           if (lane == 0) {
-            tc::tma_store_3d(&tm_nz, stg, t * (BN / 2) + half * 64, mb * BM + quad * 32, b);
+            tc::tma_store_3d(&tm_nz, stg, t * (BN / 2) + cq * 32, mb * BM + quad * 32, b);
             tc::bulk_commit();
           }
           sb ^= 1;
         }
         if (++acc == NACC) { acc = 0; aph ^= 1; }
       }
-      // per-row partial maxima [bh, n, 4] fp32 (fused softmax input); halves 2,3 unused here
-      if (RMAX) {
-        rowmax[((int64_t)b * n + grow) * 4 + half] = mx;
-        rowmax[((int64_t)b * n + grow) * 4 + 2 + half] = -INFINITY;
-      }
+      // per-row partial maxima [bh, n, 4] fp32, one per column quarter (fused softmax input)
+      if (RMAX) rowmax[((int64_t)b * n + grow) * 4 + cq] = mx;
     }
     if (lane == 0) tc::bulk_wait<0>();
   }
@@ -360,6 +393,19 @@ static int num_sms() {
   return cached;
 }
 
+template <typename T, int GS, bool PRE>
+static auto pick_kernel(bool mask, bool dbg, bool rowmax) -> decltype(&sddmm24_tc_kernel<T, GS, false, false, false, PRE>) {
+  if (mask) return dbg ? sddmm24_tc_kernel<T, GS, true, false, true, PRE> : sddmm24_tc_kernel<T, GS, false, false, true, PRE>;
+  if (dbg) return rowmax ? sddmm24_tc_kernel<T, GS, true, true, false, PRE> : sddmm24_tc_kernel<T, GS, true, false, false, PRE>;
+  return rowmax ? sddmm24_tc_kernel<T, GS, false, true, false, PRE> : sddmm24_tc_kernel<T, GS, false, false, false, PRE>;
+}
+
+// scale = 2^e, e <= 0, normal: Q * scale is exact in bf16 (fp32's exponent range)
+static bool exact_prescale(float scale) {
+  int e = 0;
+  return std::isfinite(scale) && scale > 0.f && scale <= 1.f && scale >= 1e-30f && std::frexp(scale, &e) == 0.5f;
+}
+
 template <typename T, int GS>
 static cudaError_t launch_typed(const void* q, const void* k, void* nz, uint32_t* meta, float scale, int64_t bh, int n,
                                 int m, float* dbg, float* rowmax, const TileKeepTc& tk, cudaStream_t s) {
@@ -368,11 +414,11 @@ static cudaError_t launch_typed(const void* q, const void* k, void* nz, uint32_t
   CUtensorMap tq, tkm, tn;
   if (!encode_tmap_3d(&tq, dt, 2, (void*)q, HD, n, bh, HD, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !encode_tmap_3d(&tkm, dt, 2, (void*)k, HD, m, bh, HD, BN, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !encode_tmap_3d(&tn, dt, 2, nz, m / 2, n, bh, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+      !encode_tmap_3d(&tn, dt, 2, nz, m / 2, n, bh, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorInvalidValue;
-  auto kern = tk.keep ? (dbg ? sddmm24_tc_kernel<T, GS, true, false, true> : sddmm24_tc_kernel<T, GS, false, false, true>)
-            : dbg ? (rowmax ? sddmm24_tc_kernel<T, GS, true, true, false> : sddmm24_tc_kernel<T, GS, true, false, false>)
-                  : (rowmax ? sddmm24_tc_kernel<T, GS, false, true, false> : sddmm24_tc_kernel<T, GS, false, false, false>);
+  auto kern = pick_kernel<T, GS, false>(tk.keep != nullptr, dbg != nullptr, rowmax != nullptr);
+  if constexpr (std::is_same<T, __nv_bfloat16>::value)
+    if (exact_prescale(scale)) kern = pick_kernel<T, GS, true>(tk.keep != nullptr, dbg != nullptr, rowmax != nullptr);
   if (tk.keep && rowmax) return cudaErrorNotSupported;  // row maxima are unmasked-only
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
   if (e != cudaSuccess) return e;

@@ -140,6 +140,29 @@ def test_sddmm_same_scores_bitexact(mode, dtype, math_mode):
                 assert torch.equal(nz[b].cpu(), torch.from_numpy(want_nz.astype(np.float32)).to(nz.dtype))
 
 
+@pytest.mark.parametrize("mode", ["1:2", "2:4"])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("scale", [0.125, 0.1, 1.0, 2.0 ** -7])
+def test_sddmm_tcgen05_scales_bitexact(mode, dtype, scale):
+    """tcgen05 SDDMM at d = 64 with power-of-two scales (bf16: Q scaled in shared memory, the
+    epilogue reads post-scale scores) and other scales (per-score multiply): selection and
+    nonzeros bit-exact on the dumped scores, the dump equal to scale * Q K^T within fp32."""
+    m = MODES[mode]
+    g = torch.Generator().manual_seed(int(scale * 1000) + 7)
+    q = torch.randn((2, 256, 64), generator=g).to(dtype).cuda()
+    k = torch.randn((2, 384, 64), generator=g).to(dtype).cuda()
+    dbg = torch.empty((2, 256, 384), dtype=torch.float32, device="cuda")
+    c, _ = dfss.sddmm_prune(q, k, m, scale, scores_out=dbg)
+    s = _np(dbg)
+    exact = np.einsum("bnd,bmd->bnm", _np(q), _np(k)) * scale
+    assert_close(s, exact, 1e-5, 1e-5 * max(1.0, float(np.abs(exact).max())), "scores")
+    meta = logical_meta(c)
+    for b in range(2):
+        want_nz, want_meta, _ = oracle_on_scores(s[b], mode)
+        assert np.array_equal(meta[b], want_meta)
+        assert torch.equal(c.nonzeros[b].cpu(), torch.from_numpy(want_nz.astype(np.float32)).to(dtype))
+
+
 def test_sddmm_reference_golden_cases():
     """The reference's own fused instances (fp64) run in fp32: integer-lattice cases are
     exact in fp32 and must match the reference bitwise; the others match the oracle on the

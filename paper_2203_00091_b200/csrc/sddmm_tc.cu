@@ -77,6 +77,7 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, 
                                           uint8_t* stg, uint32_t lane, uint32_t* meta_b, int row_blk, float* dbg,
                                           int64_t dbg_row, int m, float& mx, uint32_t two, const TileKeepTc& tk,
                                           int grow) {
+  constexpr bool SK = PRE && std::is_same<T, __half>::value;  // scale the kept values
   uint32_t packed[8];
   // the select24 rule with the metadata in float arithmetic on the FMA-lite pipe (as in the
   // fused kernel, flash_tc.cu prune_exp_tile): exact 0 / 1 pair-winner flags from saturated
@@ -85,13 +86,18 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, 
   float wf[2] = {8388608.f + 34952.f, 8388608.f + 34952.f};
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
-    // PRE: Q was scaled in shared memory (exact power of two), the accumulator holds the
-    // post-scale scores (tcgen05 writes zero sums as +0: already canonical)
+    // PRE (power-of-two scale): bf16 -- Q was scaled in shared memory, the accumulator holds
+    // the post-scale scores; fp16 -- select on the raw scores and scale the kept values (every
+    // nonzero fp16 score is >= 2^-48 in magnitude, so the scaled score is exact: same order, no
+    // new ties).  tcgen05 writes zero sums as +0: already canonical.
     const float v0 = PRE ? __uint_as_float(r[4 * g + 0]) : scale_canon(__uint_as_float(r[4 * g + 0]), scale);
     const float v1 = PRE ? __uint_as_float(r[4 * g + 1]) : scale_canon(__uint_as_float(r[4 * g + 1]), scale);
     const float v2 = PRE ? __uint_as_float(r[4 * g + 2]) : scale_canon(__uint_as_float(r[4 * g + 2]), scale);
     const float v3 = PRE ? __uint_as_float(r[4 * g + 3]) : scale_canon(__uint_as_float(r[4 * g + 3]), scale);
-    if (DBG) *reinterpret_cast<float4*>(dbg + dbg_row * m + colh + cc * 32 + 4 * g) = make_float4(v0, v1, v2, v3);
+    if (DBG) {
+      const float ds = SK ? scale : 1.f;
+      *reinterpret_cast<float4*>(dbg + dbg_row * m + colh + cc * 32 + 4 * g) = make_float4(v0 * ds, v1 * ds, v2 * ds, v3 * ds);
+    }
     const float w01 = fmaxf(v0, v1), l01 = fminf(v0, v1);
     const float w23 = fmaxf(v2, v3), l23 = fminf(v2, v3);
     if (RMAX) mx = fmaxf(mx, fmaxf(w01, w23));
@@ -114,6 +120,7 @@ __device__ __forceinline__ void epi_chunk(const uint32_t (&r)[32], float scale, 
       nf = -4.f;
     }
     wf[g >> 2] = fmaf(nf, (float)(1 << (4 * (g & 3))), wf[g >> 2]);
+    if (SK) mul2s(lo, hi, scale, lo, hi);
     packed[g] = pack2<T>(lo, hi);
   }
   const uint32_t W = __byte_perm(__float_as_uint(wf[0]), __float_as_uint(wf[1]), 0x5410);
@@ -136,17 +143,23 @@ template <typename T, bool DBG, bool RMAX, bool MASK, bool PRE>
 __device__ __forceinline__ void epi_chunk12(const uint32_t (&r)[32], float scale, int colh, int cc, int unit0,
                                             uint8_t* stg, uint32_t lane, uint32_t* meta_b, int row_blk, float* dbg,
                                             int64_t dbg_row, int m, float& mx, const TileKeepTc& tk, int grow) {
+  constexpr bool SK = PRE && std::is_same<T, __half>::value;  // scale the kept values
   uint32_t packed[8];
   uint32_t W[2] = {0u, 0u};
 #pragma unroll
   for (int g = 0; g < 8; ++g) {  // g: pairs 2g, 2g + 1
-    // PRE: Q was scaled in shared memory (exact power of two), the accumulator holds the
-    // post-scale scores (tcgen05 writes zero sums as +0: already canonical)
+    // PRE (power-of-two scale): bf16 -- Q was scaled in shared memory, the accumulator holds
+    // the post-scale scores; fp16 -- select on the raw scores and scale the kept values (every
+    // nonzero fp16 score is >= 2^-48 in magnitude, so the scaled score is exact: same order, no
+    // new ties).  tcgen05 writes zero sums as +0: already canonical.
     const float v0 = PRE ? __uint_as_float(r[4 * g + 0]) : scale_canon(__uint_as_float(r[4 * g + 0]), scale);
     const float v1 = PRE ? __uint_as_float(r[4 * g + 1]) : scale_canon(__uint_as_float(r[4 * g + 1]), scale);
     const float v2 = PRE ? __uint_as_float(r[4 * g + 2]) : scale_canon(__uint_as_float(r[4 * g + 2]), scale);
     const float v3 = PRE ? __uint_as_float(r[4 * g + 3]) : scale_canon(__uint_as_float(r[4 * g + 3]), scale);
-    if (DBG) *reinterpret_cast<float4*>(dbg + dbg_row * m + colh + cc * 32 + 4 * g) = make_float4(v0, v1, v2, v3);
+    if (DBG) {
+      const float ds = SK ? scale : 1.f;
+      *reinterpret_cast<float4*>(dbg + dbg_row * m + colh + cc * 32 + 4 * g) = make_float4(v0 * ds, v1 * ds, v2 * ds, v3 * ds);
+    }
     float k0, k1;
     uint32_t n0 = select12(v0, v1, k0), n1 = select12(v2, v3, k1);
     if (MASK) {  // (tile columns are even: a pair never straddles two tiles)
@@ -154,6 +167,7 @@ __device__ __forceinline__ void epi_chunk12(const uint32_t (&r)[32], float scale
       if (!tk.kept(grow, colh + cc * 32 + 4 * g + 2)) { n1 = 0x4u; k1 = 0.f; }
     }
     if (RMAX) mx = fmaxf(mx, fmaxf(k0, k1));
+    if (SK) mul2s(k0, k1, scale, k0, k1);
     packed[g] = pack2<T>(k0, k1);
     W[g >> 2] += (n0 | (n1 << 4)) << (8 * (g & 3));
   }
@@ -253,7 +267,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
         const int qs = it & 1;
         const uint32_t qph = (it >> 1) & 1;
-        tc::mbar_wait_sleep(PRE ? &q_ready[qs] : &q_full[qs], qph);
+        constexpr bool QS = PRE && std::is_same<T, __nv_bfloat16>::value;  // Q scaled in smem
+        tc::mbar_wait_sleep(QS ? &q_ready[qs] : &q_full[qs], qph);
         const uint32_t q_addr = tc::smem_u32(smem + SMEM_Q + qs * Q_BYTES);
         for (int t = 0; t < ntiles; ++t) {
           const uint32_t idesc = (m - t * BN >= BN) ? idesc256 : idesc128;
@@ -281,7 +296,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // the attention scale is an exact power of two and the inputs bf16 (fp32's exponent range):
     // Q * scale is exact, so the MMA accumulates the post-scale scores directly and the epilogue
     // drops its per-score multiply (4 of ~29 instructions per group)
-    if (PRE) {
+    if (PRE && std::is_same<T, __nv_bfloat16>::value) {
       const __nv_bfloat162 s2 = __float2bfloat162_rn(scale);
       int it = 0;
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
@@ -363,7 +378,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (++acc == NACC) { acc = 0; aph ^= 1; }
       }
       // per-row partial maxima [bh, n, 4] fp32, one per column quarter (fused softmax input)
-      if (RMAX) rowmax[((int64_t)b * n + grow) * 4 + cq] = mx;
+      if (RMAX) rowmax[((int64_t)b * n + grow) * 4 + cq] = (PRE && std::is_same<T, __half>::value) ? mx * scale : mx;
     }
     if (lane == 0) tc::bulk_wait<0>();
   }
@@ -400,10 +415,11 @@ static auto pick_kernel(bool mask, bool dbg, bool rowmax) -> decltype(&sddmm24_t
   return rowmax ? sddmm24_tc_kernel<T, GS, false, true, false, PRE> : sddmm24_tc_kernel<T, GS, false, false, false, PRE>;
 }
 
-// scale = 2^e, e <= 0, normal: Q * scale is exact in bf16 (fp32's exponent range)
+// scale = 2^e, -60 <= e <= 0: bf16 Q * scale is exact (fp32's exponent range); fp16 scores
+// (>= 2^-48 when nonzero) times scale stay normal fp32, so scaling them is exact
 static bool exact_prescale(float scale) {
   int e = 0;
-  return std::isfinite(scale) && scale > 0.f && scale <= 1.f && scale >= 1e-30f && std::frexp(scale, &e) == 0.5f;
+  return std::isfinite(scale) && scale > 0.f && scale <= 1.f && scale >= 0x1p-60f && std::frexp(scale, &e) == 0.5f;
 }
 
 template <typename T, int GS>
@@ -416,9 +432,8 @@ static cudaError_t launch_typed(const void* q, const void* k, void* nz, uint32_t
       !encode_tmap_3d(&tkm, dt, 2, (void*)k, HD, m, bh, HD, BN, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !encode_tmap_3d(&tn, dt, 2, nz, m / 2, n, bh, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorInvalidValue;
-  auto kern = pick_kernel<T, GS, false>(tk.keep != nullptr, dbg != nullptr, rowmax != nullptr);
-  if constexpr (std::is_same<T, __nv_bfloat16>::value)
-    if (exact_prescale(scale)) kern = pick_kernel<T, GS, true>(tk.keep != nullptr, dbg != nullptr, rowmax != nullptr);
+  auto kern = exact_prescale(scale) ? pick_kernel<T, GS, true>(tk.keep != nullptr, dbg != nullptr, rowmax != nullptr)
+                                    : pick_kernel<T, GS, false>(tk.keep != nullptr, dbg != nullptr, rowmax != nullptr);
   if (tk.keep && rowmax) return cudaErrorNotSupported;  // row maxima are unmasked-only
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
   if (e != cudaSuccess) return e;

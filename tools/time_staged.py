@@ -19,7 +19,8 @@ def t_ms(fn, it=10):
 
 
 for name, (b, h, n, dt, mode) in {"c2": (32, 12, 512, torch.bfloat16, "2:4"), "c4": (8, 12, 4096, torch.bfloat16, "2:4"),
-                                  "c4_12": (8, 12, 4096, torch.bfloat16, "1:2")}.items():
+                                  "c4_12": (8, 12, 4096, torch.bfloat16, "1:2"),
+                                  "c3": (16, 16, 1024, torch.float16, "2:4"), "c4h": (8, 12, 4096, torch.float16, "2:4")}.items():
     if os.environ.get("CONFIGS") and name not in os.environ["CONFIGS"].split(","):
         continue
     q, k, v = (torch.randn(b, h, n, 64, device="cuda", dtype=dt) for _ in range(3))

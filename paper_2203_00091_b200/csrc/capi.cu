@@ -113,8 +113,11 @@ int dfss_spmm(const void* p, const uint32_t* meta_hw, const void* v, void* out, 
   if (int st = check_keep(tile_keep, tile_rows, tile_cols, mode)) return st;
   if (!p || !meta_hw || !v || !out) return fail(DFSS_ERR_INVALID, "null tensor pointer");
   cudaStream_t s = (cudaStream_t)stream;
-  if (!tile_keep && dfss::tc_spmm_supported(mode, p_dtype, v_dtype, out_dtype, rows, n_k, d) && dfss_has_tcgen05())
-    return cuda_status(dfss::launch_spmm_tc(p, meta_hw, v, out, mode, p_dtype, out_dtype, bh, rows, n_k, d, row_max, s));
+  // block masks on the tcgen05 path too: its transform warps zero the absent nonzeros in shared memory
+  if ((!tile_keep || !row_max) && dfss::tc_spmm_supported(mode, p_dtype, v_dtype, out_dtype, rows, n_k, d) &&
+      dfss_has_tcgen05())
+    return cuda_status(dfss::launch_spmm_tc(p, meta_hw, v, out, mode, p_dtype, out_dtype, bh, rows, n_k, d, row_max, s,
+                                            tile_keep, tile_rows, tile_cols));
   if (row_max) return fail(DFSS_ERR_UNSUPPORTED, "fused softmax SpMM needs the tcgen05 path (2:4 or 1:2, 16-bit, d=64)");
   if (d > 256) return fail(DFSS_ERR_UNSUPPORTED, "head dim > 256 not supported by the FFMA SpMM");
   return cuda_status(dfss::launch_spmm_simt(p, meta_hw, v, out, mode, p_dtype, v_dtype, out_dtype, bh, rows, n_k, d,

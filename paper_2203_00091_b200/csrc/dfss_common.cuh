@@ -194,7 +194,8 @@ cudaError_t launch_sddmm_tc(const void* q, const void* k, void* nz, uint32_t* me
 // rowmax (nullable): [bh, rows, 2] partial row maxima from the SDDMM; when given, the SpMM
 // applies softmax on the fly: P = exp(s - max) in smem, out = (P.V) / sum(P).
 cudaError_t launch_spmm_tc(const void* p, const uint32_t* meta, const void* v, void* out, int gs, int dtype,
-                           int out_dtype, int64_t bh, int rows, int n_k, int d, const float* rowmax, cudaStream_t s);
+                           int out_dtype, int64_t bh, int rows, int n_k, int d, const float* rowmax, cudaStream_t s,
+                           const uint8_t* keep = nullptr, int tile_rows = 0, int tile_cols = 0);
 bool tc_sddmm_supported(int gs, int in_dtype, int nz_dtype, int n, int m, int d);
 // fully fused attention (flash_tc.cu): no n x n tensor in HBM
 bool tc_flash_supported(int gs, int dtype, int n, int d);

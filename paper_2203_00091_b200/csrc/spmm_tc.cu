@@ -92,11 +92,19 @@ __device__ __forceinline__ uint32_t meta12_to_24(uint32_t w0, uint32_t w1) {
   return (v0 & 0x000F000Fu) | ((v0 & 0x0F000F00u) >> 4) | ((v1 & 0x000F000Fu) << 8) | ((v1 & 0x0F000F00u) << 4);
 }
 
-template <typename T, typename TO, bool SOFTMAX, int GS>
-__global__ void __launch_bounds__(SOFTMAX ? 640 : 384, 1)
+// BlockMask for the tcgen05 SpMM (MASKZ): the transform warps zero the absent nonzeros of each
+// staged P tile before its MMAs (the reference skips them, sparse_ops.py:57-64), so whatever a
+// caller left in the absent slots never reaches the product.
+struct SpmmKeep {
+  const uint8_t* keep = nullptr;
+  int tile_rows = 1, tile_cols = 2, grid_cols = 0;
+};
+
+template <typename T, typename TO, bool SOFTMAX, int GS, bool MASKZ = false>
+__global__ void __launch_bounds__(SOFTMAX || MASKZ ? 640 : 384, 1)
     spmm24_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_v,
                      const uint32_t* __restrict__ meta, TO* __restrict__ out, int bh, int rows, int n_k,
-                     const float* __restrict__ rowmax) {
+                     const float* __restrict__ rowmax, SpmmKeep mk) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + SMEM_BAR);
@@ -165,7 +173,7 @@ __global__ void __launch_bounds__(SOFTMAX ? 640 : 384, 1)
         const uint32_t d_tmem = tmem_base + acc * HD;
         for (int kb = 0; kb < kblocks; ++kb) {
           tc::mbar_wait(&full[s], ph);
-          if (SOFTMAX) tc::mbar_wait(&p_ready[s], ph);
+          if (SOFTMAX || MASKZ) tc::mbar_wait(&p_ready[s], ph);
           tc::mbar_wait(&e_full[s], ph);
           tc::tc_fence_after();
           const uint32_t p_addr = tc::smem_u32(smem + SMEM_P + s * P_BYTES);
@@ -277,6 +285,44 @@ __global__ void __launch_bounds__(SOFTMAX ? 640 : 384, 1)
       }
       if (++acc == NACC) { acc = 0; aph ^= 1; }
     }
+  } else if (MASKZ && warp >= 12) {
+    // ------------------------------------------------------------ BlockMask: zero absent nonzeros
+    // warp (quad, half): row r of the block, 16-byte units 4 half .. 4 half + 3 (8 nonzeros =
+    // 16 dense columns each) of the 128B-swizzled P row
+    const int quad = warp & 3;
+    const int half = (warp - 12) >> 2;
+    const int r = quad * 32 + lane;
+    const bool unit_tiles = mk.tile_cols % 16 == 0;  // a unit lies in one tile: one lookup, no read
+    int s = 0;
+    uint32_t ph = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+      const int rb = item % rblocks;
+      const uint8_t* krow = mk.keep + (int64_t)((rb * BM + r) / mk.tile_rows) * mk.grid_cols;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        tc::mbar_wait(&full[s], ph);
+        uint8_t* prow = smem + SMEM_P + s * P_BYTES + r * 128;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int u = 4 * half + c;
+          const int d0 = 2 * (kb * (BKL / 2) + 8 * u);  // first dense column of the unit
+          uint4* dst = reinterpret_cast<uint4*>(prow + ((u ^ (r & 7)) << 4));
+          if (unit_tiles) {
+            if (!__ldg(krow + d0 / mk.tile_cols)) *dst = make_uint4(0u, 0u, 0u, 0u);
+          } else {
+            uint4 x = *dst;
+            uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (!__ldg(krow + (d0 + 2 * e) / mk.tile_cols)) w[e >> 1] &= (e & 1) ? 0x0000ffffu : 0xffff0000u;
+            *dst = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+        tc::fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&p_ready[s]);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
+      }
+    }
   } else if (SOFTMAX && warp >= 12) {
     // ------------------------------------------------------------ softmax transform
     const int quad = warp & 3;
@@ -348,7 +394,7 @@ static int num_sms_spmm() {
 
 template <typename T, typename TO, int GS>
 static cudaError_t spmm_launch_typed(const void* p, const uint32_t* meta, const void* v, void* out, int64_t bh, int rows,
-                                     int n_k, const float* rowmax, cudaStream_t s) {
+                                     int n_k, const float* rowmax, const SpmmKeep& mk, cudaStream_t s) {
   const CUtensorMapDataType dt =
       std::is_same<T, __nv_bfloat16>::value ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   CUtensorMap tp, tv;
@@ -357,32 +403,46 @@ static cudaError_t spmm_launch_typed(const void* p, const uint32_t* meta, const 
     return cudaErrorInvalidValue;
   const int items = (int)bh * (rows / BM);
   const int grid = items < num_sms_spmm() ? items : num_sms_spmm();
+  if (rowmax && mk.keep) return cudaErrorNotSupported;  // the fused softmax is unmasked-only
   if (rowmax) {
     auto kern = spmm24_tc_kernel<T, TO, true, GS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
     if (e != cudaSuccess) return e;
-    kern<<<grid, 640, SMEM_TOTAL, s>>>(tp, tv, meta, (TO*)out, (int)bh, rows, n_k, rowmax);
+    kern<<<grid, 640, SMEM_TOTAL, s>>>(tp, tv, meta, (TO*)out, (int)bh, rows, n_k, rowmax, mk);
+  } else if (mk.keep) {
+    auto kern = spmm24_tc_kernel<T, TO, false, GS, true>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, 640, SMEM_TOTAL, s>>>(tp, tv, meta, (TO*)out, (int)bh, rows, n_k, nullptr, mk);
   } else {
     auto kern = spmm24_tc_kernel<T, TO, false, GS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TOTAL);
     if (e != cudaSuccess) return e;
-    kern<<<grid, 384, SMEM_TOTAL, s>>>(tp, tv, meta, (TO*)out, (int)bh, rows, n_k, nullptr);
+    kern<<<grid, 384, SMEM_TOTAL, s>>>(tp, tv, meta, (TO*)out, (int)bh, rows, n_k, nullptr, mk);
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_spmm_tc(const void* p, const uint32_t* meta, const void* v, void* out, int gs, int dtype,
-                           int out_dtype, int64_t bh, int rows, int n_k, int d, const float* rowmax, cudaStream_t s) {
+                           int out_dtype, int64_t bh, int rows, int n_k, int d, const float* rowmax, cudaStream_t s,
+                           const uint8_t* keep, int tile_rows, int tile_cols) {
   if (!tc_spmm_supported(gs, dtype, dtype, out_dtype, rows, n_k, d)) return cudaErrorNotSupported;
   if (bh == 0) return cudaSuccess;
+  SpmmKeep mk;
+  if (keep) {
+    mk.keep = keep;
+    mk.tile_rows = tile_rows;
+    mk.tile_cols = tile_cols;
+    mk.grid_cols = (n_k + tile_cols - 1) / tile_cols;
+  }
   auto go = [&](auto gs_tag) {
     constexpr int G = decltype(gs_tag)::value;
     if (dtype == DFSS_BF16)
       return out_dtype == DFSS_F32
-                 ? spmm_launch_typed<__nv_bfloat16, float, G>(p, meta, v, out, bh, rows, n_k, rowmax, s)
-                 : spmm_launch_typed<__nv_bfloat16, __nv_bfloat16, G>(p, meta, v, out, bh, rows, n_k, rowmax, s);
-    return out_dtype == DFSS_F32 ? spmm_launch_typed<__half, float, G>(p, meta, v, out, bh, rows, n_k, rowmax, s)
-                                 : spmm_launch_typed<__half, __half, G>(p, meta, v, out, bh, rows, n_k, rowmax, s);
+                 ? spmm_launch_typed<__nv_bfloat16, float, G>(p, meta, v, out, bh, rows, n_k, rowmax, mk, s)
+                 : spmm_launch_typed<__nv_bfloat16, __nv_bfloat16, G>(p, meta, v, out, bh, rows, n_k, rowmax, mk, s);
+    return out_dtype == DFSS_F32 ? spmm_launch_typed<__half, float, G>(p, meta, v, out, bh, rows, n_k, rowmax, mk, s)
+                                 : spmm_launch_typed<__half, __half, G>(p, meta, v, out, bh, rows, n_k, rowmax, mk, s);
   };
   return gs == 2 ? go(std::integral_constant<int, 2>{}) : go(std::integral_constant<int, 4>{});
 }

@@ -332,6 +332,37 @@ def test_softmax_16bit_fast_path_edges(dtype):
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("tiles", [(32, 16), (16, 64), (64, 48), (32, 8)])
+def test_softmax_16bit_block_mask(dtype, tiles):
+    """softmax_rows with a BlockMask on 16-bit rows: tile widths that are multiples of 16 run the
+    packed fast path (absent vectors -inf before the max), 8 the generic kernel; both equal the
+    reference softmax over the present entries (absent -> 0) at 8e-3; NaN in an absent entry is
+    ignored, in a present one raises."""
+    rng = np.random.default_rng(tiles[0] * 100 + tiles[1])
+    tr, tc_ = tiles
+    for rows, nz in ((96, 256), (64, 1024), (32, 2048)):
+        keep = rng.random((-(-rows // tr), -(-2 * nz // tc_))) < 0.5
+        keep[np.arange(keep.shape[0]), rng.integers(0, keep.shape[1], keep.shape[0])] = True
+        mask = dfss.BlockMask(keep, tile_rows=tr, tile_cols=tc_)
+        s = (rng.standard_normal((2, rows, 2 * nz)) * 4).astype(np.float32)
+        c = dfss.compress_logical(torch.from_numpy(s).to(dtype).cuda(), M24)
+        present = mask.nonzero_keep(rows, 2 * nz)
+        nzv = c.nonzeros.clone()
+        nzv[:, torch.from_numpy(~present).cuda()] = float("nan")  # absent entries are never read
+        cm = dfss.CompressedSparse(rows, 2 * nz, c.mode, nzv, c.meta_hw, block_mask=mask)
+        got = _np(dfss.softmax_rows(cm).nonzeros)
+        for b in range(2):
+            want = oracle_c.softmax_nonzeros(_np(c.nonzeros[b]), present)
+            assert_close(got[b], want, 8e-3, 8e-5, f"masked softmax tiles={tiles} rows={rows} nz={nz}")
+            assert not got[b][~present].any()
+        bad = nzv.clone()
+        r, j = np.argwhere(present)[len(np.argwhere(present)) // 2]
+        bad[1, r, j] = float("nan")
+        with pytest.raises(ValueError, match="NaN"):
+            dfss.softmax_rows(dfss.CompressedSparse(rows, 2 * nz, c.mode, bad, c.meta_hw, block_mask=mask))
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 def test_staged_12_tcgen05_attention_matches_reference(dtype):
     """1:2 through the staged reference-shaped API on the tcgen05 kernels (16-bit, tiled shape):
     sddmm_prune -> softmax_rows -> spmm equals the reference nm_attention at 2e-2."""
@@ -388,6 +419,37 @@ def test_spmm_matches_decompress_oracle(mode, dtype):
             want = oracle_c.spmm_gather(nzp[b], colidx, _np(v[b]))
             tol = 1e-5 if dtype == torch.float32 else 1e-2
             assert_close(out[b], want, tol, tol, f"spmm {bh, rows, cols, d}")
+
+
+@pytest.mark.parametrize("mode", ["1:2", "2:4"])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("tiles", [(32, 16), (16, 8), (64, 64), (128, 6)])
+def test_spmm_block_mask_tcgen05(mode, dtype, tiles):
+    """spmm with a BlockMask on the tcgen05 kernel (16-bit, d = 64): absent nonzeros -- NaN here --
+    are zeroed in shared memory before the MMAs (whole 16-byte units for tile widths that are
+    multiples of 16, element-wise otherwise), so the output equals the reference gather over the
+    present entries (sparse_ops.py:57-64)."""
+    rng = np.random.default_rng(tiles[0] + tiles[1])
+    tr, tc_ = tiles
+    bh, rows, cols = 2, 256, 512
+    if tc_ % 2 or (mode == "2:4" and tc_ % 4):
+        pytest.skip("tile width must hold whole groups")
+    m = MODES[mode]
+    keep = rng.random((-(-rows // tr), -(-cols // tc_))) < 0.5
+    mask = dfss.BlockMask(keep, tile_rows=tr, tile_cols=tc_)
+    a = dfss.compress_logical(torch.from_numpy(rng.standard_normal((bh, rows, cols)).astype(np.float32) / 4)
+                              .to(dtype).cuda(), m)
+    present = mask.nonzero_keep(rows, cols)
+    nz = a.nonzeros.clone()
+    nz[:, torch.from_numpy(~present).cuda()] = float("nan")
+    p = dfss.CompressedSparse(rows, cols, a.mode, nz, a.meta_hw, block_mask=mask)
+    v = torch.from_numpy(rng.standard_normal((bh, cols, 64)).astype(np.float32)).to(dtype).cuda()
+    out = _np(dfss.spmm(p, v).data)
+    meta = logical_meta(a)
+    for b in range(bh):
+        colidx = ref.nonzero_columns(meta[b].ravel(), rows, cols, mode)
+        want = oracle_c.spmm_gather(_np(a.nonzeros[b]), colidx, _np(v[b]), present)
+        assert_close(out[b], want, 1e-2, 1e-2, f"masked spmm {mode} tiles={tiles}")
 
 
 def test_spmm_linear_in_v():

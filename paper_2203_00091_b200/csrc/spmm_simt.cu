@@ -116,7 +116,10 @@ __global__ void __launch_bounds__(256) spmm_tiled_kernel(const TP* __restrict__ 
   const uint32_t* mb = meta + (int64_t)b * geo.words_per_bh();
   const uint4* vb = reinterpret_cast<const uint4*>(v + (int64_t)b * n_k * 64);
   if (threadIdx.x < 64) Vs[KT][threadIdx.x] = 0.f;
-  const int orow = threadIdx.x >> 3, cb = threadIdx.x & 7;  // output row, 8-column block
+  // output row; columns 4cb .. 4cb+3 and 32+4cb .. 32+4cb+3: the 8 threads of a row read two
+  // contiguous 128-byte halves of the V row (one shared-memory wavefront each) -- an 8-column
+  // block per thread read them at a 32-byte stride (twice the wavefronts)
+  const int orow = threadIdx.x >> 3, cb = threadIdx.x & 7;
   float acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = 0.f;
@@ -154,8 +157,8 @@ __global__ void __launch_bounds__(256) spmm_tiled_kernel(const TP* __restrict__ 
 #pragma unroll 4
     for (int jl = 0; jl < NZT; ++jl) {
       const float w = Ps[orow][jl];
-      const float4* vr = reinterpret_cast<const float4*>(&Vs[Cs[orow][jl]][8 * cb]);
-      const float4 x0 = vr[0], x1 = vr[1];
+      const float4* vr = reinterpret_cast<const float4*>(&Vs[Cs[orow][jl]][4 * cb]);
+      const float4 x0 = vr[0], x1 = vr[8];
       acc[0] = fmaf(w, x0.x, acc[0]);
       acc[1] = fmaf(w, x0.y, acc[1]);
       acc[2] = fmaf(w, x0.z, acc[2]);
@@ -169,9 +172,12 @@ __global__ void __launch_bounds__(256) spmm_tiled_kernel(const TP* __restrict__ 
   }
   const int r = row0 + orow;
   if (r < rows) {
-    TO* o = out + ((int64_t)b * rows + r) * 64 + 8 * cb;
+    TO* o = out + ((int64_t)b * rows + r) * 64 + 4 * cb;  // columns 4cb.. and 32+4cb.. (see Vs reads)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) o[i] = DT<TO>::from_f(acc[i]);
+    for (int i = 0; i < 4; ++i) {
+      o[i] = DT<TO>::from_f(acc[i]);
+      o[32 + i] = DT<TO>::from_f(acc[4 + i]);
+    }
   }
 }
 
@@ -355,7 +361,10 @@ __global__ void __launch_bounds__(256) spmm_softmax_f32_tiled_kernel(const float
     }
   }
   __syncthreads();
-  const int orow = threadIdx.x >> 3, cb = threadIdx.x & 7;  // output row, 8-column block
+  // output row; columns 4cb .. 4cb+3 and 32+4cb .. 32+4cb+3: the 8 threads of a row read two
+  // contiguous 128-byte halves of the V row (one shared-memory wavefront each) -- an 8-column
+  // block per thread read them at a 32-byte stride (twice the wavefronts)
+  const int orow = threadIdx.x >> 3, cb = threadIdx.x & 7;
   float acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = 0.f;
@@ -388,8 +397,8 @@ __global__ void __launch_bounds__(256) spmm_softmax_f32_tiled_kernel(const float
 #pragma unroll 4
     for (int jl = 0; jl < NZT; ++jl) {
       const float w = Ps[orow][jl];
-      const float4* vr = reinterpret_cast<const float4*>(&Vs[Cs[orow][jl]][8 * cb]);
-      const float4 x0 = vr[0], x1 = vr[1];
+      const float4* vr = reinterpret_cast<const float4*>(&Vs[Cs[orow][jl]][4 * cb]);
+      const float4 x0 = vr[0], x1 = vr[8];
       acc[0] = fmaf(w, x0.x, acc[0]);
       acc[1] = fmaf(w, x0.y, acc[1]);
       acc[2] = fmaf(w, x0.z, acc[2]);
@@ -404,9 +413,9 @@ __global__ void __launch_bounds__(256) spmm_softmax_f32_tiled_kernel(const float
   const int r = row0 + orow;
   if (r < rows) {
     const float inv = s_inv[orow];
-    float4* o = reinterpret_cast<float4*>(out + ((int64_t)b * rows + r) * 64 + 8 * cb);
+    float4* o = reinterpret_cast<float4*>(out + ((int64_t)b * rows + r) * 64 + 4 * cb);
     o[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-    o[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+    o[8] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
   }
 }
 

@@ -20,13 +20,27 @@ constexpr int BM = 64, BN = 64, BK = 32;
 // rows 4*ty .. 4*ty+3, columns 4*tx .. 4*tx+3 (one 2:4 group, two 1:2 groups).
 // (16-bit inputs: at least 2 CTAs / SM, so ptxas keeps their conversions in registers instead of
 // spilling; fp32 (the c1 exact path) keeps 64 registers / 4 CTAs: 114 registers were 10 % slower)
+// four consecutive elements (16 B fp32 / 8 B 16-bit, aligned) as floats, or zeros
+template <typename TIn>
+__device__ __forceinline__ void load4(const TIn* __restrict__ p, bool ok, float (&x)[4]) {
+  if constexpr (std::is_same<TIn, float>::value) {
+    const float4 v = ok ? __ldg(reinterpret_cast<const float4*>(p)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
+  } else {
+    const uint2 u = ok ? __ldg(reinterpret_cast<const uint2*>(p)) : make_uint2(0u, 0u);
+    const TIn* h = reinterpret_cast<const TIn*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) x[e] = DT<TIn>::to_f(h[e]);
+  }
+}
+
 template <typename TIn, typename TNz, int GS>
 __global__ void __launch_bounds__(256, std::is_same<TIn, float>::value ? 4 : 2) sddmm_simt_kernel(const TIn* __restrict__ q, const TIn* __restrict__ k,
                                                          TNz* __restrict__ nz, uint32_t* __restrict__ meta,
                                                          float scale, int n, int m, int d,
                                                          const uint8_t* __restrict__ keep, int tile_rows,
                                                          int tile_cols, float* __restrict__ dbg, MetaGeom geo,
-                                                         uint32_t two) {
+                                                         uint32_t two, int vec4) {
   __shared__ __align__(16) float Qs[BK][BM + 4];
   __shared__ __align__(16) float Ks[BK][BN + 4];
   __shared__ uint8_t nibs[BM][BN / GS];
@@ -63,12 +77,30 @@ __global__ void __launch_bounds__(256, std::is_same<TIn, float>::value ? 4 : 2) 
   }
   if (row0 < n && cta_live) {
     for (int k0 = 0; k0 < d; k0 += BK) {
-      for (int i = threadIdx.x; i < BM * BK; i += 256) {
-        const int r = i / BK, kk = i % BK;
-        const int gr = row0 + r, gk = k0 + kk;
-        Qs[kk][r] = (gr < n && gk < d) ? DT<TIn>::to_f(q[(int64_t)gr * d + gk]) : 0.f;
-        const int gc = col0 + r;
-        Ks[kk][r] = (gc < m && gk < d) ? DT<TIn>::to_f(k[(int64_t)gc * d + gk]) : 0.f;
+      if (vec4) {  // d % 4 == 0, aligned rows: four elements per load (the scalar loop below
+                   // spent a quarter of the kernel's instructions on loads and index math)
+#pragma unroll
+        for (int it = 0; it < (BM * BK / 4) / 256; ++it) {
+          const int i = threadIdx.x + 256 * it;
+          const int r = i / (BK / 4), kq = (i % (BK / 4)) * 4;
+          const int gr = row0 + r, gc = col0 + r, gk = k0 + kq;
+          float a[4], c[4];
+          load4<TIn>(q + (int64_t)gr * d + gk, gr < n && gk < d, a);
+          load4<TIn>(k + (int64_t)gc * d + gk, gc < m && gk < d, c);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            Qs[kq + e][r] = a[e];
+            Ks[kq + e][r] = c[e];
+          }
+        }
+      } else {
+        for (int i = threadIdx.x; i < BM * BK; i += 256) {
+          const int r = i / BK, kk = i % BK;
+          const int gr = row0 + r, gk = k0 + kk;
+          Qs[kk][r] = (gr < n && gk < d) ? DT<TIn>::to_f(q[(int64_t)gr * d + gk]) : 0.f;
+          const int gc = col0 + r;
+          Ks[kk][r] = (gc < m && gk < d) ? DT<TIn>::to_f(k[(int64_t)gc * d + gk]) : 0.f;
+        }
       }
       __syncthreads();
 #pragma unroll 8
@@ -162,12 +194,13 @@ static cudaError_t sddmm_simt_typed(const void* q, const void* k, void* nz, uint
     uint32_t* mb = meta + b0 * geo.words_per_bh();
     float* db = dbg ? dbg + b0 * n * m : nullptr;
     dim3 grid((m + BN - 1) / BN, 2 * geo.rblocks, (unsigned)nb);
+    const int vec4 = d % 4 == 0 && ((uintptr_t)qb | (uintptr_t)kb) % (4 * sizeof(TIn)) == 0;
     if (gs == 4)
       sddmm_simt_kernel<TIn, TNz, 4><<<grid, 256, 0, s>>>(qb, kb, nzb, mb, scale, n, m, d, keep, tile_rows, tile_cols,
-                                                          db, geo, 2u);
+                                                          db, geo, 2u, vec4);
     else
       sddmm_simt_kernel<TIn, TNz, 2><<<grid, 256, 0, s>>>(qb, kb, nzb, mb, scale, n, m, d, keep, tile_rows, tile_cols,
-                                                          db, geo, 2u);
+                                                          db, geo, 2u, vec4);
   }
   return cudaGetLastError();
 }

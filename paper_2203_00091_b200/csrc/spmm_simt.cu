@@ -320,10 +320,17 @@ __global__ void __launch_bounds__(256) spmm_simt_softmax_d64_kernel(const float*
 }
 
 // Tiled variant (d == 64, n_k % 128 == 0): a CTA owns 32 rows of one (batch, head) and streams
-// V through shared memory in 128-key tiles, so each V row is read from L2 once per CTA instead
+// V through shared memory in 64-key tiles, so each V row is read from L2 once per CTA instead
 // of once per nonzero (the warp-per-row kernel is L2-bandwidth-bound at larger n).  For either
-// mode the nonzeros of a row that fall in a 128-key tile are the contiguous range
-// [k0 / 2, k0 / 2 + 64).  Accumulation stays in ascending nonzero order.
+// mode the nonzeros of a row that fall in a 64-key tile are the contiguous range
+// [k0 / 2, k0 / 2 + 32).
+// The tile's weights are scattered into a dense [32 rows][128 keys] block (zeros where a key
+// is not kept) and multiplied as a dense register-blocked product: a thread owns 4 rows x 2
+// columns; per 4 keys, 4 broadcast loads of 4 weights and 4 8-byte V loads feed 32 FFMAs (the
+// per-nonzero gather of a V row moved ~4x more shared-memory wavefronts per FMA).  Twice the
+// FMAs of the sparse gather, but the added terms are fma(0, v, acc) = acc exactly (V finite,
+// dense.py:34-35), and keys are accumulated in ascending order: the result is bitwise the
+// sparse accumulation in ascending nonzero order.
 template <int GS>
 __global__ void __launch_bounds__(256) spmm_softmax_f32_tiled_kernel(const float* __restrict__ p,
                                                                      const uint32_t* __restrict__ meta,
@@ -331,10 +338,9 @@ __global__ void __launch_bounds__(256) spmm_softmax_f32_tiled_kernel(const float
                                                                      float* __restrict__ out, int rows, int n_k,
                                                                      MetaGeom geo) {
   constexpr float kLog2e = 1.4426950408889634f;
-  constexpr int RB = 32, KT = 128, NZT = KT / 2;
+  constexpr int RB = 32, KT = 64, NZT = KT / 2;  // 64-key tiles: 16 KB of V + 8.5 KB of weights
   __shared__ __align__(16) float Vs[KT][64];
-  __shared__ float Ps[RB][NZT + 1];
-  __shared__ uint8_t Cs[RB][NZT];
+  __shared__ __align__(16) float Pd[RB][KT + 4];  // dense weights, row-major (rows 16 B aligned)
   __shared__ float s_mlb[RB], s_inv[RB];
   const int b = blockIdx.y, row0 = blockIdx.x * RB;
   const int nzc = n_k / 2;
@@ -361,61 +367,67 @@ __global__ void __launch_bounds__(256) spmm_softmax_f32_tiled_kernel(const float
     }
   }
   __syncthreads();
-  // output row; columns 4cb .. 4cb+3 and 32+4cb .. 32+4cb+3: the 8 threads of a row read two
-  // contiguous 128-byte halves of the V row (one shared-memory wavefront each) -- an 8-column
-  // block per thread read them at a 32-byte stride (twice the wavefronts)
-  const int orow = threadIdx.x >> 3, cb = threadIdx.x & 7;
-  float acc[8];
+  // thread: rows 4 * warp .. + 3 (one weight float4 per key, a broadcast within the warp),
+  // columns 2 * lane, 2 * lane + 1 (the warp reads a whole 256-byte V row per key)
+  float acc[4][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.f;
   for (int k0 = 0; k0 < n_k; k0 += KT) {
-    // V tile [128 keys][64] (float4 per thread x 8)
+    // V tile [128 keys][64] (float4 per thread x 8) and the zeroed weight block
 #pragma unroll
     for (int i = 0; i < (KT * 16) / 256; ++i) {
       const int idx = threadIdx.x + 256 * i;
       reinterpret_cast<float4*>(&Vs[0][0])[idx] = vb[(int64_t)k0 * 16 + idx];
     }
-    // this tile's nonzeros of the CTA's rows: weights and tile-local columns
+#pragma unroll
+    for (int i = 0; i < (KT * RB / 4) / 256; ++i) {
+      const int idx = threadIdx.x + 256 * i;  // float4 idx % (KT / 4) of row idx / (KT / 4)
+      *reinterpret_cast<float4*>(&Pd[idx / (KT / 4)][4 * (idx % (KT / 4))]) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+    // scatter this tile's weights of the CTA's rows to their keys
 #pragma unroll
     for (int i = 0; i < (RB * NZT) / 256; ++i) {
       const int idx = threadIdx.x + 256 * i;
       const int rr = idx / NZT, jl = idx % NZT;
       const int r = row0 + rr, j = k0 / 2 + jl;
-      float w = 0.f;
-      int col = k0;  // rows past the end: weight 0 on tile row 0
       if (r < rows) {
         const int g = (GS == 4) ? (j >> 1) : j;
         int shift;
         const uint32_t nib = (mb[geo.word_of(r, g, shift)] >> shift) & 0xFu;
-        col = (GS == 4) ? 4 * g + (int)((j & 1) ? ((nib >> 2) & 3u) : (nib & 3u)) : 2 * g + (nib == 0xEu ? 1 : 0);
-        w = exp2f(fmaf(pb[(int64_t)r * nzc + j], kLog2e, -s_mlb[rr]));
+        const int col = (GS == 4) ? 4 * g + (int)((j & 1) ? ((nib >> 2) & 3u) : (nib & 3u)) : 2 * g + (nib == 0xEu ? 1 : 0);
+        Pd[rr][col - k0] = exp2f(fmaf(pb[(int64_t)r * nzc + j], kLog2e, -s_mlb[rr]));
       }
-      Ps[rr][jl] = w;
-      Cs[rr][jl] = (uint8_t)(col - k0);
     }
     __syncthreads();
-#pragma unroll 4
-    for (int jl = 0; jl < NZT; ++jl) {
-      const float w = Ps[orow][jl];
-      const float4* vr = reinterpret_cast<const float4*>(&Vs[Cs[orow][jl]][4 * cb]);
-      const float4 x0 = vr[0], x1 = vr[8];
-      acc[0] = fmaf(w, x0.x, acc[0]);
-      acc[1] = fmaf(w, x0.y, acc[1]);
-      acc[2] = fmaf(w, x0.z, acc[2]);
-      acc[3] = fmaf(w, x0.w, acc[3]);
-      acc[4] = fmaf(w, x1.x, acc[4]);
-      acc[5] = fmaf(w, x1.y, acc[5]);
-      acc[6] = fmaf(w, x1.z, acc[6]);
-      acc[7] = fmaf(w, x1.w, acc[7]);
+#pragma unroll 2
+    for (int kk = 0; kk < KT; kk += 4) {
+      float w[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 t = *reinterpret_cast<const float4*>(&Pd[4 * warp + i][kk]);
+        w[i][0] = t.x, w[i][1] = t.y, w[i][2] = t.z, w[i][3] = t.w;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {  // keys in ascending order
+        const float2 x = *reinterpret_cast<const float2*>(&Vs[kk + e][2 * lane]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc[i][0] = fmaf(w[i][e], x.x, acc[i][0]);
+          acc[i][1] = fmaf(w[i][e], x.y, acc[i][1]);
+        }
+      }
     }
     __syncthreads();
   }
-  const int r = row0 + orow;
-  if (r < rows) {
-    const float inv = s_inv[orow];
-    float4* o = reinterpret_cast<float4*>(out + ((int64_t)b * rows + r) * 64 + 4 * cb);
-    o[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-    o[8] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int rr = 4 * warp + i, r = row0 + rr;
+    if (r < rows) {
+      const float inv = s_inv[rr];
+      *reinterpret_cast<float2*>(out + ((int64_t)b * rows + r) * 64 + 2 * lane) =
+          make_float2(acc[i][0] * inv, acc[i][1] * inv);
+    }
   }
 }
 

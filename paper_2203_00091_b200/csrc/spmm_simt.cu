@@ -435,9 +435,11 @@ cudaError_t launch_spmm_simt_softmax_f32(const void* p, const uint32_t* meta, co
                                         int64_t bh, int rows, int n_k, int d, cudaStream_t s) {
   if (bh == 0 || rows == 0 || d == 0) return cudaSuccess;
   if (d > 64) return cudaErrorNotSupported;
-  // tiled from n_k = 512 up (L2-bound warp kernel: n = 1024 1.79 -> 1.50 ms for 96 heads); the
-  // warp-per-row kernel is faster on short rows (n = 384: 0.198 vs 0.233 ms, tools/time_f32_sweep.py)
-  if (d == 64 && n_k % 128 == 0 && n_k >= 512 && ((uintptr_t)v & 15) == 0 && ((uintptr_t)out & 15) == 0) {
+  // tiled from n_k = 512 up (L2-bound warp kernel: n = 1024 1.79 -> 1.50 ms for 96 heads), and on
+  // shorter rows once there are >= 4 waves of 32-row CTAs (n = 384 x 96 heads: 0.159 vs 0.179 ms per
+  // step); few CTAs (c1: 12 heads x 12 row blocks) keep the warp-per-row kernel (0.030 vs 0.037 ms)
+  const bool tiled_pays = n_k >= 512 || bh * ((rows + 31) / 32) >= 4 * 148;
+  if (d == 64 && n_k % 128 == 0 && tiled_pays && ((uintptr_t)v & 15) == 0 && ((uintptr_t)out & 15) == 0) {
     const MetaGeom geo(rows, n_k / gs);
     for (int64_t b0 = 0; b0 < bh; b0 += 65535) {  // bh on gridDim.y (<= 65535): slices
       const int64_t nb = bh - b0 < 65535 ? bh - b0 : 65535;

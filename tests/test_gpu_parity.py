@@ -953,10 +953,13 @@ def test_block_mask_fuzz_many_items(case):
                      f"fuzz case {case}: n={n} tiles={tr}x{tc_} density={density} style={style} head {h}")
 
 
-@pytest.mark.parametrize("n,mode", [(512, "1:2"), (1024, "1:2"), (640, "2:4")])
-def test_exact_fp32_longer_rows_match_reference(n, mode):
-    """Exact-FP32 path at the 1e-5 bar on rows long enough for the shared-memory-tiled SpMM
-    (n >= 512; softmax fused), against the reference nm_attention in float64."""
-    (q, k, v), (q64, k64, v64) = seeded_qkv((1, 3, n, 64), torch.float32, seed=n + 7)
+@pytest.mark.parametrize("n,mode,heads", [(512, "1:2", 3), (1024, "1:2", 3), (640, "2:4", 3), (384, "1:2", 64)])
+def test_exact_fp32_longer_rows_match_reference(n, mode, heads):
+    """Exact-FP32 path at the 1e-5 bar where the shared-memory-tiled SpMM runs (n >= 512, or
+    >= 4 waves of 32-row blocks: 64 heads at n = 384; softmax fused), against the reference
+    nm_attention in float64 (first, middle and last heads)."""
+    (q, k, v), (q64, k64, v64) = seeded_qkv((1, heads, n, 64), torch.float32, seed=n + 7)
     out = _np(dfss.dfss_attention(q, k, v, mode, math_mode="ffma"))
-    assert_close(out, oracle_attention(q64, k64, v64, mode), 1e-5, 1e-5, f"exact fp32 {mode} n={n}")
+    for h in sorted({0, heads // 2, heads - 1}):
+        assert_close(out[:, h:h + 1], oracle_attention(q64[:, h:h + 1], k64[:, h:h + 1], v64[:, h:h + 1], mode),
+                     1e-5, 1e-5, f"exact fp32 {mode} n={n} head {h}")

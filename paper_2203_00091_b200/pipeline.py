@@ -211,6 +211,18 @@ def dfss_attention_dump(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode=
 _HOST_STREAMS: dict[int, tuple[torch.cuda.Stream, torch.cuda.Stream, torch.cuda.Stream]] = {}
 
 
+def _piece_bounds(bh: int, chunks: int) -> list[int]:
+    """Piece boundaries over the flattened batch x heads: `chunks` equal pieces, the last one cut
+    into halves / quarters so the copy-out after the last kernel (the pipeline's tail) is short
+    (c2, 4 pieces: 1.79 -> 1.7 ms per call, tools/host_timeline.py)."""
+    chunks = max(1, min(int(chunks), bh))
+    bounds = [bh * i // chunks for i in range(chunks + 1)]
+    lo, hi = bounds[-2], bounds[-1]
+    if chunks > 1 and hi - lo >= 4:
+        bounds[-1:] = [lo + (hi - lo) // 2, lo + 3 * (hi - lo) // 4, hi]
+    return bounds
+
+
 def dfss_attention_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode="2:4", *, math_mode: str = "auto",
                         block_mask: BlockMask | None = None, out: torch.Tensor | None = None, chunks: int = 4,
                         device: torch.device | int | None = None, non_blocking: bool = False) -> torch.Tensor:
@@ -238,8 +250,8 @@ def dfss_attention_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode=
     if out is None:
         out = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
     of = out.view(bh, n, d)
-    chunks = max(1, min(int(chunks), bh))
-    bounds = [bh * i // chunks for i in range(chunks + 1)]
+    bounds = _piece_bounds(bh, chunks)
+    chunks = len(bounds) - 1
     width = max(bounds[i + 1] - bounds[i] for i in range(chunks))
     if dev.index not in _HOST_STREAMS:
         _HOST_STREAMS[dev.index] = tuple(torch.cuda.Stream(dev) for _ in range(3))

@@ -118,6 +118,7 @@ int dfss_spmm(const void* p, const uint32_t* meta_hw, const void* v, void* out, 
       dfss_has_tcgen05())
     return cuda_status(dfss::launch_spmm_tc(p, meta_hw, v, out, mode, p_dtype, out_dtype, bh, rows, n_k, d, row_max, s,
                                             tile_keep, tile_rows, tile_cols));
+  if (row_max && tile_keep) return fail(DFSS_ERR_UNSUPPORTED, "fused softmax SpMM is unmasked-only");
   if (row_max) return fail(DFSS_ERR_UNSUPPORTED, "fused softmax SpMM needs the tcgen05 path (2:4 or 1:2, 16-bit, d=64)");
   if (d > 256) return fail(DFSS_ERR_UNSUPPORTED, "head dim > 256 not supported by the FFMA SpMM");
   return cuda_status(dfss::launch_spmm_simt(p, meta_hw, v, out, mode, p_dtype, v_dtype, out_dtype, bh, rows, n_k, d,

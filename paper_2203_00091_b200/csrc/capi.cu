@@ -125,6 +125,12 @@ int dfss_spmm(const void* p, const uint32_t* meta_hw, const void* v, void* out, 
                                             tile_keep, tile_rows, tile_cols, s));
 }
 
+// exact-FP32 attention (math auto) with the SpMM on tcgen05 as 3xTF32: 1:2, d = 64, n % 128 == 0
+static bool exact_f32_on_tc(int mode, int dtype, int math, int n, int d) {
+  return math == DFSS_MATH_AUTO && dtype == DFSS_F32 && mode == 2 && dfss::tc_spmm_tf32x3_supported(2, n, n, d) &&
+         dfss_has_tcgen05();
+}
+
 int64_t dfss_nm_attention_workspace_bytes_for(int mode, int dtype, int math, int64_t bh, int n, int d,
                                               int tile_rows, int tile_cols, int masked) {
   if (!valid_mode(mode) || !valid_dtype(dtype) || bh < 0 || n < 1 || d < 1) return -1;
@@ -136,7 +142,10 @@ int64_t dfss_nm_attention_workspace_bytes_for(int mode, int dtype, int math, int
   if (math == DFSS_MATH_TF32 && dtype == DFSS_F32 && dfss::tc_flash_tf32_supported(mode, n, d) &&
       (!masked || (mask_ok && dfss::flash_mask_two_set_ok(n))) && dfss_has_tcgen05())
     return dfss::flash_tf32_workspace_bytes(bh, n, masked);  // V^T (K-major tf32 B) + mask bitmaps
-  return dfss_nm_attention_workspace_bytes(mode, dtype, bh, n, d);
+  const int64_t staged = dfss_nm_attention_workspace_bytes(mode, dtype, bh, n, d);
+  if (!masked && exact_f32_on_tc(mode, dtype, math, n, d))
+    return staged + dfss::spmm_tf32x3_workspace_bytes(bh, n);  // + V^T hi / lo of the 3xTF32 SpMM
+  return staged;
 }
 
 int64_t dfss_nm_attention_workspace_bytes(int mode, int dtype, int64_t bh, int n, int d) {
@@ -239,6 +248,15 @@ int nm_attention_impl(const void* q, const void* k, const void* v, void* out, in
   if (st) return st;
   if (fused)
     return dfss_spmm(nz, meta, v, out, mode, dtype, dtype, dtype, bh, n, n, d, nullptr, 0, 0, row_max, stream);
+  if (dtype == DFSS_F32 && exact_f32_on_tc(mode, dtype, math, n, d) &&
+      workspace_bytes >= dfss_nm_attention_workspace_bytes(mode, dtype, bh, n, d) + dfss::spmm_tf32x3_workspace_bytes(bh, n)) {
+    // exact FP32 (math auto): row softmax in place, then the SpMM on tcgen05 as 3xTF32 (spmm_tf32.cu:
+    // the selection is already fixed by the FFMA SDDMM; ~2^-21 relative error per product)
+    st = dfss_softmax_rows(nz, nz, dtype, dtype, bh, n, n / 2, nullptr, 0, 0, nullptr, stream);
+    if (st) return st;
+    return cuda_status(dfss::launch_spmm_tf32x3((const float*)nz, meta, (const float*)v, (float*)out, bh, n, n,
+                                                ws + dfss_nm_attention_workspace_bytes(mode, dtype, bh, n, d), s));
+  }
   if (dtype == DFSS_F32 && d <= 64)  // exact FP32: softmax fused into the SIMT SpMM (one pass less)
     return cuda_status(dfss::launch_spmm_simt_softmax_f32(nz, meta, v, out, mode, bh, n, n, d, s));
   st = dfss_softmax_rows(nz, nz, dtype, dtype, bh, n, n / 2, nullptr, 0, 0, nullptr, stream);

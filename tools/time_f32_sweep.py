@@ -6,8 +6,8 @@ import paper_2203_00091_b200 as dfss
 for n in (384, 512, 768, 1024):
     q, k, v = (torch.randn(8, 12, n, 64, device="cuda") for _ in range(3))
     out = torch.empty_like(q)
-    ws = torch.empty(dfss.workspace_bytes("1:2", torch.float32, 96, n, 64, "ffma"), dtype=torch.uint8, device="cuda")
-    f = lambda: dfss.dfss_attention(q, k, v, "1:2", math_mode="ffma", out=out, workspace=ws)  # noqa: E731
+    ws = torch.empty(dfss.workspace_bytes("1:2", torch.float32, 96, n, 64, os.environ.get("MATH", "auto")), dtype=torch.uint8, device="cuda")
+    f = lambda: dfss.dfss_attention(q, k, v, "1:2", math_mode=os.environ.get("MATH", "auto"), out=out, workspace=ws)  # noqa: E731
     for _ in range(3):
         f()
     torch.cuda.synchronize()

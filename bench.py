@@ -59,7 +59,7 @@ for _n in (384, 512, 768, 1024, 2048, 4096):
                                       desc=f"sweep 1:2 tf32 (fp32 inputs), batch 8, 12 heads, seq {_n}")
     if _n <= 1024:
         CONFIGS[f"c5_12f32_{_n}"] = dict(batch=8, heads=12, seq=_n, d=64, mode="1:2", dtype="float32",
-                                         desc=f"sweep 1:2 fp32 (exact FFMA), batch 8, 12 heads, seq {_n}")
+                                         desc=f"sweep 1:2 fp32 (fp32-accurate: 3xTF32 on tcgen05 from ~8 M scores, FFMA below), batch 8, 12 heads, seq {_n}")
 DT = {"float32": torch.float32, "bfloat16": torch.bfloat16, "float16": torch.float16}
 DTYPE_TAG = {"float32": "f32", "bfloat16": "bf16", "float16": "f16"}
 METRIC = "DFSS attention ms & speedup vs dense attention (seq 512–4096) on B200; TFLOPS"
@@ -251,7 +251,8 @@ def kernel_stats(cfg_name: str, key: str) -> dict:
 
 
 #: kernels one dfss_attention call launches on each path (dfss_nm_attention, capi.cu)
-LAUNCHES = {"fused-16bit": 1, "fused-tf32": 2, "staged-tcgen05": 2, "staged-ffma": 2, "staged-masked": 3}
+LAUNCHES = {"fused-16bit": 1, "fused-tf32": 2, "staged-tcgen05": 2, "staged-ffma": 2, "staged-masked": 3,
+            "staged-3xtf32": 6}
 
 
 def roofline(cfg_name: str, path: str, ms: float, bh: int) -> dict:
@@ -280,6 +281,19 @@ def roofline(cfg_name: str, path: str, ms: float, bh: int) -> dict:
         stats = kernel_stats(cfg_name, "flash" if path == "fused-16bit" else "flashtf32")
         peak_tensor = (f"MEASURED_PEAKS.json bf16_tflops ({src})" if path == "fused-16bit" else
                        f"MEASURED_PEAKS.json bf16_tflops / 2 for tf32 ({src})")
+    elif path == "staged-3xtf32":
+        # scores (3 tf32 passes of QK^T), in-place softmax, SpMM (3 sparse tf32 passes); bytes: the
+        # nonzeros written, softmaxed in place (read + write), read by the SpMM, metadata written /
+        # read, and Q / K / V read and split into hi / lo, O written
+        nz = n * (n // 2) * eb
+        meta = n * (n // 2) // 2
+        nbytes = (4 * nz + 2 * meta + 16 * n * d * eb) * bh
+        flops = 3.0 * 3.0 * n * n * d * bh
+        tf = tf_bf16 / 2
+        floors = {"hbm": nbytes / (hbm * 1e9), "tensor": flops / (tf * 1e12)}
+        kname = "sddmm12_tf32x3_kernel + softmax + spmm12_tf32x3_kernel (staged 3xTF32)"
+        stats = {}
+        peak_tensor = f"MEASURED_PEAKS.json bf16_tflops / 2 for tf32 ({src})"
     else:
         gs = 2 if cfg["mode"] == "1:2" else 4
         nz = n * (n // 2) * eb
@@ -320,7 +334,7 @@ def run_dfss(args, cfg_name, ws, rank, local, device, report_extra=True, info=Tr
     bh = hi - lo
     mode = dfss.SparsityMode.parse(cfg["mode"])
     math_mode = cfg.get("math", "auto")
-    path = dfss.attention_path(mode, q.dtype, n, d, math_mode)
+    path = dfss.attention_path(mode, q.dtype, n, d, math_mode, bh=max(bh, 1))
     ws_bytes = dfss.workspace_bytes(mode, q.dtype, max(bh, 1), n, d, math_mode)
     workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
     out = torch.empty_like(q)

@@ -45,6 +45,7 @@ SIGNATURES = {
     "dfss_nm_attention_dump": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i64, _i32, _i32, _vp, _i32, _i32, _vp,
                                       _i64, _vp, _vp, _vp, _vp]),
     "dfss_nm_attention_path": (_i32, [_i32, _i32, _i32, _i32, _i32, _i32, _i32, _i32]),
+    "dfss_nm_attention_path_bh": (_i32, [_i32, _i32, _i32, _i64, _i32, _i32, _i32, _i32, _i32]),
     "dfss_prune_scores": (_i32, [_vp, _vp, _vp, _vp, _i32, _i32, _i64, _i32, _vp]),
     "dfss_prune_scores_f64": (_i32, [_vp, _vp, _vp, _vp, _i32, _i64, _i32, _vp]),
     "dfss_meta_hw_to_logical": (_i32, [_vp, _vp, _i32, _i64, _i32, _i32, _vp]),

@@ -126,9 +126,16 @@ int dfss_spmm(const void* p, const uint32_t* meta_hw, const void* v, void* out, 
 }
 
 // exact-FP32 attention (math auto) with the SpMM on tcgen05 as 3xTF32: 1:2, d = 64, n % 128 == 0
-static bool exact_f32_on_tc(int mode, int dtype, int math, int n, int d) {
-  return math == DFSS_MATH_AUTO && dtype == DFSS_F32 && mode == 2 && dfss::tc_spmm_tf32x3_supported(2, n, n, d) &&
+// -- from ~8 M scores up: below, its six launches cost more than the FFMA pair saves (c1,
+// 12 x 384^2: 0.038 vs 0.029 ms; 96 x 384^2: 0.080 vs 0.159 ms)
+static bool exact_f32_on_tc(int mode, int dtype, int math, int64_t bh, int n, int d) {
+  return math == DFSS_MATH_AUTO && dtype == DFSS_F32 && mode == 2 && bh * (int64_t)n * n >= (8 << 20) &&
+         dfss::tc_spmm_tf32x3_supported(2, n, n, d) && dfss::tc_sddmm_tf32x3_supported(2, n, n, d) &&
          dfss_has_tcgen05();
+}
+// its workspace beyond the staged buffers: V^T hi / lo (SpMM), then Q / K hi / lo (SDDMM)
+static int64_t exact_f32_tc_extra_bytes(int64_t bh, int n) {
+  return dfss::spmm_tf32x3_workspace_bytes(bh, n) + dfss::sddmm_tf32x3_workspace_bytes(bh, n, n);
 }
 
 int64_t dfss_nm_attention_workspace_bytes_for(int mode, int dtype, int math, int64_t bh, int n, int d,
@@ -143,8 +150,8 @@ int64_t dfss_nm_attention_workspace_bytes_for(int mode, int dtype, int math, int
       (!masked || (mask_ok && dfss::flash_mask_two_set_ok(n))) && dfss_has_tcgen05())
     return dfss::flash_tf32_workspace_bytes(bh, n, masked);  // V^T (K-major tf32 B) + mask bitmaps
   const int64_t staged = dfss_nm_attention_workspace_bytes(mode, dtype, bh, n, d);
-  if (!masked && exact_f32_on_tc(mode, dtype, math, n, d))
-    return staged + dfss::spmm_tf32x3_workspace_bytes(bh, n);  // + V^T hi / lo of the 3xTF32 SpMM
+  if (!masked && exact_f32_on_tc(mode, dtype, math, bh, n, d))
+    return staged + exact_f32_tc_extra_bytes(bh, n);  // + the 3xTF32 kernels' split operands
   return staged;
 }
 
@@ -166,10 +173,10 @@ int dfss_nm_attention(const void* q, const void* k, const void* v, void* out, in
 
 namespace {
 
-enum Path { kFused16 = 1, kFusedTf32 = 2, kStagedTc = 3, kStagedFfma = 4, kStagedMasked = 5 };
+enum Path { kFused16 = 1, kFusedTf32 = 2, kStagedTc = 3, kStagedFfma = 4, kStagedMasked = 5, kStaged3xTf32 = 6 };
 
 // The path dfss_nm_attention(_masked) takes (no launch).  Validation is the caller's.
-int attention_path(int mode, int dtype, int math, int n, int d, bool masked, int tile_rows, int tile_cols) {
+int attention_path(int mode, int dtype, int math, int64_t bh, int n, int d, bool masked, int tile_rows, int tile_cols) {
   const bool tc = dfss_has_tcgen05() != 0;
   if (math == DFSS_MATH_AUTO && dtype != DFSS_F32 && dfss::tc_flash_supported(mode, dtype, n, d) &&
       (!masked || dfss::tc_flash_mask_supported(tile_rows, tile_cols)) && tc)
@@ -182,6 +189,7 @@ int attention_path(int mode, int dtype, int math, int n, int d, bool masked, int
   if (math == DFSS_MATH_AUTO && dtype != DFSS_F32 && dfss::tc_sddmm_supported(mode, dtype, dtype, n, n, d) &&
       dfss::tc_spmm_supported(mode, dtype, dtype, dtype, n, n, d) && tc)
     return kStagedTc;
+  if (exact_f32_on_tc(mode, dtype, math, bh, n, d)) return kStaged3xTf32;
   return kStagedFfma;
 }
 
@@ -197,7 +205,7 @@ int nm_attention_impl(const void* q, const void* k, const void* v, void* out, in
   const int64_t need =
       dfss_nm_attention_workspace_bytes_for(mode, dtype, math, bh, n, d, tile_rows, tile_cols, tile_keep != nullptr);
   if (need > 0 && (!workspace || workspace_bytes < need)) return fail(DFSS_ERR_INVALID, "workspace too small");
-  const int path = attention_path(mode, dtype, math, n, d, tile_keep != nullptr, tile_rows, tile_cols);
+  const int path = attention_path(mode, dtype, math, bh, n, d, tile_keep != nullptr, tile_rows, tile_cols);
   if (path < 0) return fail(DFSS_ERR_UNSUPPORTED, "tf32 attention needs fp32 inputs, mode 1:2, d = 64 and n % 128 == 0");
   const bool dumping = dump_s != nullptr;
   if (dumping && !dump_meta) return fail(DFSS_ERR_INVALID, "dump needs both score and metadata buffers");
@@ -240,6 +248,19 @@ int nm_attention_impl(const void* q, const void* k, const void* v, void* out, in
     return dfss_spmm(nz, meta, v, out, mode, dtype, dtype, dtype, bh, n, n, d, tile_keep, tile_rows, tile_cols,
                      nullptr, stream);
   }
+  const int64_t staged_bytes = dfss_nm_attention_workspace_bytes(mode, dtype, bh, n, d);
+  if (path == kStaged3xTf32) {  // (its workspace was checked above: dfss_nm_attention_workspace_bytes_for)
+    // exact FP32 (math auto) on tcgen05 as 3xTF32: scores + 1:2 prune (sddmm_tf32.cu), row softmax in
+    // place, SpMM (spmm_tf32.cu); fp32-accurate, selection bit-exact on the dumped scores
+    char* x3 = ws + staged_bytes;
+    int st = cuda_status(dfss::launch_sddmm_tf32x3((const float*)q, (const float*)k, (float*)nz, meta, scale, bh, n, n,
+                                                   dump_s, x3 + dfss::spmm_tf32x3_workspace_bytes(bh, n), s));
+    if (!st && dumping) st = cuda_status(cudaMemcpyAsync(dump_meta, meta, meta_bytes, cudaMemcpyDeviceToDevice, s));
+    if (st) return st;
+    st = dfss_softmax_rows(nz, nz, dtype, dtype, bh, n, n / 2, nullptr, 0, 0, nullptr, stream);
+    if (st) return st;
+    return cuda_status(dfss::launch_spmm_tf32x3((const float*)nz, meta, (const float*)v, (float*)out, bh, n, n, x3, s));
+  }
   // SDDMM+prune (+row max) -> SpMM with the softmax applied to the staged P tiles
   const bool fused = path == kStagedTc;
   int st = dfss_sddmm_prune(q, k, nz, meta, scale, mode, dtype, dtype, math, bh, n, n, d, nullptr, 0, 0, dump_s,
@@ -248,15 +269,6 @@ int nm_attention_impl(const void* q, const void* k, const void* v, void* out, in
   if (st) return st;
   if (fused)
     return dfss_spmm(nz, meta, v, out, mode, dtype, dtype, dtype, bh, n, n, d, nullptr, 0, 0, row_max, stream);
-  if (dtype == DFSS_F32 && exact_f32_on_tc(mode, dtype, math, n, d) &&
-      workspace_bytes >= dfss_nm_attention_workspace_bytes(mode, dtype, bh, n, d) + dfss::spmm_tf32x3_workspace_bytes(bh, n)) {
-    // exact FP32 (math auto): row softmax in place, then the SpMM on tcgen05 as 3xTF32 (spmm_tf32.cu:
-    // the selection is already fixed by the FFMA SDDMM; ~2^-21 relative error per product)
-    st = dfss_softmax_rows(nz, nz, dtype, dtype, bh, n, n / 2, nullptr, 0, 0, nullptr, stream);
-    if (st) return st;
-    return cuda_status(dfss::launch_spmm_tf32x3((const float*)nz, meta, (const float*)v, (float*)out, bh, n, n,
-                                                ws + dfss_nm_attention_workspace_bytes(mode, dtype, bh, n, d), s));
-  }
   if (dtype == DFSS_F32 && d <= 64)  // exact FP32: softmax fused into the SIMT SpMM (one pass less)
     return cuda_status(dfss::launch_spmm_simt_softmax_f32(nz, meta, v, out, mode, bh, n, n, d, s));
   st = dfss_softmax_rows(nz, nz, dtype, dtype, bh, n, n / 2, nullptr, 0, 0, nullptr, stream);
@@ -285,8 +297,13 @@ int dfss_nm_attention_dump(const void* q, const void* k, const void* v, void* ou
 }
 
 int dfss_nm_attention_path(int mode, int dtype, int math, int n, int d, int tile_rows, int tile_cols, int masked) {
-  if (!valid_mode(mode) || !valid_dtype(dtype) || n < 1 || d < 1) return DFSS_ERR_INVALID;
-  return attention_path(mode, dtype, math, n, d, masked != 0, tile_rows, tile_cols);
+  return dfss_nm_attention_path_bh(mode, dtype, math, 1, n, d, tile_rows, tile_cols, masked);
+}
+
+int dfss_nm_attention_path_bh(int mode, int dtype, int math, int64_t bh, int n, int d, int tile_rows, int tile_cols,
+                              int masked) {
+  if (!valid_mode(mode) || !valid_dtype(dtype) || bh < 0 || n < 1 || d < 1) return DFSS_ERR_INVALID;
+  return attention_path(mode, dtype, math, bh, n, d, masked != 0, tile_rows, tile_cols);
 }
 
 int dfss_prune_scores(const float* scores, void* nonzeros, uint8_t* meta_logical, uint8_t* kept, int mode,

@@ -217,6 +217,11 @@ struct TileMask;
 // two pre-kernels that build them on stream s
 void prepare_mask_bits(TileMask& m, int n, void* workspace, cudaStream_t s);
 bool tc_spmm_supported(int gs, int p_dtype, int v_dtype, int out_dtype, int rows, int n_k, int d);
+// fp32 1:2 fused score + prune at fp32 accuracy on tcgen05 (3xTF32, sddmm_tf32.cu); workspace: Q / K hi / lo
+bool tc_sddmm_tf32x3_supported(int gs, int n, int m, int d);
+int64_t sddmm_tf32x3_workspace_bytes(int64_t bh, int n, int m);
+cudaError_t launch_sddmm_tf32x3(const float* q, const float* k, float* nz, uint32_t* meta, float scale, int64_t bh,
+                                int n, int m, float* dbg, void* workspace, cudaStream_t s);
 // fp32 1:2 SpMM at fp32 accuracy on tcgen05 (3xTF32, spmm_tf32.cu); workspace: V^T hi / lo
 bool tc_spmm_tf32x3_supported(int gs, int rows, int n_k, int d);
 int64_t spmm_tf32x3_workspace_bytes(int64_t bh, int n_k);

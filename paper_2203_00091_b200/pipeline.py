@@ -128,16 +128,18 @@ _CALL_CACHE: dict = {}
 
 
 #: dfss_nm_attention_path ids (include/dfss.h)
-PATHS = {1: "fused-16bit", 2: "fused-tf32", 3: "staged-tcgen05", 4: "staged-ffma", 5: "staged-masked"}
+PATHS = {1: "fused-16bit", 2: "fused-tf32", 3: "staged-tcgen05", 4: "staged-ffma", 5: "staged-masked",
+         6: "staged-3xtf32"}
 
 
 def attention_path(mode, dtype: torch.dtype, n: int, d: int, math_mode: str = "auto",
-                   block_mask: BlockMask | None = None) -> str:
-    """Name of the kernel path dfss_attention takes for these arguments (no launch)."""
+                   block_mask: BlockMask | None = None, bh: int = 1) -> str:
+    """Name of the kernel path dfss_attention takes for these arguments (no launch); ``bh`` is the
+    flattened batch x heads count (the exact-FP32 3xTF32 path is chosen from ~8 M scores)."""
     mode = as_mode(mode)
     tr, tc_ = (block_mask.tile_rows, block_mask.tile_cols) if block_mask is not None else (0, 0)
-    pid = int(_lib.load().dfss_nm_attention_path(mode.group_size, _lib.dtype_id(dtype), _MATH[math_mode], n, d, tr,
-                                                 tc_, int(block_mask is not None)))
+    pid = int(_lib.load().dfss_nm_attention_path_bh(mode.group_size, _lib.dtype_id(dtype), _MATH[math_mode], int(bh), n,
+                                                    d, tr, tc_, int(block_mask is not None)))
     if pid < 0:
         _lib.check(pid, "attention path")
     return PATHS[pid]
@@ -205,7 +207,7 @@ def dfss_attention_dump(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, mode=
         logical = pairs.reshape(bh, n, n // 2).to(torch.uint8)
     shape = tuple(q.shape[:-2])
     return AttentionDump(out, scores.reshape(shape + (n, n)), logical.reshape(shape + (n, n // mode.group_size)),
-                         attention_path(mode, q.dtype, n, d, math_mode, block_mask))
+                         attention_path(mode, q.dtype, n, d, math_mode, block_mask, bh))
 
 
 _HOST_STREAMS: dict[int, tuple[torch.cuda.Stream, torch.cuda.Stream, torch.cuda.Stream]] = {}

@@ -953,25 +953,23 @@ def test_block_mask_fuzz_many_items(case):
                      f"fuzz case {case}: n={n} tiles={tr}x{tc_} density={density} style={style} head {h}")
 
 
-@pytest.mark.parametrize("shape", [(1, 12, 384), (2, 8, 1024), (1, 160, 512), (1, 2, 4096)])
-def test_exact_fp32_3xtf32_spmm_matches_reference(shape):
-    """Exact-FP32 1:2 attention with math "auto": FFMA SDDMM + selection, in-place row softmax,
-    the SpMM on tcgen05 as 3xTF32 (spmm_tf32.cu) -- at the 1e-5 bar against the reference in
-    float64 (first and last heads; 160 heads: several row blocks per CTA), and within 5e-6 of
-    the explicit "ffma" mode (pure FFMA SpMM) everywhere."""
+@pytest.mark.parametrize("shape", [(1, 64, 384), (2, 8, 1024), (1, 160, 512), (1, 2, 4096)])
+def test_exact_fp32_3xtf32_matches_reference(shape):
+    """Exact-FP32 1:2 attention with math "auto" on tcgen05 as 3xTF32: scores + selection
+    (sddmm_tf32.cu), in-place row softmax, SpMM (spmm_tf32.cu).  Against the reference in float64
+    at the 1e-5 bar (first and last heads, n <= 1024; 160 heads: several row blocks per CTA), and
+    against the pure-FFMA mode ("ffma") everywhere within 5e-6 -- except rows whose selection
+    differs at a near tie between the two fp32-accurate score computations (<= 1e-3 of the rows)."""
     b, h, n = shape
     (q, k, v), (q64, k64, v64) = seeded_qkv((b, h, n, 64), torch.float32, seed=n + h)
     out = _np(dfss.dfss_attention(q, k, v, "1:2"))
-    # both modes select on the same FFMA scores: any difference is the SpMM's arithmetic (both
-    # fp32-accurate; their accumulation orders differ over up to 2048 terms)
-    ffma = _np(dfss.dfss_attention(q, k, v, "1:2", math_mode="ffma"))
-    assert_close(out, ffma, 5e-6, 5e-6, f"3xtf32 vs ffma {shape}")
-    # against the float64 reference on a few heads up to n = 1024 (more rows meet fp32-vs-fp64
-    # near-tie selection flips -- one row at n = 4096 -- which both modes share)
     for hh in (sorted({0, h - 1}) if n <= 1024 else []):
         sl = (slice(0, 1), slice(hh, hh + 1))
         assert_close(out[sl], oracle_attention(q64[sl], k64[sl], v64[sl], "1:2"), 1e-5, 1e-5,
-                     f"3xtf32 spmm {shape} h={hh}")
+                     f"3xtf32 {shape} h={hh}")
+    ffma = _np(dfss.dfss_attention(q, k, v, "1:2", math_mode="ffma"))
+    bad_rows = (np.abs(out - ffma) > 5e-6 + 5e-6 * np.abs(ffma)).any(axis=-1)
+    assert bad_rows.sum() <= max(2, int(1e-3 * bad_rows.size)), (int(bad_rows.sum()), bad_rows.size)
 
 
 @pytest.mark.parametrize("n,mode,heads", [(512, "1:2", 3), (1024, "1:2", 3), (640, "2:4", 3), (384, "1:2", 64)])

@@ -249,7 +249,8 @@ int nm_attention_impl(const void* q, const void* k, const void* v, void* out, in
                      nullptr, stream);
   }
   const int64_t staged_bytes = dfss_nm_attention_workspace_bytes(mode, dtype, bh, n, d);
-  if (path == kStaged3xTf32) {  // (its workspace was checked above: dfss_nm_attention_workspace_bytes_for)
+  const bool x3_aligned = (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)out) & 15) == 0;
+  if (path == kStaged3xTf32 && x3_aligned) {  // (workspace checked above; unaligned views: the FFMA pair)
     // exact FP32 (math auto) on tcgen05 as 3xTF32: scores + 1:2 prune (sddmm_tf32.cu), row softmax in
     // place, SpMM (spmm_tf32.cu); fp32-accurate, selection bit-exact on the dumped scores
     char* x3 = ws + staged_bytes;

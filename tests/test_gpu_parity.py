@@ -972,6 +972,22 @@ def test_exact_fp32_3xtf32_matches_reference(shape):
     assert bad_rows.sum() <= max(2, int(1e-3 * bad_rows.size)), (int(bad_rows.sum()), bad_rows.size)
 
 
+def test_exact_fp32_3xtf32_unaligned_views_fall_back():
+    """Views that are not 16-byte aligned take the FFMA pair instead of the 3xTF32 kernels (TMA /
+    vector loads need alignment): same result as the aligned call within fp32 accuracy."""
+    (q, k, v), _ = seeded_qkv((1, 64, 384, 64), torch.float32, seed=3)
+    flat = [torch.empty(x.numel() + 1, device="cuda") for x in (q, k, v)]
+    views = []
+    for f, x in zip(flat, (q, k, v)):
+        f[1:].copy_(x.reshape(-1))
+        views.append(f[1:].view(x.shape))  # 4-byte offset
+    assert views[0].data_ptr() % 16 != 0
+    want = _np(dfss.dfss_attention(q, k, v, "1:2"))
+    got = _np(dfss.dfss_attention(*views, "1:2"))
+    bad_rows = (np.abs(got - want) > 5e-6 + 5e-6 * np.abs(want)).any(axis=-1)
+    assert bad_rows.sum() <= 2
+
+
 @pytest.mark.parametrize("n,mode,heads", [(512, "1:2", 3), (1024, "1:2", 3), (640, "2:4", 3), (384, "1:2", 64)])
 def test_exact_fp32_longer_rows_match_reference(n, mode, heads):
     """Exact-FP32 path at the 1e-5 bar where the shared-memory-tiled SpMM runs (n >= 512, or

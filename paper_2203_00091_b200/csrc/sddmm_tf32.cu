@@ -4,7 +4,7 @@
 //
 // The exact-FP32 attention path (nm_attention on fp32 inputs, math "auto", 1e-5 bar).  The
 // dropped Ql Kl^T term and the rounding of the split parts leave the scores within a few fp32
-// ulps of the FFMA scores (tools/x3 check in DESIGN §4.2: same maximum error against float64
+// ulps of the FFMA scores (tools/x3_accuracy.py, profiles/x3_accuracy.txt: same maximum error against float64
 // as FFMA on the c1 inputs); the selection is bit-exact on the scores this kernel computes
 // (the dump hook writes them), as for every other SDDMM here (codec.py:104-123: element 1 of a
 // pair survives iff v1 > v0, ties to the lower index).  The explicit "ffma" math mode keeps

@@ -40,10 +40,13 @@ __global__ void __launch_bounds__(256, std::is_same<TIn, float>::value ? 4 : 2) 
                                                          float scale, int n, int m, int d,
                                                          const uint8_t* __restrict__ keep, int tile_rows,
                                                          int tile_cols, float* __restrict__ dbg, MetaGeom geo,
-                                                         uint32_t two, int vec4) {
+                                                         uint32_t two, int vec4, int pdl) {
   __shared__ __align__(16) float Qs[BK][BM + 4];
   __shared__ __align__(16) float Ks[BK][BN + 4];
   __shared__ uint8_t nibs[BM][BN / GS];
+  // a programmatic dependent (the exact-FP32 SpMM) may start launching now; it waits for this
+  // grid's completion before reading its results (griddepcontrol.wait)
+  if (pdl) asm volatile("griddepcontrol.launch_dependents;");
 
   const int b = blockIdx.z;
   const int row0 = blockIdx.y * BM, col0 = blockIdx.x * BN;
@@ -195,12 +198,15 @@ static cudaError_t sddmm_simt_typed(const void* q, const void* k, void* nz, uint
     float* db = dbg ? dbg + b0 * n * m : nullptr;
     dim3 grid((m + BN - 1) / BN, 2 * geo.rblocks, (unsigned)nb);
     const int vec4 = d % 4 == 0 && ((uintptr_t)qb | (uintptr_t)kb) % (4 * sizeof(TIn)) == 0;
+    // early dependent launch only when this grid is a single wave (4 CTAs per SM): dependents
+    // would otherwise take the slots of this grid's later CTAs
+    const int pdl = (int64_t)grid.x * grid.y * grid.z <= 4 * 148;
     if (gs == 4)
       sddmm_simt_kernel<TIn, TNz, 4><<<grid, 256, 0, s>>>(qb, kb, nzb, mb, scale, n, m, d, keep, tile_rows, tile_cols,
-                                                          db, geo, 2u, vec4);
+                                                          db, geo, 2u, vec4, pdl);
     else
       sddmm_simt_kernel<TIn, TNz, 2><<<grid, 256, 0, s>>>(qb, kb, nzb, mb, scale, n, m, d, keep, tile_rows, tile_cols,
-                                                          db, geo, 2u, vec4);
+                                                          db, geo, 2u, vec4, pdl);
   }
   return cudaGetLastError();
 }

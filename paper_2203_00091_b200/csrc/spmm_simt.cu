@@ -255,6 +255,8 @@ __global__ void __launch_bounds__(256) spmm_simt_softmax_d64_kernel(const float*
                                                                     float* __restrict__ out, int64_t total_rows,
                                                                     int rows, int n_k, MetaGeom geo) {
   constexpr float kLog2e = 1.4426950408889634f;
+  // launched as a programmatic dependent of the SDDMM (see the launch): wait for its results
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31, hl = lane & 15, part = lane >> 4;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -459,16 +461,26 @@ cudaError_t launch_spmm_simt_softmax_f32(const void* p, const uint32_t* meta, co
     const int64_t total = bh * rows;
     int64_t blocks = (total + 7) / 8;  // one row per warp
     if (blocks > 148 * 64) blocks = 148 * 64;
-    const int nk = n_k;
+    // programmatic dependent launch: the kernel's launch overlaps the SDDMM's tail (it waits
+    // for the SDDMM's results with griddepcontrol.wait) -- c1 is launch-latency-bound
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const float* pf = (const float*)p;
+    const float* vf = (const float*)v;
+    float* of = (float*)out;
+    const int64_t tr = total;
     if (gs == 4)
-      spmm_simt_softmax_d64_kernel<4><<<(int)blocks, 256, 0, s>>>((const float*)p, meta, (const float*)v,
-                                                                    (float*)out, total, rows, nk,
-                                                                    MetaGeom(rows, n_k / 4));
-    else
-      spmm_simt_softmax_d64_kernel<2><<<(int)blocks, 256, 0, s>>>((const float*)p, meta, (const float*)v,
-                                                                    (float*)out, total, rows, nk,
-                                                                    MetaGeom(rows, n_k / 2));
-    return cudaGetLastError();
+      return cudaLaunchKernelEx(&cfg, spmm_simt_softmax_d64_kernel<4>, pf, meta, vf, of, tr, rows, n_k,
+                                MetaGeom(rows, n_k / 4));
+    return cudaLaunchKernelEx(&cfg, spmm_simt_softmax_d64_kernel<2>, pf, meta, vf, of, tr, rows, n_k,
+                              MetaGeom(rows, n_k / 2));
   }
   const int64_t total = bh * rows;
   int64_t blocks = (total + 7) / 8;

@@ -126,10 +126,11 @@ int dfss_spmm(const void* p, const uint32_t* meta_hw, const void* v, void* out, 
 }
 
 // exact-FP32 attention (math auto) with the SpMM on tcgen05 as 3xTF32: 1:2, d = 64, n % 128 == 0
-// -- from ~8 M scores up: below, its six launches cost more than the FFMA pair saves (c1,
-// 12 x 384^2: 0.038 vs 0.029 ms; 96 x 384^2: 0.080 vs 0.159 ms)
+// -- from ~2.6 M scores (bh * n^2) up: below, its six launches cost more than the FFMA pair saves
+// (tools/time_f32_sizes.py: c1, 12 x 384^2 = 1.8 M: 0.039 vs 0.028 ms; 24 x 384^2 = 3.5 M: 0.041 vs
+// 0.048 ms; 12 x 512^2: 0.042 vs 0.057 ms; 96 x 384^2: 0.078 vs 0.156 ms)
 static bool exact_f32_on_tc(int mode, int dtype, int math, int64_t bh, int n, int d) {
-  return math == DFSS_MATH_AUTO && dtype == DFSS_F32 && mode == 2 && bh * (int64_t)n * n >= (8 << 20) &&
+  return math == DFSS_MATH_AUTO && dtype == DFSS_F32 && mode == 2 && bh * (int64_t)n * n >= (5 << 19) &&
          dfss::tc_spmm_tf32x3_supported(2, n, n, d) && dfss::tc_sddmm_tf32x3_supported(2, n, n, d) &&
          dfss_has_tcgen05();
 }

@@ -252,7 +252,7 @@ def kernel_stats(cfg_name: str, key: str) -> dict:
 
 #: kernels one dfss_attention call launches on each path (dfss_nm_attention, capi.cu)
 LAUNCHES = {"fused-16bit": 1, "fused-tf32": 2, "staged-tcgen05": 2, "staged-ffma": 2, "staged-masked": 3,
-            "staged-3xtf32": 6}
+            "staged-3xtf32": 5}
 
 
 def roofline(cfg_name: str, path: str, ms: float, bh: int) -> dict:
@@ -282,16 +282,16 @@ def roofline(cfg_name: str, path: str, ms: float, bh: int) -> dict:
         peak_tensor = (f"MEASURED_PEAKS.json bf16_tflops ({src})" if path == "fused-16bit" else
                        f"MEASURED_PEAKS.json bf16_tflops / 2 for tf32 ({src})")
     elif path == "staged-3xtf32":
-        # scores (3 tf32 passes of QK^T), in-place softmax, SpMM (3 sparse tf32 passes); bytes: the
-        # nonzeros written, softmaxed in place (read + write), read by the SpMM, metadata written /
-        # read, and Q / K / V read and split into hi / lo, O written
+        # scores (3 tf32 passes of QK^T) + row maxima, SpMM with the softmax fused (3 sparse tf32
+        # passes); bytes: the nonzeros written and read once, metadata written / read, and Q / K / V
+        # read and split into hi / lo, O written
         nz = n * (n // 2) * eb
         meta = n * (n // 2) // 2
-        nbytes = (4 * nz + 2 * meta + 16 * n * d * eb) * bh
+        nbytes = (2 * nz + 2 * meta + 16 * n * d * eb) * bh
         flops = 3.0 * 3.0 * n * n * d * bh
         tf = tf_bf16 / 2
         floors = {"hbm": nbytes / (hbm * 1e9), "tensor": flops / (tf * 1e12)}
-        kname = "sddmm12_tf32x3_kernel + softmax + spmm12_tf32x3_kernel (staged 3xTF32)"
+        kname = "sddmm12_tf32x3_kernel + spmm12_tf32x3_kernel (staged 3xTF32, softmax fused)"
         stats = {}
         peak_tensor = f"MEASURED_PEAKS.json bf16_tflops / 2 for tf32 ({src})"
     else:

@@ -126,11 +126,14 @@ int dfss_spmm(const void* p, const uint32_t* meta_hw, const void* v, void* out, 
 }
 
 // exact-FP32 attention (math auto) with the SpMM on tcgen05 as 3xTF32: 1:2, d = 64, n % 128 == 0
-// -- from ~2.6 M scores (bh * n^2) up: below, its six launches cost more than the FFMA pair saves
+// -- from ~2.6 M scores (bh * n^2) up: below, its five launches cost more than the FFMA pair saves
 // (tools/time_f32_sizes.py: c1, 12 x 384^2 = 1.8 M: 0.039 vs 0.028 ms; 24 x 384^2 = 3.5 M: 0.041 vs
 // 0.048 ms; 12 x 512^2: 0.042 vs 0.057 ms; 96 x 384^2: 0.078 vs 0.156 ms)
+#ifndef DFSS_X3_MIN_SCORES
+#define DFSS_X3_MIN_SCORES (5 << 19)
+#endif
 static bool exact_f32_on_tc(int mode, int dtype, int math, int64_t bh, int n, int d) {
-  return math == DFSS_MATH_AUTO && dtype == DFSS_F32 && mode == 2 && bh * (int64_t)n * n >= (5 << 19) &&
+  return math == DFSS_MATH_AUTO && dtype == DFSS_F32 && mode == 2 && bh * (int64_t)n * n >= DFSS_X3_MIN_SCORES &&
          dfss::tc_spmm_tf32x3_supported(2, n, n, d) && dfss::tc_sddmm_tf32x3_supported(2, n, n, d) &&
          dfss_has_tcgen05();
 }
@@ -252,16 +255,16 @@ int nm_attention_impl(const void* q, const void* k, const void* v, void* out, in
   const int64_t staged_bytes = dfss_nm_attention_workspace_bytes(mode, dtype, bh, n, d);
   const bool x3_aligned = (((uintptr_t)q | (uintptr_t)k | (uintptr_t)v | (uintptr_t)out) & 15) == 0;
   if (path == kStaged3xTf32 && x3_aligned) {  // (workspace checked above; unaligned views: the FFMA pair)
-    // exact FP32 (math auto) on tcgen05 as 3xTF32: scores + 1:2 prune (sddmm_tf32.cu), row softmax in
-    // place, SpMM (spmm_tf32.cu); fp32-accurate, selection bit-exact on the dumped scores
+    // exact FP32 (math auto) on tcgen05 as 3xTF32: scores + 1:2 prune + row maxima (sddmm_tf32.cu), SpMM
+    // with the row softmax fused (spmm_tf32.cu); fp32-accurate, selection bit-exact on the dumped scores
     char* x3 = ws + staged_bytes;
     int st = cuda_status(dfss::launch_sddmm_tf32x3((const float*)q, (const float*)k, (float*)nz, meta, scale, bh, n, n,
-                                                   dump_s, x3 + dfss::spmm_tf32x3_workspace_bytes(bh, n), s));
+                                                   dump_s, row_max, x3 + dfss::spmm_tf32x3_workspace_bytes(bh, n), s));
     if (!st && dumping) st = cuda_status(cudaMemcpyAsync(dump_meta, meta, meta_bytes, cudaMemcpyDeviceToDevice, s));
     if (st) return st;
-    st = dfss_softmax_rows(nz, nz, dtype, dtype, bh, n, n / 2, nullptr, 0, 0, nullptr, stream);
-    if (st) return st;
-    return cuda_status(dfss::launch_spmm_tf32x3((const float*)nz, meta, (const float*)v, (float*)out, bh, n, n, x3, s));
+    // the row softmax fused into the SpMM: exp of (score - the SDDMM's row maximum), row sums divided out
+    return cuda_status(
+        dfss::launch_spmm_tf32x3((const float*)nz, meta, (const float*)v, (float*)out, bh, n, n, row_max, x3, s));
   }
   // SDDMM+prune (+row max) -> SpMM with the softmax applied to the staged P tiles
   const bool fused = path == kStagedTc;

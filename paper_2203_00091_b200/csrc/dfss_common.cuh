@@ -221,12 +221,12 @@ bool tc_spmm_supported(int gs, int p_dtype, int v_dtype, int out_dtype, int rows
 bool tc_sddmm_tf32x3_supported(int gs, int n, int m, int d);
 int64_t sddmm_tf32x3_workspace_bytes(int64_t bh, int n, int m);
 cudaError_t launch_sddmm_tf32x3(const float* q, const float* k, float* nz, uint32_t* meta, float scale, int64_t bh,
-                                int n, int m, float* dbg, void* workspace, cudaStream_t s);
+                                int n, int m, float* dbg, float* rowmax, void* workspace, cudaStream_t s);
 // fp32 1:2 SpMM at fp32 accuracy on tcgen05 (3xTF32, spmm_tf32.cu); workspace: V^T hi / lo
 bool tc_spmm_tf32x3_supported(int gs, int rows, int n_k, int d);
 int64_t spmm_tf32x3_workspace_bytes(int64_t bh, int n_k);
 cudaError_t launch_spmm_tf32x3(const float* p, const uint32_t* meta, const float* v, float* out, int64_t bh, int rows,
-                               int n_k, void* workspace, cudaStream_t s);
+                               int n_k, const float* rowmax, void* workspace, cudaStream_t s);
 // fused 1:2 attention on fp32 inputs with tf32 tensor cores (flash_tf32.cu), n % 256 == 0, d = 64
 bool tc_flash_tf32_supported(int gs, int n, int d);
 // vt_scratch: flash_tf32_workspace_bytes of device scratch -- V^T (the kind::tf32 B operand

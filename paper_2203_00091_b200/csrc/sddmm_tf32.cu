@@ -19,6 +19,8 @@
 //   warps 4-11   epilogue: warp (quad, half) prunes rows 32 quad.. x columns 64 half.. of the
 //                tile: scale, 1:2 selection, fp32 kept values and the meta_hw words (1:2: two
 //                per 32 columns, rows r / r^8 traded, include/dfss.h) straight to global.
+#include <math_constants.h>
+
 #include <algorithm>
 #include <type_traits>
 
@@ -74,7 +76,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     sddmm12_tf32x3_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_ql,
                           const __grid_constant__ CUtensorMap tm_kh, const __grid_constant__ CUtensorMap tm_kl,
                           float* __restrict__ nz, uint32_t* __restrict__ meta, float scale, int bh, int n, int m,
-                          float* __restrict__ dbg) {
+                          float* __restrict__ dbg, float* __restrict__ rowmax) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + SMEM_BAR);
@@ -191,6 +193,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int grow = mb * BM + row_blk;
       uint32_t* meta_b = meta + ((int64_t)b * mblocks + mb) * words * 128;
       float* nzrow = nz + ((int64_t)b * n + grow) * (m / 2);
+      float mx = -INFINITY;  // this row's maximum kept score over the warp's column half
       for (int t = 0; t < ntiles; ++t) {
         tc::mbar_wait_sleep(&t_full[acc], aph);
         tc::tc_fence_after();
@@ -215,6 +218,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const float v1 = scale_canon(__uint_as_float(r[2 * pr + 1]), scale);
             if (DBG) *reinterpret_cast<float2*>(dbg + ((int64_t)b * n + grow) * m + col + 2 * pr) = make_float2(v0, v1);
             W[pr >> 3] |= select12(v0, v1, kept[pr]) << (4 * (pr & 7));
+            mx = fmaxf(mx, kept[pr]);
           }
           float4* dst = reinterpret_cast<float4*>(nzrow + col / 2);
 #pragma unroll
@@ -229,6 +233,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         if (++acc == NACC) { acc = 0; aph ^= 1; }
       }
+      // per-row partial maxima [bh, n, 4] (halves 0, 1; 2, 3 unused): the SpMM's fused softmax
+      rowmax[((int64_t)b * n + grow) * 4 + half] = mx;
+      rowmax[((int64_t)b * n + grow) * 4 + 2 + half] = -INFINITY;
     }
   }
   tc::tc_fence_before();
@@ -249,10 +256,10 @@ int64_t sddmm_tf32x3_workspace_bytes(int64_t bh, int n, int m) {
 }
 
 cudaError_t launch_sddmm_tf32x3(const float* q, const float* k, float* nz, uint32_t* meta, float scale, int64_t bh,
-                                int n, int m, float* dbg, void* workspace, cudaStream_t s) {
+                                int n, int m, float* dbg, float* rowmax, void* workspace, cudaStream_t s) {
   if (!tc_sddmm_tf32x3_supported(2, n, m, HD)) return cudaErrorNotSupported;
   if (bh == 0) return cudaSuccess;
-  if (!workspace || ((uintptr_t)q | (uintptr_t)k) % 16) return cudaErrorInvalidValue;
+  if (!workspace || !rowmax || ((uintptr_t)q | (uintptr_t)k) % 16) return cudaErrorInvalidValue;
   const auto al = [](int64_t x) { return (x + 255) / 256 * 256; };
   char* ws = (char*)workspace;
   float* qh = (float*)ws;
@@ -282,7 +289,7 @@ cudaError_t launch_sddmm_tf32x3(const float* q, const float* k, float* nz, uint3
   if (e != cudaSuccess) return e;
   const int64_t items = bh * (n / BM);
   const int grid = (int)(items < sms ? items : sms);
-  kern<<<grid, NTHREADS, SMEM_TOTAL, s>>>(tqh, tql, tkh, tkl, nz, meta, scale, (int)bh, n, m, dbg);
+  kern<<<grid, NTHREADS, SMEM_TOTAL, s>>>(tqh, tql, tkh, tkl, nz, meta, scale, (int)bh, n, m, dbg, rowmax);
   return cudaGetLastError();
 }
 

@@ -1,11 +1,12 @@
-// spmm_tf32.cu -- O = P_sparse . V for fp32 1:2 operands on the tensor cores at fp32 accuracy
-// (3xTF32: P = Ph + Pl, V = Vh + Vl with Xh = tf32(X), Xl = X - Xh; O += Ph Vh + Ph Vl + Pl Vh).
+// spmm_tf32.cu -- O = softmax_rows(P_sparse) . V for fp32 1:2 operands on the tensor cores at fp32
+// accuracy (3xTF32: E = Eh + El, V = Vh + Vl with Xh = tf32(X), Xl = X - Xh; O += Eh Vh + Eh Vl +
+// El Vh, E = exp(P - row max), O divided by the row sums at the end).
 //
-// The exact-FP32 attention path (nm_attention on fp32 inputs at the 1e-5 bar, c1 and the
-// configs[4] fp32 arm): the selection is made by the FFMA SDDMM on its exact fp32 scores, so the
-// tensor cores only see the fixed, already normalised weights; the dropped Pl Vl term and the
-// tf32 truncation of the low parts leave a relative error of ~2^-21 per product, far inside
-// 1e-5 (sparse_ops.py:40-68 / _kernels_numba.py:91-103 accumulate in float64).
+// The exact-FP32 attention path (nm_attention on fp32 inputs, math "auto", 1e-5 bar): the
+// selection is already made on the SDDMM's fp32-accurate scores (sddmm_tf32.cu, which also
+// records the row maxima), so the tensor cores only see fixed weights; the dropped El Vl term
+// and the tf32 truncation of the low parts leave a relative error of ~2^-21 per product, far
+// inside 1e-5 (sparse_ops.py:18-68 / _kernels_numba.py:66-103 compute in float64).
 //
 // tcgen05.mma.sp.kind::tf32 (M = 128, N = 64, K = 16 dense / 8 kept) with A and the metadata in
 // TMEM and B = V^T (kind::tf32 reads B only K-major, tools/tf32_probe.cu), as in the fused
@@ -16,9 +17,10 @@
 //                V^T hi / lo tiles (64 dims x 64 keys, two atoms each) per stage;
 //   warp 1       MMA issuer: per 16-key step three sparse MMAs (hi.hi, hi.lo, lo.hi);
 //   warp 2       TMEM allocator;
-//   warps 4-7    split: a lane's P row from shared memory -> tf32 hi / lo -> TMEM A columns,
-//                its meta_hw words -> TMEM metadata columns (two TMEM A stages);
-//   warps 8-11   epilogue: TMEM -> fp32 O rows.
+//   warps 4-7    softmax + split: a lane's P row from shared memory -> exp2(p log2e - row max)
+//                (row sum accumulated) -> tf32 hi / lo -> TMEM A columns, its meta_hw words ->
+//                TMEM metadata columns (two TMEM A stages); the row sum to the epilogue;
+//   warps 8-11   epilogue: TMEM -> fp32 O rows / row sum.
 // V^T hi / lo are produced once per call by vt_split_kernel into the workspace.
 #include <type_traits>
 
@@ -37,10 +39,12 @@ constexpr int P_BYTES = BM * (BKL / 2) * 4;  // 16 KB: one 128B-swizzle atom
 constexpr int VT_ATOM = HD * 128;            // 8 KB: 64 dims x 32 keys
 constexpr int VT_BYTES = 2 * VT_ATOM;        // 16 KB per part (hi / lo)
 constexpr int STAGE_BYTES = P_BYTES + 2 * VT_BYTES;
-constexpr int SMEM_BAR = STAGES * STAGE_BYTES;
+constexpr int SMEM_L = STAGES * STAGE_BYTES;  // [NACC][128] row sums of the fused softmax
+constexpr int SMEM_BAR = SMEM_L + NACC * BM * 4;
 constexpr int SMEM_TOTAL = SMEM_BAR + 256 + 1024;
 constexpr int T_A = NACC * HD;  // A stages start after the accumulators: [stage][part][chunk] x 32 cols
 constexpr int NTHREADS = 12 * 32;
+constexpr float kLog2e = 1.4426950408889634f;
 }  // namespace
 
 __device__ __forceinline__ void mma_sp_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t e_tmem,
@@ -61,7 +65,7 @@ __device__ __forceinline__ uint32_t tf32_rna(float x) {
 __global__ void __launch_bounds__(NTHREADS, 1)
     spmm12_tf32x3_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_vh,
                          const __grid_constant__ CUtensorMap tm_vl, const uint32_t* __restrict__ meta,
-                         float* __restrict__ out, int bh, int rows, int n_k) {
+                         float* __restrict__ out, int bh, int rows, int n_k, const float* __restrict__ rowmax) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + SMEM_BAR);
@@ -71,7 +75,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* a_empty = a_full + ASTAGES;    // [ASTAGES] MMAs reading that A stage retired
   uint64_t* d_full = a_empty + ASTAGES;    // [NACC]
   uint64_t* d_empty = d_full + NACC;       // [NACC] (4 epilogue warps)
-  uint32_t* tmem_slot = (uint32_t*)(d_empty + NACC);
+  uint64_t* l_full = d_empty + NACC;       // [NACC] row sums in smem (4 split warps)
+  uint32_t* tmem_slot = (uint32_t*)(l_full + NACC);
+  float* lsum = (float*)(smem + SMEM_L);
 
   const uint32_t warp = tc::warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -95,6 +101,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int i = 0; i < NACC; ++i) {
       tc::mbar_init(&d_full[i], 1);
       tc::mbar_init(&d_empty[i], 4);
+      tc::mbar_init(&l_full[i], 4);
     }
     tc::fence_barrier_init();
   }
@@ -168,11 +175,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int quad = warp & 3;
     const int r = quad * 32 + lane;  // row within the 128-row block == TMEM lane
     const uint32_t lane_base = tmem_base + ((uint32_t)(quad * 32) << 16);
-    int s = 0, as = 0;
-    uint32_t ph = 0, aph = 0;
+    int s = 0, as = 0, acc = 0;
+    uint32_t ph = 0, aph = 0, dph = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       const int b = item / rblocks, rb = item % rblocks;
       const uint32_t* mrow = meta + ((int64_t)b * rblocks + rb) * words * 128 + r;
+      // fused row softmax (sparse_ops.py:18-37): the SDDMM's row maximum, exp2 of the scaled
+      // difference per kept value, the row sum handed to the epilogue
+      const float4 mp = *reinterpret_cast<const float4*>(rowmax + ((int64_t)b * rows + rb * BM + r) * 4);
+      const float mb = fmaxf(fmaxf(mp.x, mp.y), fmaxf(mp.z, mp.w)) * kLog2e;
+      float l = 0.f;
       for (int kb = 0; kb < kblocks; ++kb) {
         uint32_t w[4];
 #pragma unroll
@@ -191,8 +203,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              hi[4 * u + e] = tf32_rna(xv[e]);
-              lo[4 * u + e] = __float_as_uint(xv[e] - __uint_as_float(hi[4 * u + e]));
+              const float p = exp2f(fmaf(xv[e], kLog2e, -mb));
+              l += p;
+              hi[4 * u + e] = tf32_rna(p);
+              lo[4 * u + e] = __float_as_uint(p - __uint_as_float(hi[4 * u + e]));
             }
           }
           tc::tmem_st_32x32b_x16(abase + c * 32 + 16, hi);
@@ -207,6 +221,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (++s == STAGES) { s = 0; ph ^= 1; }
         if (++as == ASTAGES) { as = 0; aph ^= 1; }
       }
+      // the row sum to the epilogue (buffer acc is free once its previous O was drained)
+      tc::mbar_wait_sleep(&d_empty[acc], dph ^ 1);
+      lsum[acc * BM + r] = l;
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&l_full[acc]);
+      if (++acc == NACC) { acc = 0; dph ^= 1; }
     }
   } else if (warp >= 8) {
     // ------------------------------------------------------------ epilogue
@@ -217,6 +237,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       const int b = item / rblocks, rb = item % rblocks;
       tc::mbar_wait_sleep(&d_full[acc], dph);
+      tc::mbar_wait_sleep(&l_full[acc], dph);
+      const float inv = 1.0f / lsum[acc * BM + r];
       tc::tc_fence_after();
       uint32_t r0[32], r1[32];
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * HD;
@@ -230,10 +252,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       float4* orow = reinterpret_cast<float4*>(out + ((int64_t)b * rows + rb * BM + r) * HD);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        orow[j] = make_float4(__uint_as_float(r0[4 * j]), __uint_as_float(r0[4 * j + 1]), __uint_as_float(r0[4 * j + 2]),
-                              __uint_as_float(r0[4 * j + 3]));
-        orow[8 + j] = make_float4(__uint_as_float(r1[4 * j]), __uint_as_float(r1[4 * j + 1]),
-                                  __uint_as_float(r1[4 * j + 2]), __uint_as_float(r1[4 * j + 3]));
+        orow[j] = make_float4(__uint_as_float(r0[4 * j]) * inv, __uint_as_float(r0[4 * j + 1]) * inv,
+                              __uint_as_float(r0[4 * j + 2]) * inv, __uint_as_float(r0[4 * j + 3]) * inv);
+        orow[8 + j] = make_float4(__uint_as_float(r1[4 * j]) * inv, __uint_as_float(r1[4 * j + 1]) * inv,
+                                  __uint_as_float(r1[4 * j + 2]) * inv, __uint_as_float(r1[4 * j + 3]) * inv);
       }
       if (++acc == NACC) { acc = 0; dph ^= 1; }
     }
@@ -274,10 +296,10 @@ bool tc_spmm_tf32x3_supported(int gs, int rows, int n_k, int d) {
 int64_t spmm_tf32x3_workspace_bytes(int64_t bh, int n_k) { return 2 * ((bh * (int64_t)n_k * HD * 4 + 255) / 256 * 256); }
 
 cudaError_t launch_spmm_tf32x3(const float* p, const uint32_t* meta, const float* v, float* out, int64_t bh, int rows,
-                               int n_k, void* workspace, cudaStream_t s) {
+                               int n_k, const float* rowmax, void* workspace, cudaStream_t s) {
   if (!tc_spmm_tf32x3_supported(2, rows, n_k, HD)) return cudaErrorNotSupported;
   if (bh == 0) return cudaSuccess;
-  if (!workspace) return cudaErrorInvalidValue;
+  if (!workspace || !rowmax) return cudaErrorInvalidValue;
   float* vth = (float*)workspace;
   float* vtl = (float*)((char*)workspace + spmm_tf32x3_workspace_bytes(bh, n_k) / 2);
   const CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
@@ -300,7 +322,7 @@ cudaError_t launch_spmm_tf32x3(const float* p, const uint32_t* meta, const float
   const int sms = device_sms(dev);
   const int64_t items = bh * (rows / BM);
   const int grid = (int)(items < sms ? items : sms);
-  spmm12_tf32x3_kernel<<<grid, NTHREADS, SMEM_TOTAL, s>>>(tp, th, tl, meta, out, (int)bh, rows, n_k);
+  spmm12_tf32x3_kernel<<<grid, NTHREADS, SMEM_TOTAL, s>>>(tp, th, tl, meta, out, (int)bh, rows, n_k, rowmax);
   return cudaGetLastError();
 }
 

@@ -35,7 +35,9 @@ constexpr int ATOM = BM * 128;           // 16 KB: 128 rows x 32 fp32
 constexpr int TILE = 2 * ATOM;           // 32 KB: 128 rows x 64 dims
 constexpr int KST = 2;
 constexpr int S_QH = 0, S_QL = TILE, S_K = 2 * TILE;  // K ring: [stage][hi, lo]
-constexpr int SMEM_BAR = S_K + KST * 2 * TILE;
+constexpr int STG_BYTES = 32 * 128;  // per epilogue warp: 32 rows x 32 kept fp32 (128B-swizzled rows)
+constexpr int S_STG = S_K + KST * 2 * TILE;
+constexpr int SMEM_BAR = S_STG + 8 * STG_BYTES;
 constexpr int SMEM_TOTAL = SMEM_BAR + 256 + 1024;
 constexpr int NACC = 2;
 constexpr int NTHREADS = 12 * 32;
@@ -75,7 +77,7 @@ template <bool DBG>
 __global__ void __launch_bounds__(NTHREADS, 1)
     sddmm12_tf32x3_kernel(const __grid_constant__ CUtensorMap tm_qh, const __grid_constant__ CUtensorMap tm_ql,
                           const __grid_constant__ CUtensorMap tm_kh, const __grid_constant__ CUtensorMap tm_kl,
-                          float* __restrict__ nz, uint32_t* __restrict__ meta, float scale, int bh, int n, int m,
+                          const __grid_constant__ CUtensorMap tm_nz, float* __restrict__ nz, uint32_t* __restrict__ meta, float scale, int bh, int n, int m,
                           float* __restrict__ dbg, float* __restrict__ rowmax) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -99,6 +101,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc::prefetch_tmap(&tm_ql);
     tc::prefetch_tmap(&tm_kh);
     tc::prefetch_tmap(&tm_kl);
+    tc::prefetch_tmap(&tm_nz);
     tc::mbar_init(q_full, 1);
     tc::mbar_init(q_empty, 1);
     for (int i = 0; i < KST; ++i) {
@@ -186,13 +189,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int half = ew >> 2;
     const int row_blk = quad * 32 + lane;
     const int words = m / 16;  // 1:2 meta_hw words per row-block lane
+    // kept values leave through a shared-memory staging tile and one TMA store per tile (direct
+    // 16-byte stores, one row per lane, kept L1 68 % busy for 113 us at n = 1024)
+    uint8_t* stg = smem + S_STG + ew * STG_BYTES;
     int acc = 0;
     uint32_t aph = 0;
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       const int b = item / mblocks, mb = item % mblocks;
       const int grow = mb * BM + row_blk;
       uint32_t* meta_b = meta + ((int64_t)b * mblocks + mb) * words * 128;
-      float* nzrow = nz + ((int64_t)b * n + grow) * (m / 2);
       float mx = -INFINITY;  // this row's maximum kept score over the warp's column half
       for (int t = 0; t < ntiles; ++t) {
         tc::mbar_wait_sleep(&t_full[acc], aph);
@@ -206,6 +211,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&t_empty[acc]);
+        if (lane == 0) tc::bulk_wait_read<0>();  // the previous tile's store has read the staging tile
+        __syncwarp();
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           const uint32_t(&r)[32] = cc ? rb : ra;
@@ -220,9 +227,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             W[pr >> 3] |= select12(v0, v1, kept[pr]) << (4 * (pr & 7));
             mx = fmaxf(mx, kept[pr]);
           }
-          float4* dst = reinterpret_cast<float4*>(nzrow + col / 2);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) dst[j] = make_float4(kept[4 * j], kept[4 * j + 1], kept[4 * j + 2], kept[4 * j + 3]);
+          for (int j = 0; j < 4; ++j)  // 16-byte unit 4 cc + j of this lane's 128-byte row, swizzled
+            *reinterpret_cast<float4*>(stg + lane * 128 + (((4 * cc + j) ^ (lane & 7)) << 4)) =
+                make_float4(kept[4 * j], kept[4 * j + 1], kept[4 * j + 2], kept[4 * j + 3]);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const uint32_t partner = __shfl_xor_sync(0xffffffffu, W[h], 8);
@@ -231,12 +239,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             meta_b[(int64_t)((col >> 4) + h) * 128 + row_blk] = word;
           }
         }
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          tc::tma_store_3d(&tm_nz, stg, (t * BN + half * 64) / 2, mb * BM + quad * 32, b);
+          tc::bulk_commit();
+        }
         if (++acc == NACC) { acc = 0; aph ^= 1; }
       }
       // per-row partial maxima [bh, n, 4] (halves 0, 1; 2, 3 unused): the SpMM's fused softmax
       rowmax[((int64_t)b * n + grow) * 4 + half] = mx;
       rowmax[((int64_t)b * n + grow) * 4 + 2 + half] = -INFINITY;
     }
+    if (lane == 0) tc::bulk_wait<0>();
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -273,7 +288,7 @@ cudaError_t launch_sddmm_tf32x3(const float* q, const float* k, float* nz, uint3
   split_tf32_kernel<<<(unsigned)std::min<int64_t>((nk4 + 255) / 256, sms * 8), 256, 0, s>>>((const float4*)k,
                                                                                           (float4*)kh, (float4*)kl, nk4);
   const CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-  CUtensorMap tqh, tql, tkh, tkl;
+  CUtensorMap tqh, tql, tkh, tkl, tnz;
   const uint64_t row = HD * 4;
   const uint64_t qdims[3] = {(uint64_t)HD, (uint64_t)n, (uint64_t)bh}, qstr[2] = {row, (uint64_t)n * row};
   const uint64_t kdims[3] = {(uint64_t)HD, (uint64_t)m, (uint64_t)bh}, kstr[2] = {row, (uint64_t)m * row};
@@ -283,13 +298,17 @@ cudaError_t launch_sddmm_tf32x3(const float* q, const float* k, float* nz, uint3
       !encode_tmap(&tkh, dt, 3, kh, kdims, kstr, box, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !encode_tmap(&tkl, dt, 3, kl, kdims, kstr, box, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
+  const uint64_t ndims[3] = {(uint64_t)m / 2, (uint64_t)n, (uint64_t)bh};
+  const uint64_t nstr[2] = {(uint64_t)m / 2 * 4, (uint64_t)n * (m / 2) * 4};
+  const uint32_t nbox[3] = {32, 32, 1};
+  if (!encode_tmap(&tnz, dt, 3, nz, ndims, nstr, nbox, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
   auto kern = dbg ? sddmm12_tf32x3_kernel<true> : sddmm12_tf32x3_kernel<false>;
   static std::atomic<uint64_t> attr[2];
   cudaError_t e = set_max_smem_once((const void*)kern, attr[dbg ? 1 : 0], current_device());
   if (e != cudaSuccess) return e;
   const int64_t items = bh * (n / BM);
   const int grid = (int)(items < sms ? items : sms);
-  kern<<<grid, NTHREADS, SMEM_TOTAL, s>>>(tqh, tql, tkh, tkl, nz, meta, scale, (int)bh, n, m, dbg, rowmax);
+  kern<<<grid, NTHREADS, SMEM_TOTAL, s>>>(tqh, tql, tkh, tkl, tnz, nz, meta, scale, (int)bh, n, m, dbg, rowmax);
   return cudaGetLastError();
 }
 

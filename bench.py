@@ -252,7 +252,7 @@ def kernel_stats(cfg_name: str, key: str) -> dict:
 
 #: kernels one dfss_attention call launches on each path (dfss_nm_attention, capi.cu)
 LAUNCHES = {"fused-16bit": 1, "fused-tf32": 2, "staged-tcgen05": 2, "staged-ffma": 2, "staged-masked": 3,
-            "staged-3xtf32": 5}
+            "staged-3xtf32": 4}
 
 
 def roofline(cfg_name: str, path: str, ms: float, bh: int) -> dict:

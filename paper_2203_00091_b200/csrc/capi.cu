@@ -126,7 +126,7 @@ int dfss_spmm(const void* p, const uint32_t* meta_hw, const void* v, void* out, 
 }
 
 // exact-FP32 attention (math auto) with the SpMM on tcgen05 as 3xTF32: 1:2, d = 64, n % 128 == 0
-// -- from ~2.6 M scores (bh * n^2) up: below, its five launches cost more than the FFMA pair saves
+// -- from ~2.6 M scores (bh * n^2) up: below, its four launches cost more than the FFMA pair saves
 // (tools/time_f32_sizes.py: c1, 12 x 384^2 = 1.8 M: 0.039 vs 0.028 ms; 24 x 384^2 = 3.5 M: 0.041 vs
 // 0.048 ms; 12 x 512^2: 0.042 vs 0.057 ms; 96 x 384^2: 0.078 vs 0.156 ms)
 #ifndef DFSS_X3_MIN_SCORES

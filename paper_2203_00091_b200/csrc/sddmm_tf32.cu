@@ -58,10 +58,17 @@ __device__ __forceinline__ float tf32_round(float x) {
   return __uint_as_float(y);
 }
 
-// x -> hi = tf32(x), lo = tf32(x - hi) (both with zero low mantissa bits)
-__global__ void __launch_bounds__(256) split_tf32_kernel(const float4* __restrict__ x, float4* __restrict__ hi,
-                                                         float4* __restrict__ lo, int64_t n4) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+// x -> hi = tf32(x), lo = tf32(x - hi) (both with zero low mantissa bits), for Q and K in one launch
+__global__ void __launch_bounds__(256) split_tf32_kernel(const float4* __restrict__ xa, float4* __restrict__ ha,
+                                                         float4* __restrict__ la, int64_t na,
+                                                         const float4* __restrict__ xb, float4* __restrict__ hb,
+                                                         float4* __restrict__ lb, int64_t nb) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < na + nb; j += (int64_t)gridDim.x * blockDim.x) {
+    const bool first = j < na;
+    const int64_t i = first ? j : j - na;
+    const float4* x = first ? xa : xb;
+    float4* hi = first ? ha : hb;
+    float4* lo = first ? la : lb;
     const float4 v = x[i];
     float4 h, l;
     h.x = tf32_round(v.x), l.x = tf32_round(v.x - h.x);
@@ -283,10 +290,8 @@ cudaError_t launch_sddmm_tf32x3(const float* q, const float* k, float* nz, uint3
   float* kl = (float*)(ws + 2 * al(bh * (int64_t)n * HD * 4) + al(bh * (int64_t)m * HD * 4));
   const int64_t nq4 = bh * (int64_t)n * HD / 4, nk4 = bh * (int64_t)m * HD / 4;
   const int sms = device_sms(current_device());
-  split_tf32_kernel<<<(unsigned)std::min<int64_t>((nq4 + 255) / 256, sms * 8), 256, 0, s>>>((const float4*)q,
-                                                                                          (float4*)qh, (float4*)ql, nq4);
-  split_tf32_kernel<<<(unsigned)std::min<int64_t>((nk4 + 255) / 256, sms * 8), 256, 0, s>>>((const float4*)k,
-                                                                                          (float4*)kh, (float4*)kl, nk4);
+  split_tf32_kernel<<<(unsigned)std::min<int64_t>((nq4 + nk4 + 255) / 256, sms * 8), 256, 0, s>>>(
+      (const float4*)q, (float4*)qh, (float4*)ql, nq4, (const float4*)k, (float4*)kh, (float4*)kl, nk4);
   const CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   CUtensorMap tqh, tql, tkh, tkl, tnz;
   const uint64_t row = HD * 4;

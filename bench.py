@@ -59,7 +59,7 @@ for _n in (384, 512, 768, 1024, 2048, 4096):
                                       desc=f"sweep 1:2 tf32 (fp32 inputs), batch 8, 12 heads, seq {_n}")
     if _n <= 1024:
         CONFIGS[f"c5_12f32_{_n}"] = dict(batch=8, heads=12, seq=_n, d=64, mode="1:2", dtype="float32",
-                                         desc=f"sweep 1:2 fp32 (fp32-accurate: 3xTF32 on tcgen05 from ~2.6 M scores, FFMA below), batch 8, 12 heads, seq {_n}")
+                                         desc=f"sweep 1:2 fp32 (fp32-accurate: 3xTF32 on tcgen05 from ~1 M scores, FFMA below), batch 8, 12 heads, seq {_n}")
 DT = {"float32": torch.float32, "bfloat16": torch.bfloat16, "float16": torch.float16}
 DTYPE_TAG = {"float32": "f32", "bfloat16": "bf16", "float16": "f16"}
 METRIC = "DFSS attention ms & speedup vs dense attention (seq 512–4096) on B200; TFLOPS"

@@ -186,7 +186,7 @@ int dfss_nm_attention_dump(const void* q, const void* k, const void* v, void* ou
 /* Which path dfss_nm_attention(_masked) takes for these arguments (no launch): 1 fused 16-bit
  * (flash_tc.cu), 2 fused tf32 (flash_tf32.cu), 3 staged tcgen05 SDDMM + softmax-fused SpMM,
  * 4 staged exact-FP32 FFMA, 5 staged with a block mask, 6 staged exact-FP32 on tcgen05 as
- * 3xTF32 (sddmm_tf32.cu / spmm_tf32.cu: fp32 1:2, math auto, from ~2.6 M scores = bh * n^2);
+ * 3xTF32 (sddmm_tf32.cu / spmm_tf32.cu: fp32 1:2, math auto, from ~1 M scores = bh * n^2);
  * a negative dfss_status if unsupported.  The _bh form takes the batch x heads count (the
  * 3xTF32 choice depends on it); the other assumes bh = 1. */
 int dfss_nm_attention_path(int mode, int dtype, int math, int n, int d, int tile_rows, int tile_cols, int masked);

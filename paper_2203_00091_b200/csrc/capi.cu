@@ -126,11 +126,11 @@ int dfss_spmm(const void* p, const uint32_t* meta_hw, const void* v, void* out, 
 }
 
 // exact-FP32 attention (math auto) with the SpMM on tcgen05 as 3xTF32: 1:2, d = 64, n % 128 == 0
-// -- from ~2.6 M scores (bh * n^2) up: below, its four launches cost more than the FFMA pair saves
-// (tools/time_f32_sizes.py: c1, 12 x 384^2 = 1.8 M: 0.039 vs 0.028 ms; 24 x 384^2 = 3.5 M: 0.041 vs
-// 0.048 ms; 12 x 512^2: 0.042 vs 0.057 ms; 96 x 384^2: 0.078 vs 0.156 ms)
+// -- from ~1 M scores (bh * n^2) up: its four launches run as a programmatic-dependent chain
+// (tools/time_f32_sizes.py / bench: c1, 12 x 384^2 = 1.8 M: 0.0275 vs 0.0375 ms with the FFMA pair;
+// 24 x 384^2: 0.026 vs 0.049 ms; 96 x 384^2: 0.066 vs 0.156 ms); tiny problems keep the pair
 #ifndef DFSS_X3_MIN_SCORES
-#define DFSS_X3_MIN_SCORES (5 << 19)
+#define DFSS_X3_MIN_SCORES (1 << 20)
 #endif
 static bool exact_f32_on_tc(int mode, int dtype, int math, int64_t bh, int n, int d) {
   return math == DFSS_MATH_AUTO && dtype == DFSS_F32 && mode == 2 && bh * (int64_t)n * n >= DFSS_X3_MIN_SCORES &&
@@ -258,8 +258,13 @@ int nm_attention_impl(const void* q, const void* k, const void* v, void* out, in
     // exact FP32 (math auto) on tcgen05 as 3xTF32: scores + 1:2 prune + row maxima (sddmm_tf32.cu), SpMM
     // with the row softmax fused (spmm_tf32.cu); fp32-accurate, selection bit-exact on the dumped scores
     char* x3 = ws + staged_bytes;
-    int st = cuda_status(dfss::launch_sddmm_tf32x3((const float*)q, (const float*)k, (float*)nz, meta, scale, bh, n, n,
-                                                   dump_s, row_max, x3 + dfss::spmm_tf32x3_workspace_bytes(bh, n), s));
+    char* x3_qk = x3 + dfss::spmm_tf32x3_workspace_bytes(bh, n);
+    // split Q / K, split V^T (alongside), SDDMM, SpMM: each a programmatic dependent of the last
+    int st = cuda_status(dfss::launch_split_tf32x3((const float*)q, (const float*)k, bh, n, n, x3_qk, s));
+    if (!st) st = cuda_status(dfss::launch_vt_split_tf32x3((const float*)v, bh, n, x3, s));
+    if (!st)
+      st = cuda_status(dfss::launch_sddmm_tf32x3((const float*)q, (const float*)k, (float*)nz, meta, scale, bh, n, n,
+                                                 dump_s, row_max, x3_qk, s));
     if (!st && dumping) st = cuda_status(cudaMemcpyAsync(dump_meta, meta, meta_bytes, cudaMemcpyDeviceToDevice, s));
     if (st) return st;
     // the row softmax fused into the SpMM: exp of (score - the SDDMM's row maximum), row sums divided out

@@ -222,6 +222,9 @@ bool tc_sddmm_tf32x3_supported(int gs, int n, int m, int d);
 int64_t sddmm_tf32x3_workspace_bytes(int64_t bh, int n, int m);
 cudaError_t launch_sddmm_tf32x3(const float* q, const float* k, float* nz, uint32_t* meta, float scale, int64_t bh,
                                 int n, int m, float* dbg, float* rowmax, void* workspace, cudaStream_t s);
+cudaError_t launch_split_tf32x3(const float* q, const float* k, int64_t bh, int n, int m, void* workspace,
+                                cudaStream_t s);
+cudaError_t launch_vt_split_tf32x3(const float* v, int64_t bh, int n_k, void* workspace, cudaStream_t s);
 // fp32 1:2 SpMM at fp32 accuracy on tcgen05 (3xTF32, spmm_tf32.cu); workspace: V^T hi / lo
 bool tc_spmm_tf32x3_supported(int gs, int rows, int n_k, int d);
 int64_t spmm_tf32x3_workspace_bytes(int64_t bh, int n_k);

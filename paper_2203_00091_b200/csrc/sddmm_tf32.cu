@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(256) split_tf32_kernel(const float4* __restric
                                                          float4* __restrict__ la, int64_t na,
                                                          const float4* __restrict__ xb, float4* __restrict__ hb,
                                                          float4* __restrict__ lb, int64_t nb) {
+  asm volatile("griddepcontrol.launch_dependents;");  // the V^T split (independent) may start now
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < na + nb; j += (int64_t)gridDim.x * blockDim.x) {
     const bool first = j < na;
     const int64_t i = first ? j : j - na;
@@ -126,6 +127,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // launched as a programmatic dependent of the operand splits: the prologue above overlapped
+  // them; their results are read from here on
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -288,10 +293,7 @@ cudaError_t launch_sddmm_tf32x3(const float* q, const float* k, float* nz, uint3
   float* ql = (float*)(ws + al(bh * (int64_t)n * HD * 4));
   float* kh = (float*)(ws + 2 * al(bh * (int64_t)n * HD * 4));
   float* kl = (float*)(ws + 2 * al(bh * (int64_t)n * HD * 4) + al(bh * (int64_t)m * HD * 4));
-  const int64_t nq4 = bh * (int64_t)n * HD / 4, nk4 = bh * (int64_t)m * HD / 4;
   const int sms = device_sms(current_device());
-  split_tf32_kernel<<<(unsigned)std::min<int64_t>((nq4 + nk4 + 255) / 256, sms * 8), 256, 0, s>>>(
-      (const float4*)q, (float4*)qh, (float4*)ql, nq4, (const float4*)k, (float4*)kh, (float4*)kl, nk4);
   const CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   CUtensorMap tqh, tql, tkh, tkl, tnz;
   const uint64_t row = HD * 4;
@@ -313,7 +315,35 @@ cudaError_t launch_sddmm_tf32x3(const float* q, const float* k, float* nz, uint3
   if (e != cudaSuccess) return e;
   const int64_t items = bh * (n / BM);
   const int grid = (int)(items < sms ? items : sms);
-  kern<<<grid, NTHREADS, SMEM_TOTAL, s>>>(tqh, tql, tkh, tkl, tnz, nz, meta, scale, (int)bh, n, m, dbg, rowmax);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = SMEM_TOTAL;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tqh, tql, tkh, tkl, tnz, nz, meta, scale, (int)bh, n, m, dbg, rowmax);
+}
+
+// Q, K -> tf32 hi / lo in the workspace (one launch; the first of the 3xTF32 chain: split, V^T
+// split, SDDMM, SpMM, each later one a programmatic dependent of the one before)
+cudaError_t launch_split_tf32x3(const float* q, const float* k, int64_t bh, int n, int m, void* workspace,
+                                cudaStream_t s) {
+  if (bh == 0) return cudaSuccess;
+  if (!workspace || ((uintptr_t)q | (uintptr_t)k) % 16) return cudaErrorInvalidValue;
+  const auto al = [](int64_t x) { return (x + 255) / 256 * 256; };
+  char* ws = (char*)workspace;
+  float* qh = (float*)ws;
+  float* ql = (float*)(ws + al(bh * (int64_t)n * HD * 4));
+  float* kh = (float*)(ws + 2 * al(bh * (int64_t)n * HD * 4));
+  float* kl = (float*)(ws + 2 * al(bh * (int64_t)n * HD * 4) + al(bh * (int64_t)m * HD * 4));
+  const int64_t nq4 = bh * (int64_t)n * HD / 4, nk4 = bh * (int64_t)m * HD / 4;
+  const int sms = device_sms(current_device());
+  split_tf32_kernel<<<(unsigned)std::min<int64_t>((nq4 + nk4 + 255) / 256, sms * 8), 256, 0, s>>>(
+      (const float4*)q, (float4*)qh, (float4*)ql, nq4, (const float4*)k, (float4*)kh, (float4*)kl, nk4);
   return cudaGetLastError();
 }
 

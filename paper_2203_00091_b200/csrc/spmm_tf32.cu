@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent of the SDDMM
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 // V [bh][n][64] fp32 -> V^T hi / lo [bh][64][n] (hi = tf32(v) round-to-nearest, lo = v - hi)
 __global__ void __launch_bounds__(256) vt_split_kernel(const float* __restrict__ v, float* __restrict__ vth,
                                                        float* __restrict__ vtl, int n, int64_t bh) {
+  asm volatile("griddepcontrol.launch_dependents;");  // the SDDMM may launch (it waits on this grid)
   __shared__ float tile[32][HD + 1];
   const int k0 = blockIdx.x * 32;
   for (int64_t b = blockIdx.y; b < bh; b += gridDim.y) {
@@ -287,6 +289,9 @@ __global__ void __launch_bounds__(256) vt_split_kernel(const float* __restrict__
     }
     __syncthreads();
   }
+  // a programmatic dependent of the Q / K split: run alongside it (independent work), but finish
+  // only after it, so the SDDMM that waits on this grid sees both
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 bool tc_spmm_tf32x3_supported(int gs, int rows, int n_k, int d) {
@@ -314,7 +319,6 @@ cudaError_t launch_spmm_tf32x3(const float* p, const uint32_t* meta, const float
       !encode_tmap(&th, dt, 3, vth, vdims, vstr, vbox, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !encode_tmap(&tl, dt, 3, vtl, vdims, vstr, vbox, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
-  vt_split_kernel<<<dim3(n_k / 32, (unsigned)(bh < 65535 ? bh : 65535)), 256, 0, s>>>(v, vth, vtl, n_k, bh);
   const int dev = current_device();
   static std::atomic<uint64_t> attr{0};
   cudaError_t e = set_max_smem_once((const void*)spmm12_tf32x3_kernel, attr, dev);
@@ -322,8 +326,35 @@ cudaError_t launch_spmm_tf32x3(const float* p, const uint32_t* meta, const float
   const int sms = device_sms(dev);
   const int64_t items = bh * (rows / BM);
   const int grid = (int)(items < sms ? items : sms);
-  spmm12_tf32x3_kernel<<<grid, NTHREADS, SMEM_TOTAL, s>>>(tp, th, tl, meta, out, (int)bh, rows, n_k, rowmax);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = SMEM_TOTAL;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, spmm12_tf32x3_kernel, tp, th, tl, meta, out, (int)bh, rows, n_k, rowmax);
+}
+
+// V -> V^T hi / lo in the workspace, as a programmatic dependent of the Q / K split (see the kernel)
+cudaError_t launch_vt_split_tf32x3(const float* v, int64_t bh, int n_k, void* workspace, cudaStream_t s) {
+  if (bh == 0) return cudaSuccess;
+  if (!workspace) return cudaErrorInvalidValue;
+  float* vth = (float*)workspace;
+  float* vtl = (float*)((char*)workspace + spmm_tf32x3_workspace_bytes(bh, n_k) / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_k / 32, (unsigned)(bh < 65535 ? bh : 65535));
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, vt_split_kernel, v, vth, vtl, n_k, bh);
 }
 
 }  // namespace dfss

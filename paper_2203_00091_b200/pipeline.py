@@ -135,7 +135,7 @@ PATHS = {1: "fused-16bit", 2: "fused-tf32", 3: "staged-tcgen05", 4: "staged-ffma
 def attention_path(mode, dtype: torch.dtype, n: int, d: int, math_mode: str = "auto",
                    block_mask: BlockMask | None = None, bh: int = 1) -> str:
     """Name of the kernel path dfss_attention takes for these arguments (no launch); ``bh`` is the
-    flattened batch x heads count (the exact-FP32 3xTF32 path is chosen from ~2.6 M scores)."""
+    flattened batch x heads count (the exact-FP32 3xTF32 path is chosen from ~1 M scores)."""
     mode = as_mode(mode)
     tr, tc_ = (block_mask.tile_rows, block_mask.tile_cols) if block_mask is not None else (0, 0)
     pid = int(_lib.load().dfss_nm_attention_path_bh(mode.group_size, _lib.dtype_id(dtype), _MATH[math_mode], int(bh), n,

@@ -113,7 +113,10 @@ CASES = [
     ("1:2", torch.float32, "tf32", (1, 4, 512, 64), "zeros", "fused-tf32"),
     # staged paths through the same hook
     ("2:4", torch.float32, "auto", (1, 12, 384, 64), "normal", "staged-ffma"),        # c1-shaped (2:4 here)
-    ("1:2", torch.float32, "auto", (1, 12, 384, 64), "normal", "staged-ffma"),        # c1
+    ("1:2", torch.float32, "ffma", (1, 12, 384, 64), "normal", "staged-ffma"),        # c1, pure FFMA
+    ("1:2", torch.float32, "auto", (1, 12, 384, 64), "normal", "staged-3xtf32"),      # c1 (3xTF32 on tcgen05)
+    ("1:2", torch.float32, "auto", (1, 8, 512, 64), "lattice", "staged-3xtf32"),      # exact ties, 3xTF32
+    ("1:2", torch.float32, "auto", (1, 8, 512, 64), "zeros", "staged-3xtf32"),        # +-0 queries, 3xTF32
 ]
 
 
